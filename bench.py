@@ -1,0 +1,360 @@
+"""Benchmark: fine-grid DoF updates/s per adaFACx cycle (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload config2|config1|config4|config2-small|config4-small]
+
+A step is one additive cycle (ReferenceEngine.advance, solvers.py:334-399)
+over the resident level hierarchy.  Default workload: BASELINE configs[1]
+(2D adaFACx + BoxMG/Galerkin, depth 6, per-block log-uniform eps, seeded).
+
+* value      -- N_fine / t_cycle, device time (CUDA events on the engine's
+                stream, graph replay), L2 flushed (256 MiB write) before every
+                timed cycle; N_fine = composite DoFs of the finest level.
+* e2e        -- same metric through the drop-in API (GpuEngine, sync="eager"):
+                every step uploads tree.u (all levels, pinned host memory),
+                runs one cycle, downloads tree.u and the cycle's stats.
+* roofline   -- dominant kernel: algorithmic bytes per launch / mean launch
+                time (events around each launch, tmg_profile_cycles).
+* cpu_baseline -- the CPU oracle port (oracle/mg2d.py, numpy, 1 core) on a
+                bounded sample of the same workload.
+* --impl reference -- the reference's CPU algorithm (oracle port; the
+                reference is pure Python and cannot travel to the box) on the
+                same workload; rank 0 only.
+
+Multi-GPU: the 2D workloads do not shard (replicas only);
+under torchrun every rank runs an independent replica on its own GPU, timing
+is the max over ranks and value counts the DoFs of all replicas.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fine-grid DoF updates/s per adaFACx cycle (all levels); HBM GB/s vs roofline"
+UNIT = "DoF-updates/s"
+FLUSH_BYTES = 256 << 20
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Dist:
+    def __init__(self):
+        self.ws, self.rank, self.local = dist_env()
+        self.pg = None
+        if self.ws > 1:
+            import torch.distributed as td
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            td.init_process_group("gloo")
+            self.td = td
+
+    def barrier(self):
+        if self.ws > 1:
+            self.td.barrier()
+
+    def max(self, x: float) -> float:
+        if self.ws == 1:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64)
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.ws > 1:
+            self.td.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# algorithmic byte model, fp64 = 8 B
+
+def bytes_model(eng, wl):
+    """Per-launch algorithmic bytes of the fine-level kernels and the whole-cycle B_alg."""
+    L = wl.ltop
+    N = 3**L + 1
+    nv = N * N
+    ncell = (3**L) ** 2
+    boxmg = wl.flavor == "boxmg"
+    var_eps = True
+    # k_down_fine: read u, eps (per cell), rhs, diag, flags; write rho, rdof, g
+    down_fine = nv * (8 + 8 + 8 + 1) + ncell * 8 * var_eps + nv * 3 * 8
+    # k_up_fine: read g, flags, u; write u; coarse carry + P reads are 1/9-size
+    Nc = 3 ** (L - 1) + 1
+    up_fine = nv * (8 + 1 + 8 + 8) + Nc * Nc * 8 * (1 + (25 if boxmg else 0))
+    # whole-cycle B_alg: fine 24 (+8 eps) per DoF; coarse 48 (+8*9 op)
+    # + BoxMG P 8*24/9 per fine DoF of every level > lmin
+    counts = eng.level_counts()
+    fine_dofs = counts[L][0]
+    coarse = sum(counts[l][0] for l in range(eng.lmin, L))
+    b_alg = fine_dofs * (24 + 8 * var_eps) + coarse * (48 + (72 if boxmg else 8))
+    if boxmg:
+        b_alg += sum(counts[l][0] for l in range(eng.lmin + 1, L + 1)) * 8 * 24 / 9
+    return {"k_down_fine": down_fine, "k_up_fine": up_fine, "cycle": b_alg}
+
+
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"tmg_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sms.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, p[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": float(np.median(sms)) if sms else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def cpu_port_time(wl_name: str, cycles: int, budget_s: float = 20.0):
+    """Oracle (numpy restatement of the reference) on 1 core: seconds per cycle."""
+    from oracle import mg2d
+    from paper_1903_10367_b200 import workloads
+    wl = workloads.by_name(wl_name)
+    t = mg2d.Tree(lmin=wl.tree.lmin, lmax=wl.tree.lmax)
+    t.refined = [r.copy() for r in wl.tree.refined]
+    t.u = [u.copy() for u in wl.tree.u]
+    t.eps = [e.copy() for e in wl.tree.eps]
+    t0 = time.perf_counter()
+    eng = mg2d.Engine(t, mg2d.Config(variant=wl.variant, flavor=wl.flavor))
+    setup = time.perf_counter() - t0
+    eng.rhs.update(wl.rhs)
+    eng.advance()  # warm-up
+    done, t0 = 0, time.perf_counter()
+    while done < cycles:
+        eng.advance()
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = (time.perf_counter() - t0) / done
+    return dt, done, setup, wl
+
+
+def run_reference(args, dist: Dist):
+    if dist.rank != 0:
+        return
+    from oracle import mg2d
+    from paper_1903_10367_b200 import workloads
+    wl = workloads.by_name(args.workload)
+    n_fine = wl.fine_dofs()
+    # time K steps on one engine (each step = one cycle of the port)
+    t = mg2d.Tree(lmin=wl.tree.lmin, lmax=wl.tree.lmax)
+    t.refined = [r.copy() for r in wl.tree.refined]
+    t.u = [u.copy() for u in wl.tree.u]
+    t.eps = [e.copy() for e in wl.tree.eps]
+    eng = mg2d.Engine(t, mg2d.Config(variant=wl.variant, flavor=wl.flavor))
+    eng.rhs.update(wl.rhs)
+    for _ in range(args.warmup):
+        eng.advance()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        eng.advance()
+    total = time.perf_counter() - t0
+    v = n_fine * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, SURVEY.md §8(d))",
+        "config": {"workload": wl.name, "levels": f"{wl.tree.lmin}..{wl.ltop}",
+                   "variant": wl.variant, "flavor": wl.flavor, "n_fine": n_fine},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"{args.steps} cycles of {wl.name} after {args.warmup} warm-up; "
+                                   "oracle/mg2d.py (numpy restatement of treemg, bit-identical "
+                                   "iterates), single thread"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, dist: Dist):
+    import torch
+
+    from paper_1903_10367_b200 import GpuEngine, SolverConfig, workloads
+    from paper_1903_10367_b200 import build as b
+
+    if dist.rank == 0:
+        b.build()
+    dist.barrier()
+    dev = dist.local if dist.ws > 1 else 0
+    torch.cuda.set_device(dev)
+    wl = workloads.by_name(args.workload)
+    n_fine = wl.fine_dofs()
+
+    # ---- device-resident timing (value) ------------------------------------
+    eng = GpuEngine(wl.tree, SolverConfig(variant=wl.variant, flavor=wl.flavor), device=dev,
+                    sync="lazy")
+    eng.rhs.update(wl.rhs)
+    eng.advance_many(max(args.warmup, 3))
+    launches = eng.launches_per_cycle()
+    updates = eng.advance_many(1)[0].updates  # count_updates (solvers.py:449-459)
+    clk = ClockSampler(dev)
+    clk.start()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ms = eng.time_cycles(args.steps, flush_bytes=FLUSH_BYTES)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = clk.stop()
+    ms_warm = eng.time_cycles(args.steps, flush_bytes=0)
+    ms_max = dist.max(ms)
+    ms_step = ms_max / args.steps
+    value = dist.ws * n_fine / (ms_step * 1e-3)
+
+    # ---- per-kernel times (roofline of the dominant kernel) --------------------
+    prof = eng.profile_cycles(max(args.steps, 5))
+    bm = bytes_model(eng, wl)
+    top = max(prof.items(), key=lambda kv: kv[1][0])
+    kname, (kms, kcnt) = top
+    total_prof = sum(v[0] for v in prof.values())
+    peak = None
+    peak_src = "fallback 6650 GB/s (B200_PROFILING.md)"
+    try:
+        peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+        peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except (OSError, KeyError, ValueError):
+        peak = 6650.0
+    kbytes = bm.get(kname)
+    achieved = kbytes / (kms / kcnt * 1e-3) / 1e9 if kbytes else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.workload, {}).get(kname)
+        except ValueError:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if achieved else None, "traffic": traffic,
+                "algorithmic_bytes_per_launch": kbytes, "mean_launch_us": 1e3 * kms / kcnt,
+                "share_of_cycle": kms / total_prof, "peak_source": peak_src,
+                "cycle_B_alg": bm["cycle"],
+                "cycle_achieved_GBps": bm["cycle"] / (ms_step * 1e-3) / 1e9,
+                "cycle_frac": bm["cycle"] / (ms_step * 1e-3) / 1e9 / peak}
+    eng.close()
+
+    # ---- end to end through the drop-in API -------------------------------------
+    wl2 = workloads.by_name(args.workload)
+    tree = wl2.tree
+    for l in range(len(tree.u)):  # pinned host memory for tree.u
+        pin = torch.empty(tree.u[l].shape, dtype=torch.float64, pin_memory=True).numpy()
+        pin[...] = tree.u[l]
+        tree.u[l] = pin
+    e2 = GpuEngine(tree, SolverConfig(variant=wl2.variant, flavor=wl2.flavor), device=dev,
+                   sync="eager")
+    e2.rhs.update(wl2.rhs)
+    for _ in range(max(args.warmup, 3)):
+        e2.push()
+        e2.advance()
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2.push()          # H2D: every level of tree.u
+        e2.advance()       # one cycle + D2H of every level of tree.u and the stats
+    torch.cuda.synchronize()
+    t_e2e = dist.max(time.perf_counter() - t0)
+    h2d = sum(tree.u[l].nbytes for l in range(e2.lmin - 1, e2.ltop + 1))
+    d2h = sum(tree.u[l].nbytes for l in range(e2.lmin, e2.ltop + 1)) + 32
+    e2e = {"value": dist.ws * n_fine * args.steps / t_e2e, "unit": UNIT,
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "ms_per_step": 1e3 * t_e2e / args.steps, "api": "GpuEngine(sync='eager').push()+advance()"}
+    e2.close()
+
+    # ---- CPU baseline (rank 0 at N=1 only) ---------------------------------------
+    cpu = None
+    if dist.rank == 0 and dist.ws == 1 and not args.no_cpu:
+        dt, done, setup, _ = cpu_port_time(args.workload, 400, budget_s=args.cpu_budget)
+        cpu = {"value": n_fine / dt, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"{done} cycles of {wl.name} (after 1 warm-up) in "
+                         f"{dt * done:.1f} s; oracle/mg2d.py numpy restatement, 1 thread; "
+                         f"setup {setup:.2f} s"}
+
+    if dist.rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, SURVEY.md §8(d))",
+            "config": {"workload": wl.name, "levels": f"{wl.tree.lmin}..{wl.ltop}",
+                       "variant": wl.variant, "flavor": wl.flavor, "n_fine": n_fine,
+                       "parallelism": "replicas" if dist.ws > 1 else "single",
+                       "l2": f"flushed ({FLUSH_BYTES >> 20} MiB write) before every timed cycle",
+                       "ms_per_step_l2_warm": ms_warm / args.steps,
+                       "total_updates_per_s": dist.ws * updates / (ms_step * 1e-3)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": launches * args.steps,
+            "kernel_ms": {k: round(v[0] / v[1], 6) for k, v in prof.items()},
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--workload", default="config2")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            run_reference(args, dist)
+        else:
+            run_ours(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,153 @@
+/*
+ * tmg.h -- C ABI of the B200 additive-FAC / adaFACx engine (libtmg.so).
+ *
+ * Drop-in boundary for the hot path of the reference solver
+ * (/root/reference/pkg/src/treemg).  The reference has no FFI: its path sits
+ * behind the Python engine protocol of ``ReferenceEngine``
+ * (solvers.py:129-492).  Every entry point below replaces one method of that
+ * protocol; the Python mirror ``paper_1903_10367_b200.solvers.GpuEngine``
+ * binds them through ctypes.
+ *
+ * Conventions: plain pointers and sizes only.  A level l has n = 3^l cells
+ * per axis; vertex fields are (n+1)^2 fp64 and cell fields n^2, C-ordered
+ * [i][j] with i along x (spacetree.py:86-120).  All input arrays are copied;
+ * the handle owns every device buffer, its CUDA stream and graph.  There is
+ * no CPU fallback: without a CUDA device tmg_create fails with TMG_ECUDA.
+ *
+ * Status codes (mirroring the reference's exceptions):
+ *   TMG_OK          0
+ *   TMG_EINVAL      1  bad argument / config / unsupported   -> ValueError   (solvers.py:93-100,150,254)
+ *   TMG_EDEGENERATE 2  degenerate collapsed BoxMG stencil    -> ArithmeticError (operators.py:295-297)
+ *   TMG_ECUDA       3  CUDA runtime failure / no device      -> RuntimeError
+ * tmg_last_error() returns a thread-local message for the last failure.
+ */
+#ifndef TMG_H
+#define TMG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TMG_OK 0
+#define TMG_EINVAL 1
+#define TMG_EDEGENERATE 2
+#define TMG_ECUDA 3
+
+/* solver variants, solvers.py:70-78 */
+#define TMG_ADDITIVE 0
+#define TMG_ADDITIVE_EXP 1
+#define TMG_BPX 2
+#define TMG_AFACC 3
+#define TMG_ADAFAC_PI 4
+#define TMG_ADAFAC_JAC 5
+#define TMG_MULTIPLICATIVE_V10 6 /* not offered on the device: tmg_create -> TMG_EINVAL */
+
+/* operator flavours, solvers.py:95 */
+#define TMG_GEOMETRIC 0
+#define TMG_BOXMG 1
+
+/* tables readable with tmg_get_table */
+#define TMG_TABLE_A 0    /* ops[l] 3x3 stencil rows, (n+1)^2 x 9 (operators.py:201-202, 241-248) */
+#define TMG_TABLE_DIAG 1 /* ops[l].diag(), (n+1)^2 (operators.py:190-199, 241-242) */
+#define TMG_TABLE_P 2    /* transfers[l].p_table, (n+1)^2 x 7 x 7 (operators.py:306-437) */
+#define TMG_TABLE_RT 3   /* transfers[l].rtilde per-vertex, (n+1)^2 x 7 x 7 (operators.py:508-547) */
+#define TMG_TABLE_EFFEPS 4 /* eff_eps[l], n^2 (solvers.py:165-175) */
+
+typedef struct tmg_handle tmg_handle;
+
+/* SolverConfig, solvers.py:82-104 */
+typedef struct {
+  int32_t variant;
+  int32_t flavor;
+  double omega;
+  double omega_tilde; /* NaN = "None" -> omega (solvers.py:102-104) */
+  double omega_hat;
+  double damping_scale;
+  int32_t rtilde_true_operator;
+  int32_t device;
+} tmg_config;
+
+/* The spacetree data model, spacetree.py:86-120.  refined[l] for l < lmax
+ * ((3^l)^2 bytes, 0/1; a NULL entry means "no cell refined"); eps[l] and u[l]
+ * for l < nlevels (nlevels = len(tree.u) = depth + 1). */
+typedef struct {
+  int32_t lmin;
+  int32_t lmax;
+  int32_t nlevels;
+  const uint8_t* const* refined;
+  const double* const* eps;
+  const double* const* u;
+} tmg_tree;
+
+/* CycleStats, solvers.py:107-115 (level_dofs via tmg_level_counts) */
+typedef struct {
+  double l2h;
+  double linf;
+  int64_t dofs;
+  int64_t updates;
+} tmg_stats;
+
+/* ReferenceEngine.__init__ + rebuild(): solvers.py:137-141, 145-255.
+ * Classifies vertices, builds eff_eps, stencils, BoxMG P, Galerkin rows and
+ * R~ on the device and uploads u. */
+int tmg_create(const tmg_tree* tree, const tmg_config* cfg, tmg_handle** out);
+
+/* ReferenceEngine.rebuild() after a mesh / material change (solvers.py:145-255):
+ * rebuilds every operator from the new tree and re-uploads u. rhs is kept. */
+int tmg_rebuild(tmg_handle* h, const tmg_tree* tree);
+
+/* engine.rhs[level] = rhs (solvers.py:140, 305-309); rhs == NULL deletes it. */
+int tmg_set_rhs(tmg_handle* h, int32_t level, const double* rhs);
+
+/* tree.u[level][...] = u (host -> device) / u = tree.u[level] (device -> host). */
+int tmg_set_u(tmg_handle* h, int32_t level, const double* u);
+int tmg_get_u(tmg_handle* h, int32_t level, double* u);
+
+/* ReferenceEngine.update_fas_state(), solvers.py:280-296. */
+int tmg_update_fas_state(tmg_handle* h);
+
+/* ncycles x ReferenceEngine.advance(), solvers.py:334-399: stats[k] is the
+ * residual of the iterate cycle k started from.  stats may be NULL. */
+int tmg_cycle(tmg_handle* h, int32_t ncycles, tmg_stats* stats);
+
+/* ReferenceEngine.residual_stats(), solvers.py:461-482. */
+int tmg_residual_stats(tmg_handle* h, tmg_stats* out);
+
+/* ltop (solvers.py:148) and level range held by the handle. */
+int tmg_levels(tmg_handle* h, int32_t* lmin, int32_t* ltop);
+
+/* masks[l]["dof"].sum() and masks[l]["composite"].sum() (solvers.py:184-192, 443). */
+int tmg_level_counts(tmg_handle* h, int32_t level, int64_t* dof, int64_t* composite,
+                     int64_t* hanging);
+
+/* masks[l]["kinds"] (spacetree.py:164-191), int8 (n+1)^2. */
+int tmg_get_kinds(tmg_handle* h, int32_t level, int8_t* out);
+
+/* Operator tables (see TMG_TABLE_*) for tests and inspection. */
+int tmg_get_table(tmg_handle* h, int32_t which, int32_t level, double* out);
+
+/* Device timing of ncycles cycles (CUDA events on the handle's stream, inputs
+ * resident): total milliseconds.  flush_bytes > 0 writes a scratch buffer of
+ * that size (larger than L2) before every cycle, outside the timed events;
+ * flush_bytes == 0 times the cycles back to back.  Used by bench.py. */
+int tmg_time_cycles(tmg_handle* h, int32_t ncycles, int64_t flush_bytes, float* ms);
+
+/* Per-kernel device times over ncycles (events around every launch, no graph):
+ * names[k] (static strings), ms[k] summed, launches[k]; returns count via *nk. */
+int tmg_profile_cycles(tmg_handle* h, int32_t ncycles, int32_t cap, const char** names,
+                       float* ms, int32_t* launches, int32_t* nk);
+
+/* Kernel launches per cycle as issued by tmg_cycle. */
+int tmg_launches_per_cycle(tmg_handle* h, int32_t* n);
+
+void tmg_destroy(tmg_handle* h);
+const char* tmg_last_error(void);
+int tmg_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TMG_H */

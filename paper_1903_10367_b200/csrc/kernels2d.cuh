@@ -1,0 +1,93 @@
+// Kernel argument blocks and declarations of the 2D engine.
+#pragma once
+
+#include "tmg_kernels.cuh"
+
+namespace tmg {
+
+constexpr int kBlock = 256;
+
+enum Variant : int {
+  VAR_ADDITIVE = 0,
+  VAR_EXP = 1,
+  VAR_BPX = 2,
+  VAR_AFACC = 3,
+  VAR_PI = 4,
+  VAR_JAC = 5,
+  VAR_V10 = 6
+};
+
+struct DownArgs {
+  int N, is_top, variant, write;
+  const double* u;
+  const uint8_t* flags;
+  const double* diag;  // where(dof, op.diag(), 1)
+  OpView op;           // ops[l]
+  OpView rop;          // refined_ops[l] (OP_NONE when absent)
+  const double* rhs;   // engine.rhs[l] or nullptr
+  // finer level (restriction sources), valid when !is_top
+  int Nf;
+  const double* rho_f;
+  const double* rdof_f;
+  int boxmg;
+  const double* P;   // transfers[l] P planes (boxmg)
+  const double* Rt;  // transfers[l] R~ planes (RT_TABLE)
+  int rt_mode;
+  double rt_side, rt_mid, rt_scale;
+  // update parameters
+  double w_l, omega, wt, ds;
+  double hA, hB;  // hweight next to / away from refined cells
+  // outputs
+  double* rho;
+  double* rdof;
+  double* g;
+  double* part_sum;
+  double* part_max;
+};
+
+struct UpArgs {
+  int N, is_bottom, boxmg;
+  const uint8_t* flags;
+  double* u;
+  const double* g;
+  double* carry;
+  int Nc;
+  const double* carry_c;
+  const double* P;    // transfers[l-1] P planes (boxmg)
+  const double* inj;  // adafac-pi injected d on the coarse grid, or nullptr
+  double ds;
+};
+
+__global__ void k_flags(uint8_t* flags, int n, const uint8_t* ref_prev, const uint8_t* ref_cur);
+__global__ void k_take(uint8_t* flags_c, int Nc, const uint8_t* flags_f, int Nf);
+__global__ void k_eff(double* eff, double* epsm, double* reff, const double* eps,
+                      const double* eff_child, const uint8_t* ref_cur, const uint8_t* ref_prev, int n);
+__global__ void k_const_check(const double* arr, size_t n, int* flag);
+__global__ void k_count_kinds(const uint8_t* flags, size_t nv, unsigned long long* counts);
+__global__ void k_elem_diag(double* raw, double* diag, const double* eps, const uint8_t* flags, int n);
+__global__ void k_table_diag(double* raw, double* diag, const double* tbl, const uint8_t* flags,
+                             size_t nv);
+__global__ void k_assemble(double* tbl, const double* eps, int n);
+__global__ void k_gamma_x(double* ex, const double* tf, int nc, const uint8_t* ref,
+                          const uint8_t* ref_prev, int* deg);
+__global__ void k_gamma_y(double* ey, const double* tf, int nc, const uint8_t* ref,
+                          const uint8_t* ref_prev, int* deg);
+__global__ void k_p_init(double* P, int nc, const double* ex, const double* ey);
+__global__ void k_p_interior(double* P, int nc, const double* tf, const double* ex, const double* ey,
+                             const uint8_t* ref, const uint8_t* ref_prev);
+__global__ void k_p_fix(double* P, int nc, const uint8_t* flags_f);
+__global__ void k_rap(double* tbl, const uint8_t* flags_c, int nc, const double* tf,
+                      const uint8_t* flags_f, const double* P);
+__global__ void k_rtilde(double* Rt, int nc, const double* P, int pconst, const double* tf,
+                         const uint8_t* flags_f, const double* diag_f, double omega);
+__global__ void k_down(DownArgs a);
+__global__ void k_inject_d(double* inj, const uint8_t* flags_c, int Nc, const double* d, int Nf);
+__global__ void k_up(UpArgs a);
+__global__ void k_inject_u(double* uc, const uint8_t* flags_c, int Nc, const double* uf, int Nf);
+__global__ void k_hang(double* u, const uint8_t* flags, int N, const double* uc, int Nc);
+__global__ void k_finalize(const double* part_sum, const double* part_max, int nparts, double* hist,
+                           int* counter, int cap);
+
+void upload_constants(cudaStream_t s);
+
+}  // namespace tmg

@@ -1,0 +1,376 @@
+"""Drop-in GPU engine with the reference engine protocol.
+
+``GpuEngine(tree, cfg)`` mirrors ``treemg.solvers.ReferenceEngine``
+(``/root/reference/pkg/src/treemg/solvers.py:129-492``): same constructor,
+``rebuild()``, ``update_fas_state()``, ``advance() -> CycleStats``,
+``residual_stats()``, ``fine_solution()``, ``composite_solution()``, the
+``rhs`` dict hook and the ``ltop`` / ``masks`` attributes, with the same
+exceptions (ValueError / ArithmeticError).  All arithmetic runs in libtmg.so
+on the GPU; this module only moves arrays across the C ABI.
+
+State ownership.  The reference mutates ``tree.u[l]`` in place every cycle
+(solvers.py:395).  With ``sync="eager"`` (default) the engine does the same:
+after each ``advance()`` every level of ``tree.u`` is refreshed in place from
+the device.  With ``sync="lazy"`` the device copy is authoritative and
+``tree.u`` is refreshed only by ``pull()`` (or ``fine_solution()`` /
+``composite_solution()``); host edits to ``tree.u`` must then be preceded by
+``pull()`` and followed by ``update_fas_state()`` (which pushes them) or
+``push()``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+
+from . import _abi
+from .spacetree import VertexKind
+
+__all__ = ["VARIANTS", "DEVICE_VARIANTS", "PIPELINE_VARIANTS", "SolverConfig", "CycleStats",
+           "GpuEngine", "count_updates"]
+
+VARIANTS = ("additive", "additive-exp", "bpx", "afacc", "adafac-pi", "adafac-jac",
+            "multiplicative-v10")
+DEVICE_VARIANTS = VARIANTS[:6]
+PIPELINE_VARIANTS = ("additive", "adafac-pi", "adafac-jac")
+
+
+@dataclass
+class SolverConfig:
+    """solvers.py:82-104."""
+    variant: str = "adafac-jac"
+    flavor: str = "geometric"
+    omega: float = 0.6
+    omega_tilde: float | None = None
+    omega_hat: float = 0.7
+    rtilde_true_operator: bool = False
+    damping_scale: float = 1.0
+
+    def __post_init__(self):
+        if self.variant not in VARIANTS:
+            raise ValueError(f"unknown solver variant {self.variant!r}")
+        if self.flavor not in ("geometric", "boxmg"):
+            raise ValueError(f"unknown operator flavor {self.flavor!r}")
+        if not 0.0 < self.omega <= 1.0:
+            raise ValueError("omega must lie in (0, 1]")
+        if not 0.0 < self.omega_hat < 1.0:
+            raise ValueError("omega_hat must lie in (0, 1)")
+
+    @property
+    def wt(self) -> float:
+        return self.omega if self.omega_tilde is None else self.omega_tilde
+
+
+@dataclass
+class CycleStats:
+    """Residual of the iterate a cycle started from, plus work counts (solvers.py:107-115)."""
+    l2h: float
+    linf: float
+    dofs: int
+    updates: int
+    level_dofs: dict = dc_field(default_factory=dict)
+
+
+def count_updates(level_dofs: dict, variant: str, lmin: int, lmax: int) -> int:
+    """DoF updates of one cycle (bench.py:154-161)."""
+    total = sum(level_dofs[l] for l in range(lmin, lmax + 1))
+    if variant == "adafac-jac":
+        total += sum(level_dofs[l] for l in range(lmin, lmax))
+    elif variant == "adafac-pi":
+        total += sum(level_dofs[l] for l in range(lmin + 1, lmax + 1))
+    return total
+
+
+class _RhsDict(dict):
+    """engine.rhs (solvers.py:140): assignments / deletions are pushed lazily."""
+
+    def __init__(self, owner):
+        super().__init__()
+        self._dirty: set[int] = set()
+
+    def __setitem__(self, k, v):
+        super().__setitem__(int(k), v)
+        self._dirty.add(int(k))
+
+    def __delitem__(self, k):
+        super().__delitem__(int(k))
+        self._dirty.add(int(k))
+
+    def pop(self, k, *d):
+        self._dirty.add(int(k))
+        return super().pop(int(k), *d)
+
+    def clear(self):
+        self._dirty.update(self.keys())
+        super().clear()
+
+    def update(self, *a, **kw):
+        for k, v in dict(*a, **kw).items():
+            self[k] = v
+
+    def touch(self, k=None):
+        """Mark entries modified in place so the next cycle re-uploads them."""
+        self._dirty.update(self.keys() if k is None else [int(k)])
+
+
+class _TableView:
+    def __init__(self, eng, l):
+        self.eng, self.l = eng, l
+
+    def table(self) -> np.ndarray:
+        return self.eng._get_table(_abi.TABLE_A, self.l, (9,)).reshape(self.eng._nv_shape(self.l) + (3, 3))
+
+    def diag(self) -> np.ndarray:
+        return self.eng._get_table(_abi.TABLE_DIAG, self.l, ()).reshape(self.eng._nv_shape(self.l))
+
+    def stencil_at(self, i, j) -> np.ndarray:
+        return self.table()[i, j]
+
+
+class _TransferView:
+    def __init__(self, eng, l):
+        self.eng, self.l = eng, l
+
+    @property
+    def p_table(self):
+        if self.eng.cfg.flavor != "boxmg":
+            return None
+        return self.eng._get_table(_abi.TABLE_P, self.l, (49,)).reshape(self.eng._nv_shape(self.l) + (7, 7))
+
+    @property
+    def rtilde(self):
+        try:
+            return self.eng._get_table(_abi.TABLE_RT, self.l, (49,)).reshape(
+                self.eng._nv_shape(self.l) + (7, 7))
+        except ValueError:
+            return None
+
+
+class GpuEngine:
+    """B200 engine behind the ReferenceEngine protocol (solvers.py:129-492)."""
+
+    def __init__(self, tree, cfg: SolverConfig, device: int = 0, sync: str = "eager"):
+        if sync not in ("eager", "lazy"):
+            raise ValueError("sync must be 'eager' or 'lazy'")
+        if cfg.variant == "multiplicative-v10":
+            raise ValueError("multiplicative-v10 (the dense two-grid reference) is not offered "
+                             "by the device engine")
+        self.tree = tree
+        self.cfg = cfg
+        self.device = device
+        self.sync = sync
+        self.rhs = _RhsDict(self)
+        self._h = C.c_void_p()
+        self._host_stale = False
+        self._create()
+
+    # -- lifecycle ------------------------------------------------------------
+    def _cfg_struct(self) -> _abi.Config:
+        c = self.cfg
+        return _abi.Config(_abi.VARIANT_IDS[c.variant], _abi.FLAVOR_IDS[c.flavor], float(c.omega),
+                           math.nan if c.omega_tilde is None else float(c.omega_tilde),
+                           float(c.omega_hat), float(c.damping_scale),
+                           1 if c.rtilde_true_operator else 0, int(self.device))
+
+    def _create(self) -> None:
+        L = _abi.lib()
+        targs = _abi.TreeArgs(self.tree)
+        cs = self._cfg_struct()
+        _abi.check(L.tmg_create(C.byref(targs.struct), C.byref(cs), C.byref(self._h)))
+        self._after_build()
+
+    def _after_build(self) -> None:
+        L = _abi.lib()
+        lmin, ltop = C.c_int32(), C.c_int32()
+        _abi.check(L.tmg_levels(self._h, C.byref(lmin), C.byref(ltop)))
+        self.lmin, self.ltop = lmin.value, ltop.value
+        self._level_dofs = {}
+        self._composite = {}
+        self._hanging = {}
+        for l in range(self.lmin, self.ltop + 1):
+            d, c, hg = C.c_int64(), C.c_int64(), C.c_int64()
+            _abi.check(L.tmg_level_counts(self._h, l, C.byref(d), C.byref(c), C.byref(hg)))
+            self._level_dofs[l], self._composite[l], self._hanging[l] = d.value, c.value, hg.value
+        self._masks = None
+        self.rhs.touch()
+        self._host_stale = False
+        self.ops = {l: _TableView(self, l) for l in range(self.lmin, self.ltop + 1)}
+        self.transfers = {l: _TransferView(self, l) for l in range(self.lmin, self.ltop)}
+
+    def close(self) -> None:
+        if self._h:
+            _abi.lib().tmg_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def rebuild(self) -> None:
+        """(Re)build stencils, transfers and masks from the tree (solvers.py:145-255)."""
+        targs = _abi.TreeArgs(self.tree)
+        _abi.check(_abi.lib().tmg_rebuild(self._h, C.byref(targs.struct)))
+        self._after_build()
+
+    # -- host <-> device state ---------------------------------------------------
+    def push(self) -> None:
+        """Upload every level of tree.u (host authoritative)."""
+        L = _abi.lib()
+        for l in range(self.lmin - 1, self.ltop + 1):
+            a = np.ascontiguousarray(self.tree.u[l], dtype=np.float64)
+            _abi.check(L.tmg_set_u(self._h, l, _abi.ptr(a)))
+        self._host_stale = False
+
+    def pull(self) -> None:
+        """Refresh tree.u in place from the device."""
+        L = _abi.lib()
+        for l in range(self.lmin, self.ltop + 1):
+            u = self.tree.u[l]
+            if u.flags.c_contiguous and u.dtype == np.float64:
+                _abi.check(L.tmg_get_u(self._h, l, _abi.ptr(u)))
+            else:
+                tmp = np.empty(u.shape)
+                _abi.check(L.tmg_get_u(self._h, l, _abi.ptr(tmp)))
+                u[...] = tmp
+        self._host_stale = False
+
+    def _flush_rhs(self) -> None:
+        if not self.rhs._dirty:
+            return
+        L = _abi.lib()
+        for l in sorted(self.rhs._dirty):
+            if not self.lmin <= l <= self.ltop:
+                continue
+            if l in self.rhs:
+                a = np.ascontiguousarray(self.rhs[l], dtype=np.float64)
+                if a.shape != self.tree.u[l].shape:
+                    raise ValueError(f"rhs[{l}] has shape {a.shape}, expected {self.tree.u[l].shape}")
+                _abi.check(L.tmg_set_rhs(self._h, l, _abi.ptr(a)))
+            else:
+                _abi.check(L.tmg_set_rhs(self._h, l, None))
+        self.rhs._dirty.clear()
+
+    # -- protocol -------------------------------------------------------------------
+    def update_fas_state(self) -> None:
+        """Injection bottom-up, then hanging interpolation top-down (solvers.py:280-296)."""
+        if not self._host_stale:
+            self.push()
+        _abi.check(_abi.lib().tmg_update_fas_state(self._h))
+        if self.sync == "eager":
+            self.pull()
+        else:
+            self._host_stale = True
+
+    def _stats(self, s: _abi.Stats) -> CycleStats:
+        return CycleStats(s.l2h, s.linf, int(s.dofs), int(s.updates), dict(self._level_dofs))
+
+    def advance(self) -> CycleStats:
+        """One cycle; returns the residual of the starting iterate (solvers.py:334-399)."""
+        return self.advance_many(1)[0]
+
+    def advance_many(self, n: int) -> list[CycleStats]:
+        """n cycles back to back on the device, one host synchronisation."""
+        self._flush_rhs()
+        out = (_abi.Stats * max(n, 1))()
+        _abi.check(_abi.lib().tmg_cycle(self._h, n, out))
+        if self.sync == "eager":
+            self.pull()
+        else:
+            self._host_stale = True
+        return [self._stats(out[k]) for k in range(n)]
+
+    def residual_stats(self) -> CycleStats:
+        """Residual of the current iterate without advancing it (solvers.py:461-482)."""
+        self._flush_rhs()
+        s = _abi.Stats()
+        _abi.check(_abi.lib().tmg_residual_stats(self._h, C.byref(s)))
+        return self._stats(s)
+
+    def fine_solution(self) -> np.ndarray:
+        if self._host_stale:
+            self.pull()
+        return self.tree.u[self.ltop]
+
+    def composite_solution(self) -> dict:
+        if self._host_stale:
+            self.pull()
+        return {l: np.where(self.masks[l]["composite"], self.tree.u[l], 0.0)
+                for l in range(self.lmin, self.ltop + 1)}
+
+    @property
+    def masks(self) -> dict:
+        """masks[l] as in solvers.py:184-192, from the device classification."""
+        if self._masks is None:
+            self._masks = {}
+            for l in range(self.lmin, self.ltop + 1):
+                k = self.kinds(l)
+                dof = (k == VertexKind.INTERIOR_DOF) | (k == VertexKind.COARSE_OVERLAPPED)
+                hang = k == VertexKind.HANGING
+                self._masks[l] = {"kinds": k, "dof": dof, "composite": k == VertexKind.INTERIOR_DOF,
+                                  "hanging": hang, "exists": k != VertexKind.NONE,
+                                  "overlapped": k == VertexKind.COARSE_OVERLAPPED,
+                                  "rho_src": dof | hang}
+        return self._masks
+
+    def kinds(self, l: int) -> np.ndarray:
+        out = np.empty(self._nv_shape(l), dtype=np.int8)
+        _abi.check(_abi.lib().tmg_get_kinds(self._h, l, _abi.ptr(out)))
+        return out
+
+    def eff_eps(self, l: int) -> np.ndarray:
+        n = 3**l
+        return self._get_table(_abi.TABLE_EFFEPS, l, (), cells=True).reshape(n, n)
+
+    def level_counts(self) -> dict:
+        return {l: (self._level_dofs[l], self._composite[l], self._hanging[l])
+                for l in range(self.lmin, self.ltop + 1)}
+
+    def _nv_shape(self, l):
+        N = 3**l + 1
+        return (N, N)
+
+    def _get_table(self, which, l, tail, cells=False):
+        n = 3**l
+        count = n * n if cells else (n + 1) ** 2
+        out = np.empty((count,) + tuple(tail))
+        _abi.check(_abi.lib().tmg_get_table(self._h, which, l, _abi.ptr(out)))
+        return out
+
+    # -- measurement hooks (bench.py) -----------------------------------------------
+    def time_cycles(self, n: int, flush_bytes: int = 0) -> float:
+        """Device milliseconds summed over n cycles (CUDA events, graph replay);
+        flush_bytes > 0 overwrites a scratch buffer that large before each cycle."""
+        self._flush_rhs()
+        ms = C.c_float()
+        _abi.check(_abi.lib().tmg_time_cycles(self._h, n, int(flush_bytes), C.byref(ms)))
+        self._host_stale = True
+        return ms.value
+
+    def profile_cycles(self, n: int) -> dict:
+        """Per-kernel device ms over n cycles (events around each launch)."""
+        self._flush_rhs()
+        cap = 64
+        names = (C.c_char_p * cap)()
+        ms = (C.c_float * cap)()
+        cnt = (C.c_int32 * cap)()
+        nk = C.c_int32()
+        _abi.check(_abi.lib().tmg_profile_cycles(self._h, n, cap, names, ms, cnt, C.byref(nk)))
+        self._host_stale = True
+        return {names[k].decode(): (ms[k], cnt[k]) for k in range(nk.value)}
+
+    def launches_per_cycle(self) -> int:
+        n = C.c_int32()
+        _abi.check(_abi.lib().tmg_launches_per_cycle(self._h, C.byref(n)))
+        return n.value
+
+
+def device_count() -> int:
+    try:
+        return int(_abi.lib().tmg_device_count())
+    except (OSError, RuntimeError):
+        return 0
