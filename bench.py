@@ -83,27 +83,48 @@ class Dist:
 # algorithmic byte model, fp64 = 8 B
 
 def bytes_model(eng, wl):
-    """Per-launch algorithmic bytes of the fine-level kernels and the whole-cycle B_alg."""
-    L = wl.ltop
-    N = 3**L + 1
-    nv = N * N
-    ncell = (3**L) ** 2
+    """Algorithmic bytes per launch of every cycle kernel, and the whole-cycle B_alg.
+
+    A kernel's algorithmic bytes are the arrays its function must read and
+    write once each: no halo re-reads, no cache reuse
+    credit.  fp64 = 8 B, flags = 1 B per vertex.
+    """
+    L, l0 = wl.ltop, eng.lmin
     boxmg = wl.flavor == "boxmg"
-    var_eps = True
-    # k_down_fine: read u, eps (per cell), rhs, diag, flags; write rho, rdof, g
-    down_fine = nv * (8 + 8 + 8 + 1) + ncell * 8 * var_eps + nv * 3 * 8
-    # k_up_fine: read g, flags, u; write u; coarse carry + P reads are 1/9-size
-    Nc = 3 ** (L - 1) + 1
-    up_fine = nv * (8 + 1 + 8 + 8) + Nc * Nc * 8 * (1 + (25 if boxmg else 0))
-    # whole-cycle B_alg (SURVEY.md §8(d)): fine 24 (+8 eps) per DoF; coarse 48 (+8*9 op)
-    # + BoxMG P 8*24/9 per fine DoF of every level > lmin
+    jac = wl.variant == "adafac-jac"
+    rhs_levels = set(wl.rhs)
+    out = {}
+    for l in range(l0, L + 1):
+        N = 3**l + 1
+        nv, ncell = N * N, (3**l) ** 2
+        op = (72 * nv) if (boxmg and l < L) else 8 * ncell       # table rows or per-cell eps
+        rd = nv * (8 + 8 + 1) + op + (8 * nv if l in rhs_levels else 0)   # u, diag, flags
+        wr = 8 * nv + (16 * nv if l > l0 else 0)                  # g (+ rho, rdof)
+        if l < L:
+            Nf = 3 ** (l + 1) + 1
+            rd += 16 * Nf * Nf                                    # rho, rdof of the finer level
+            rd += 8 * ncell                                       # refined-op eps
+            if boxmg:
+                rd += 200 * nv + (392 * nv if jac else 0)         # P (25), R~ (49) planes
+        out[f"k_down_L{l}"] = rd + wr
+        up = nv * (8 + 1 + 8 + 8) + (8 * nv if l < L else 0)     # g, flags, u r/w (+ carry)
+        if l > l0:
+            Nc = 3 ** (l - 1) + 1
+            up += 8 * Nc * Nc + (200 * Nc * Nc if boxmg else 0)   # coarse carry (+ P)
+        out[f"k_up_L{l}"] = up
+        if l < L:
+            Nf = 3 ** (l + 1) + 1
+            out[f"k_inject_u_L{l}"] = nv * 1 + 8 * nv * 2         # flags, u_f gather, u write
+    # whole-cycle B_alg (SURVEY.md §8(d)): fine 24 (+8 eps) per DoF; coarse 48 (+ op)
+    # + BoxMG P 8*24/9 per DoF of every level above lmin
     counts = eng.level_counts()
     fine_dofs = counts[L][0]
-    coarse = sum(counts[l][0] for l in range(eng.lmin, L))
-    b_alg = fine_dofs * (24 + 8 * var_eps) + coarse * (48 + (72 if boxmg else 8))
+    coarse = sum(counts[l][0] for l in range(l0, L))
+    b_alg = fine_dofs * (24 + 8) + coarse * (48 + (72 if boxmg else 8) + (16 if jac else 0))
     if boxmg:
-        b_alg += sum(counts[l][0] for l in range(eng.lmin + 1, L + 1)) * 8 * 24 / 9
-    return {"k_down_fine": down_fine, "k_up_fine": up_fine, "cycle": b_alg}
+        b_alg += sum(counts[l][0] for l in range(l0 + 1, L + 1)) * 8 * 24 / 9
+    out["cycle"] = b_alg
+    return out
 
 
 # ---------------------------------------------------------------------------

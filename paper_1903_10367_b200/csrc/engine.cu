@@ -2,6 +2,7 @@
 // per-cycle launch sequence captured in a CUDA graph, and the C ABI declared
 // in include/tmg.h (each entry cites the ReferenceEngine method it replaces).
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -41,6 +42,9 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 inline unsigned nblk(size_t n) { return (unsigned)((n + tmg::kBlock - 1) / tmg::kBlock); }
+
+// Levels with at most kSmallLevel vertices run in the one-block coarse-chain kernel.
+constexpr size_t kSmallLevel = 1024;
 
 int ipow3(int l) {
   int r = 1;
@@ -97,8 +101,16 @@ struct tmg_handle {
   std::vector<KTimer>* timers = nullptr;
   std::vector<cudaEvent_t> ev_pool;
   int ev_used = 0;
+  struct Pending {
+    const char* name;
+    cudaEvent_t e0, e1;
+  };
+  std::vector<Pending> pending;
   void* flush_buf = nullptr;
   size_t flush_bytes = 0;
+  // coarse chain (cluster kernel) and its argument blocks
+  int lc = 0, part_base = 0;
+  unsigned long long* stamps = nullptr;  // k_coarse phase timestamps (diagnostics)
 };
 
 namespace {
@@ -123,10 +135,12 @@ void free_all(tmg_handle* h) {
 
 // --- launch helpers with optional per-kernel timing -------------------------
 
+// Profiling records an event pair around every launch and resolves all of
+// them after one synchronisation at the end (no per-launch host sync).
 int begin_k(tmg_handle* h, const char* name, cudaEvent_t* e0) {
   if (!h->profiling) return TMG_OK;
   if (h->ev_used + 2 > (int)h->ev_pool.size()) {
-    for (int k = 0; k < 64; ++k) {
+    for (int k = 0; k < 256; ++k) {
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
       h->ev_pool.push_back(e);
@@ -143,14 +157,34 @@ int end_k(tmg_handle* h, const char* name, cudaEvent_t e0) {
   if (!h->profiling) return TMG_OK;
   cudaEvent_t e1 = h->ev_pool[h->ev_used++];
   CK(cudaEventRecord(e1, h->s));
-  CK(cudaEventSynchronize(e1));
-  float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, e0, e1));
-  h->ev_used -= 2;
-  for (auto& t : *h->timers)
-    if (std::strcmp(t.name, name) == 0) { t.ms += ms; t.launches++; return TMG_OK; }
-  h->timers->push_back({name, ms, 1});
+  h->pending.push_back({name, e0, e1});
   return TMG_OK;
+}
+
+int resolve_timers(tmg_handle* h) {
+  CK(cudaStreamSynchronize(h->s));
+  for (auto& p : h->pending) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, p.e0, p.e1));
+    bool found = false;
+    for (auto& t : *h->timers)
+      if (std::strcmp(t.name, p.name) == 0) { t.ms += ms; t.launches++; found = true; break; }
+    if (!found) h->timers->push_back({p.name, ms, 1});
+  }
+  h->pending.clear();
+  h->ev_used = 0;
+  return TMG_OK;
+}
+
+// static per-level kernel names for the profiler
+const char* lvl_name(const char* base, int l) {
+  static char names[8][16][24];
+  static const char* bases[8] = {"k_down", "k_up", "k_inject_u", "k_hang", "k_inject_d", "", "", ""};
+  int b = 0;
+  while (b < 5 && std::strcmp(bases[b], base) != 0) ++b;
+  if (b >= 5 || l < 0 || l > 15) return base;
+  if (!names[b][l][0]) std::snprintf(names[b][l], 24, "%s_L%d", base, l);
+  return names[b][l];
 }
 
 #define LAUNCH(h, name, kernel, grid, ...)                         \
@@ -162,105 +196,172 @@ int end_k(tmg_handle* h, const char* name, cudaEvent_t e0) {
     TRY(end_k(h, name, e0_));                                      \
   } while (0)
 
-// --- the cycle --------------------------------------------------------------
+// 32 x 8 vertex tiles of the grid kernels (k_down, k_up)
+inline unsigned tiles_x(int N) { return (unsigned)((N + tmg::kTileX - 1) / tmg::kTileX); }
+inline unsigned tiles_y(int N) { return (unsigned)((N + tmg::kTileY - 1) / tmg::kTileY); }
 
-int enqueue_down(tmg_handle* h, bool write) {
+#define LAUNCH_TILES(h, name, kernel, N, ...)                                          \
+  do {                                                                                 \
+    cudaEvent_t e0_ = nullptr;                                                         \
+    TRY(begin_k(h, name, &e0_));                                                       \
+    kernel<<<dim3(tiles_x(N), tiles_y(N)), dim3(tmg::kTileX, tmg::kTileY), 0, (h)->s>>>( \
+        __VA_ARGS__);                                                                  \
+    CKL();                                                                             \
+    TRY(end_k(h, name, e0_));                                                          \
+  } while (0)
+
+// --- the cycle --------------------------------------------------------------
+//
+// Levels above lc ("grid levels") get one grid-wide launch per sweep; the
+// coarse chain lmin..lc runs in one thread-block-cluster launch (k_coarse).
+// Per cycle: (ltop - lc) k_down + 1 k_coarse + (ltop - lc) k_up (+ k_hang on
+// levels with hanging vertices).
+
+tmg::DownArgs make_down(tmg_handle* h, int l, bool write) {
   const int l0 = h->lmin, l1 = h->ltop;
-  const int var = h->cfg.variant;
-  for (int l = l1; l >= l0; --l) {
-    Level& c = h->L[l];
-    tmg::DownArgs a{};
-    a.N = c.N;
-    a.is_top = (l == l1);
-    a.variant = var;
-    a.write = write ? 1 : 0;
-    a.u = c.u;
-    a.flags = c.flags;
-    a.diag = c.diag;
-    a.op = c.op;
-    a.rop = c.rop;
-    a.rhs = c.rhs;
-    if (l < l1) {
-      Level& f = h->L[l + 1];
-      a.Nf = f.N;
-      a.rho_f = f.rho;
-      a.rdof_f = f.rdof;
-      a.boxmg = h->cfg.flavor == TMG_BOXMG;
-      a.P = c.P;
-      a.Rt = c.Rt;
-      a.rt_mode = c.rt_mode;
-      const double c1 = 1.0 / 3.0;
-      a.rt_side = c1 * -1.0;
-      a.rt_mid = c1 * 8.0;
-      a.rt_scale = h->cfg.omega * 3.0 / 8.0;
+  Level& c = h->L[l];
+  tmg::DownArgs a{};
+  a.N = c.N;
+  a.is_top = (l == l1);
+  a.variant = h->cfg.variant;
+  a.write = write ? 1 : 0;
+  a.u = c.u;
+  a.flags = c.flags;
+  a.diag = c.diag;
+  a.op = c.op;
+  a.rop = c.rop;
+  a.rhs = c.rhs;
+  if (l < l1) {
+    Level& f = h->L[l + 1];
+    a.Nf = f.N;
+    a.rho_f = f.rho;
+    a.rdof_f = f.rdof;
+    a.boxmg = h->cfg.flavor == TMG_BOXMG;
+    a.P = c.P;
+    a.Rt = c.Rt;
+    a.rt_mode = c.rt_mode;
+    if (a.rt_mode == tmg::RT_FROM_P) {
+      // R~ rebuilt from the P registers beat reading the stored table on every
+      // level of config 2 (measured); TMG_RT=table selects the table path.
+      const char* env = std::getenv("TMG_RT");
+      if (env && std::strcmp(env, "table") == 0) a.rt_mode = tmg::RT_TABLE;
     }
-    a.w_l = c.w_l;
-    a.omega = h->cfg.omega;
-    a.wt = h->wt;
-    a.ds = h->cfg.damping_scale;
-    a.hA = c.hA;
-    a.hB = c.hB;
-    a.rho = (l > l0) ? c.rho : nullptr;
-    a.rdof = (l > l0) ? c.rdof : nullptr;
-    a.g = c.g;
-    a.part_sum = h->part_sum + c.part_off;
-    a.part_max = h->part_max + c.part_off;
-    LAUNCH(h, l == l1 ? "k_down_fine" : "k_down_coarse", tmg::k_down, c.nblocks, a);
+    const double c1 = 1.0 / 3.0;  // interior_stencil(1.0) (discretization.py:165-167)
+    a.rt_side = c1 * -1.0;
+    a.rt_mid = c1 * 8.0;
+    a.rt_scale = h->cfg.omega * 3.0 / 8.0;  // operators.py:604
+    a.rt_omega = h->cfg.omega;               // operators.py:546
   }
-  LAUNCH(h, "k_finalize", tmg::k_finalize, 1, h->part_sum, h->part_max, h->nparts, h->hist,
-         h->counter, h->cap);
+  a.w_l = c.w_l;
+  a.omega = h->cfg.omega;
+  a.wt = h->wt;
+  a.ds = h->cfg.damping_scale;
+  a.hA = c.hA;
+  a.hB = c.hB;
+  a.rho = (l > l0) ? c.rho : nullptr;
+  a.rdof = (l > l0) ? c.rdof : nullptr;
+  a.g = c.g;
+  a.part_sum = h->part_sum + c.part_off;
+  a.part_max = h->part_max + c.part_off;
+  return a;
+}
+
+tmg::UpArgs make_up(tmg_handle* h, int l) {
+  const int l0 = h->lmin, l1 = h->ltop;
+  Level& c = h->L[l];
+  tmg::UpArgs a{};
+  a.l = l;
+  a.l0 = l0;
+  a.N = c.N;
+  a.is_bottom = (l == l0);
+  a.boxmg = h->cfg.flavor == TMG_BOXMG;
+  a.pi = h->cfg.variant == tmg::VAR_PI;
+  a.flags = c.flags;
+  a.u = c.u;
+  a.g = c.g;
+  a.carry = (l < l1) ? c.carry : nullptr;
+  if (l > l0) {
+    Level& cc = h->L[l - 1];
+    a.Nc = cc.N;
+    a.carry_c = cc.carry;
+    a.P = cc.P;
+    a.flags_c = cc.flags;
+  }
+  a.ds = h->cfg.damping_scale;
+  for (int k = l0; k < l; ++k) {
+    a.ul[k] = h->L[k].u;
+    a.fl[k] = h->L[k].flags;
+    a.Nl[k] = h->L[k].N;
+  }
+  return a;
+}
+
+int launch_coarse(tmg_handle* h, bool write) {
+  tmg::CoarseArgs a{};
+  a.l0 = h->lmin;
+  a.lc = h->lc;
+  a.part_sum = h->part_sum;
+  a.part_max = h->part_max;
+  a.part_base = h->part_base;
+  a.hist = h->hist;
+  a.counter = h->counter;
+  a.cap = h->cap;
+  a.do_up = write ? 1 : 0;
+  a.stamps = h->stamps;
+  for (int l = h->lmin; l <= h->lc; ++l) {
+    a.down[l - h->lmin] = make_down(h, l, write);
+    a.up[l - h->lmin] = make_up(h, l);
+  }
+  cudaEvent_t e0 = nullptr;
+  TRY(begin_k(h, "k_coarse", &e0));
+  tmg::k_coarse<<<1, tmg::kCoarseBlock, 0, h->s>>>(a);
+  CKL();
+  TRY(end_k(h, "k_coarse", e0));
   return TMG_OK;
 }
 
-int enqueue_fas(tmg_handle* h) {
-  const int l0 = h->lmin, l1 = h->ltop;
-  for (int l = l1 - 1; l >= l0; --l) {
-    Level& c = h->L[l];
-    Level& f = h->L[l + 1];
-    LAUNCH(h, "k_inject_u", tmg::k_inject_u, nblk(c.nv), c.u, c.flags, c.N, f.u, f.N);
+int enqueue_down(tmg_handle* h, bool write) {
+  for (int l = h->ltop; l > h->lc; --l) {
+    tmg::DownArgs a = make_down(h, l, write);
+    if (l == h->ltop)
+      LAUNCH_TILES(h, lvl_name("k_down", l), tmg::k_down<1>, h->L[l].N, a);
+    else
+      LAUNCH_TILES(h, lvl_name("k_down", l), tmg::k_down<0>, h->L[l].N, a);
   }
+  TRY(launch_coarse(h, write));
+  return TMG_OK;
+}
+
+int enqueue_hang(tmg_handle* h) {
+  const int l0 = h->lmin, l1 = h->ltop;
   for (int l = l0; l <= l1; ++l) {
     Level& c = h->L[l];
     if (c.cnt[tmg::K_HANG] == 0) continue;
     const double* uc = (l == l0) ? h->u_below : h->L[l - 1].u;
     const int Nc = (l == l0) ? h->N_below : h->L[l - 1].N;
-    LAUNCH(h, "k_hang", tmg::k_hang, nblk(c.nv), c.u, c.flags, c.N, uc, Nc);
+    LAUNCH(h, lvl_name("k_hang", l), tmg::k_hang, nblk(c.nv), c.u, c.flags, c.N, uc, Nc);
   }
   return TMG_OK;
 }
 
-int enqueue_cycle(tmg_handle* h) {
+// update_fas_state() on its own (solvers.py:280-296)
+int enqueue_fas(tmg_handle* h) {
   const int l0 = h->lmin, l1 = h->ltop;
-  const bool boxmg = h->cfg.flavor == TMG_BOXMG;
-  TRY(enqueue_down(h, true));
-  if (h->cfg.variant == tmg::VAR_PI) {
-    for (int l = l0 + 1; l <= l1; ++l) {
-      Level& c = h->L[l - 1];
-      Level& f = h->L[l];
-      LAUNCH(h, "k_inject_d", tmg::k_inject_d, nblk(c.nv), c.inj, c.flags, c.N, f.g, f.N);
-    }
-  }
-  for (int l = l0; l <= l1; ++l) {
+  for (int l = l1 - 1; l >= l0; --l) {
     Level& c = h->L[l];
-    tmg::UpArgs a{};
-    a.N = c.N;
-    a.is_bottom = (l == l0);
-    a.boxmg = boxmg;
-    a.flags = c.flags;
-    a.u = c.u;
-    a.g = c.g;
-    a.carry = (l < l1) ? c.carry : nullptr;
-    if (l > l0) {
-      Level& cc = h->L[l - 1];
-      a.Nc = cc.N;
-      a.carry_c = cc.carry;
-      a.P = cc.P;
-      a.inj = (h->cfg.variant == tmg::VAR_PI) ? cc.inj : nullptr;
-    }
-    a.ds = h->cfg.damping_scale;
-    LAUNCH(h, l == l1 ? "k_up_fine" : "k_up_coarse", tmg::k_up, nblk(c.nv), a);
+    Level& f = h->L[l + 1];
+    LAUNCH(h, lvl_name("k_inject_u", l), tmg::k_inject_u, nblk(c.nv), c.u, c.flags, c.N, f.u, f.N);
   }
-  TRY(enqueue_fas(h));
+  return enqueue_hang(h);
+}
+
+int enqueue_cycle(tmg_handle* h) {
+  TRY(enqueue_down(h, true));  // includes the coarse chain (down, stats, up)
+  for (int l = h->lc + 1; l <= h->ltop; ++l) {
+    tmg::UpArgs a = make_up(h, l);
+    LAUNCH_TILES(h, lvl_name("k_up", l), tmg::k_up, h->L[l].N, a);
+  }
+  TRY(enqueue_hang(h));  // injection rides in k_up / k_coarse
   return TMG_OK;
 }
 
@@ -505,7 +606,9 @@ int build(tmg_handle* h, const tmg_tree* t) {
       tmg::k_table_diag<<<nblk(c.nv), tmg::kBlock, 0, h->s>>>(c.diag_raw, c.diag, c.tbl, c.flags, c.nv);
       CKL();
       if (jac) {
-        c.rt_mode = tmg::RT_TABLE;
+        // unit-coefficient R~ is rebuilt from P in the cycle (RT_FROM_P); the
+        // stored table serves tmg_get_table and the true-operator variant
+        c.rt_mode = cfg.rtilde_true_operator ? tmg::RT_TABLE : tmg::RT_FROM_P;
         TRY(dalloc(h, &c.Rt, 49 * c.nv));
         if (cfg.rtilde_true_operator)
           tmg::k_rtilde<<<nblk(c.nv), tmg::kBlock, 0, h->s>>>(c.Rt, nc, c.P, 0, tf, f.flags,
@@ -522,7 +625,11 @@ int build(tmg_handle* h, const tmg_tree* t) {
   CK(cudaStreamSynchronize(h->s));
   if (hdeg) return fail(TMG_EDEGENERATE, "degenerate collapsed stencil in face-point solve");
 
-  // work buffers, u, partials
+  // coarse chain: every level up to lc runs inside the cluster kernel
+  h->lc = l0;
+  for (int l = l0; l <= l1 && l - l0 < tmg::kMaxChain; ++l)
+    if (h->L[l].nv <= kSmallLevel) h->lc = l;
+  // work buffers, u, partials (grid levels first, then one per cluster CTA)
   int parts = 0;
   for (int l = l0; l <= l1; ++l) {
     Level& c = h->L[l];
@@ -535,15 +642,18 @@ int build(tmg_handle* h, const tmg_tree* t) {
       TRY(dalloc(h, &c.rdof, c.nv));
     }
     if (l < l1) TRY(dalloc(h, &c.carry, c.nv));
-    if (cfg.variant == tmg::VAR_PI && l < l1) TRY(dalloc(h, &c.inj, c.nv));
-    c.nblocks = (int)nblk(c.nv);
-    c.part_off = parts;
-    parts += c.nblocks;
+    c.nblocks = (int)(tiles_x(c.N) * tiles_y(c.N));
+    if (l > h->lc) {
+      c.part_off = parts;
+      parts += c.nblocks;
+    }
   }
   h->N_below = ipow3(l0 - 1) + 1;
   TRY(dalloc(h, &h->u_below, (size_t)h->N_below * h->N_below));
   CK(cudaMemcpyAsync(h->u_below, t->u[l0 - 1], sizeof(double) * h->N_below * h->N_below,
                      cudaMemcpyHostToDevice, h->s));
+  h->part_base = parts;
+  TRY(dalloc(h, &h->stamps, 64));
   h->nparts = parts;
   TRY(dalloc(h, &h->part_sum, parts));
   TRY(dalloc(h, &h->part_max, parts));
@@ -840,9 +950,11 @@ int tmg_profile_cycles(tmg_handle* h, int32_t ncycles, int32_t cap, const char**
     h->host_counter++;
   }
   h->profiling = false;
+  if (rc == TMG_OK) rc = resolve_timers(h);
   h->timers = nullptr;
+  h->pending.clear();
+  h->ev_used = 0;
   if (rc != TMG_OK) return rc;
-  CK(cudaStreamSynchronize(h->s));
   int n = 0;
   for (auto& t : timers) {
     if (n >= cap) break;
@@ -859,6 +971,13 @@ int tmg_launches_per_cycle(tmg_handle* h, int32_t* n) {
   if (!h || !n) return fail(TMG_EINVAL, "null argument");
   TRY(ensure_graph(h));
   *n = h->launches;
+  return TMG_OK;
+}
+
+// diagnostics (not part of tmg.h): %globaltimer stamps of the last k_coarse phases
+int tmg_debug_stamps(tmg_handle* h, unsigned long long* out, int n) {
+  if (!h || !out) return fail(TMG_EINVAL, "null argument");
+  CK(cudaMemcpy(out, h->stamps, sizeof(unsigned long long) * std::min(n, 64), cudaMemcpyDeviceToHost));
   return TMG_OK;
 }
 

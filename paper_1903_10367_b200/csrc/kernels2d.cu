@@ -4,7 +4,11 @@
 // Thread-per-vertex kernels over dense per-level grids.  Each one evaluates
 // exactly the reference's per-element expression DAG (see tmg_kernels.cuh);
 // the file is compiled with --fmad=false.
+#include <cooperative_groups.h>
+
 #include "kernels2d.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace tmg {
 
@@ -485,115 +489,410 @@ __global__ void k_rtilde(double* __restrict__ Rt, int nc, const double* __restri
 // cycle
 // ===========================================================================
 
-template <int BS>
-__device__ __forceinline__ void block_reduce_store(double s, double m, double* part_sum,
-                                                   double* part_max) {
-  __shared__ double ss[BS / 32], sm[BS / 32];
-  for (int o = 16; o > 0; o >>= 1) {
-    s += __shfl_down_sync(0xffffffffu, s, o);
-    m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+// --- per-vertex bodies (shared by the grid kernels and the cluster kernel) ---
+
+// d-linear prolongation with an arbitrary coarse-value functor (operators.py:96-127).
+template <class CV>
+__device__ __forceinline__ double prolong_dlinear_fn(const CV& cv, int Nc, int i, int j) {
+  const int m = Nc - 1;
+  const int qi = i / 3, ri = i - 3 * qi, qni = min(qi + 1, m);
+  const int qj = j / 3, rj = j - 3 * qj, qnj = min(qj + 1, m);
+  const double c00 = cv(qi, qj), c10 = cv(qni, qj), c01 = cv(qi, qnj), c11 = cv(qni, qnj);
+  const double wli = c_WL[ri], wri = c_WR[ri];
+  const double t0 = wli * c00 + wri * c10;
+  const double t1 = wli * c01 + wri * c11;
+  return c_WL[rj] * t0 + c_WR[rj] * t1;
+}
+
+// P-table prolongation with a coarse-value functor (operators.py:570-581):
+// (oi, oj) row-major == coarse (I, J) descending.
+template <class LD, class CV>
+__device__ __forceinline__ double prolong_table_fn(const CV& cv, const double* P, int Nc, int i,
+                                                   int j) {
+  const size_t nvc = (size_t)Nc * Nc;
+  const int qi = i / 3, ri = i - 3 * qi;
+  const int qj = j / 3, rj = j - 3 * qj;
+  double w[4], x[4];
+  bool use[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int di = 1 - (k >> 1), dj = 1 - (k & 1);
+    use[k] = (di == 0 || ri > 0) && (dj == 0 || rj > 0);
+    const int I = qi + di, J = qj + dj;
+    const int oi = i - 3 * I, oj = j - 3 * J;
+    w[k] = use[k] ? LD::ld(P + (size_t)((oi + 2) * 5 + (oj + 2)) * nvc + (size_t)I * Nc + J) : 0.0;
+    x[k] = use[k] ? cv(I, J) : 0.0;
   }
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) { ss[w] = s; sm[w] = m; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double a = 0.0, b = 0.0;
-    for (int k = 0; k < BS / 32; ++k) { a += ss[k]; b = fmax(b, sm[k]); }
-    part_sum[blockIdx.x] = a;
-    part_max[blockIdx.x] = b;
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (use[k]) acc = acc + w[k] * x[k];
+  return acc;
+}
+
+// Operator image from a loaded 3x3 neighbourhood xu and operator data ow
+// (table taps, or element eps of the 4 adjacent cells): operators.py:143-248.
+template <bool CHK>
+__device__ __forceinline__ double op_from(const OpView& op, const double xu[9], const double ow[9],
+                                          int N, int i, int j) {
+  if (op.kind == OP_CONST) return const_from<CHK>(xu, N, i, j, op.s_side, op.s_mid);
+  double acc = 0.0;
+  if (op.kind == OP_TABLE) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k)
+      if (in_rng<CHK>(i + k / 3 - 1, j + k % 3 - 1, N)) acc = acc + ow[k] * xu[k];
+    return acc;
+  }
+  if (op.kind == OP_ELEMENT) {
+    const int n = N - 1;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int a0 = c & 1, a1 = c >> 1;
+      const int ci = i - a0, cj = j - a1;
+      if (CHK && !(ci >= 0 && cj >= 0 && ci < n && cj < n)) continue;
+      double e = 0.0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        e = e + c_E[c * 4 + b] * xu[((b & 1) - a0 + 1) * 3 + ((b >> 1) - a1 + 1)];
+      acc = acc + ow[c] * e;
+    }
+    return acc;
+  }
+  return 0.0;
+}
+
+template <class LD, bool CHK>
+__device__ __forceinline__ void op_load(const OpView& op, int N, int i, int j, double ow[9]) {
+  const size_t nv = (size_t)N * N, v = (size_t)i * N + j;
+  if (op.kind == OP_TABLE) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) ow[k] = LD::ld(op.tbl + (size_t)k * nv + v);
+  } else if (op.kind == OP_ELEMENT) {
+    const int n = N - 1;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int ci = i - (c & 1), cj = j - (c >> 1);
+      ow[c] = (!CHK || (ci >= 0 && cj >= 0 && ci < n && cj < n)) ? LD::ld(op.eps + (size_t)ci * n + cj)
+                                                                  : 0.0;
+    }
   }
 }
 
-// One level of the fine -> coarse sweep of advance() (solvers.py:345-375):
-// coarse right-hand side from the finer residual (R rho + rhs + bpart),
-// residual, stats, damped Jacobi and the adaFACx damping term.
-__global__ void __launch_bounds__(kBlock) k_down(DownArgs a) {
-  const size_t nv = (size_t)a.N * a.N;
-  const size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double s = 0.0, m = 0.0;
-  if (v < nv) {
-    const int i = (int)(v / a.N), j = (int)(v % a.N);
-    const uint8_t f = a.flags[v];
-    const int kind = f & 7;
-    const double au = apply_op_at(a.op, a.u, a.N, i, j);
+// advance(), fine -> coarse sweep at one vertex (solvers.py:345-375).
+// TOP: 1 = finest level (no restriction code), 0 = coarser level.  CHK:
+// range tests on (true) or compiled out for vertices whose whole footprint
+// (3x3 stencil, 5x5 / 7x7 fine window) lies inside the grid.  All loads of
+// the residual part are issued in one batch, the damping part (7x7 window of
+// rho_dof_{l+1}) in a second one.
+template <class LD, int TOP, bool CHK>
+__device__ __forceinline__ void down_vertex_impl(const DownArgs& a, int i, int j, double& s,
+                                                 double& m) {
+  constexpr bool is_top = TOP == 1;
+  const int N = a.N;
+  const size_t v = (size_t)i * N + j;
+  const size_t nv = (size_t)N * N;
+  // ---- batch 1 -------------------------------------------------------------
+  const uint8_t f = a.flags[v];
+  double xu[9], ow[9], rw[9];
+  load3x3<LD, CHK>(a.u, N, i, j, xu);
+  op_load<LD, CHK>(a.op, N, i, j, ow);
+  const double rhs = a.rhs ? LD::ld(a.rhs + v) : 0.0;
+  const double dg = a.write ? LD::ld(a.diag + v) : 1.0;
+  double pw[25], rx[25];
+  if (!is_top) {
+    op_load<LD, CHK>(a.rop, N, i, j, rw);
+    const int Nf = a.Nf, m3 = (Nf - 1) / 3;
+#pragma unroll
+    for (int k = 0; k < 25; ++k) {
+      const int oi = k / 5 - 2, oj = k % 5 - 2;
+      const int fi = 3 * i + oi, fj = 3 * j + oj;
+      bool ok;
+      if (a.boxmg) {
+        ok = in_rng<CHK>(fi, fj, Nf);
+        pw[k] = LD::ld(a.P + (size_t)k * nv + v);
+      } else {
+        ok = !CHK || !((oi < 0 && i < 1) || (oi > 0 && i > m3 - 1) || (oj < 0 && j < 1) ||
+                       (oj > 0 && j > m3 - 1));
+        pw[k] = 0.0;
+      }
+      rx[k] = ok ? LD::ld(a.rho_f + (size_t)fi * Nf + fj) : 0.0;
+    }
+  }
+  // ---- residual -------------------------------------------------------------
+  const int kind = f & 7;
+  const bool src = is_src(f), dof = is_dof(f);
+  double rho = 0.0;
+  if (src) {
+    const double au = op_from<CHK>(a.op, xu, ow, N, i, j);
     double b;
-    if (a.is_top) {
-      b = a.rhs ? a.rhs[v] : 0.0;
+    if (is_top) {
+      b = rhs;
     } else {
-      b = a.boxmg ? restrict_table_at(a.rho_f, a.Nf, a.P, a.N, i, j)
-                  : restrict_dlinear_at(a.rho_f, a.Nf, i, j);
-      if (a.rhs) b = b + a.rhs[v];
+      // b_l = R rho_{l+1} + rhs_l (solvers.py:370-371), then + bpart (:351-352)
+      if (a.boxmg) {
+        b = 0.0;  // TransferOps.restrict, 5x5 taps row-major (operators.py:586-596)
+#pragma unroll
+        for (int k = 0; k < 25; ++k)
+          if (in_rng<CHK>(3 * i + k / 5 - 2, 3 * j + k % 5 - 2, a.Nf)) b = b + pw[k] * rx[k];
+      } else {
+        const int m3 = (a.Nf - 1) / 3;  // restrict_dlinear: axis 0 then axis 1 (operators.py:111-132)
+        b = 0.0;
+#pragma unroll
+        for (int bj = 0; bj < 5; ++bj) {
+          const int oj = bj - 2;
+          if (CHK && ((oj < 0 && j < 1) || (oj > 0 && j > m3 - 1))) continue;
+          double t = 0.0;
+#pragma unroll
+          for (int ai = 0; ai < 5; ++ai) {
+            const int oi = ai - 2;
+            if (CHK && ((oi < 0 && i < 1) || (oi > 0 && i > m3 - 1))) continue;
+            t = t + c_W5[ai] * rx[ai * 5 + bj];
+          }
+          b = b + c_W5[bj] * t;
+        }
+      }
+      if (a.rhs) b = b + rhs;
       if (a.rop.kind != OP_NONE) {
-        const double bp = (kind == K_OVER) ? au : apply_op_at(a.rop, a.u, a.N, i, j);
+        const double bp = (kind == K_OVER) ? au : op_from<CHK>(a.rop, xu, rw, N, i, j);
         b = b + bp;
       }
     }
-    const double rho = is_src(f) ? b - au : 0.0;
-    const double rd = is_dof(f) ? rho : 0.0;
-    if (kind == K_DOF) {
-      const double h = (f & F_NEAR) ? a.hA : a.hB;
-      const double t = h * rd;
-      s = t * t;
-      m = fabs(rd);
-    }
-    if (a.write) {
-      double d;
-      if (a.variant == VAR_BPX && !a.is_top) d = a.omega * rd;
-      else d = (a.w_l * rd) / a.diag[v];
-      if (a.variant == VAR_JAC && !a.is_top) {
-        const double bt = (a.rt_mode == RT_GEOM_FAST)
-                              ? restrict_rt_geom_at(a.rdof_f, a.Nf, i, j, a.rt_side, a.rt_mid, a.rt_scale)
-                              : restrict_rt_table_at(a.rdof_f, a.Nf, a.Rt, a.N, i, j);
-        const double dt = is_dof(f) ? a.ds * ((a.wt * bt) / a.diag[v]) : 0.0;
-        d = d - dt;
-      }
-      a.g[v] = d;
-    }
-    if (a.rho) {
-      const bool cpt = (i % 3 == 0) && (j % 3 == 0);
-      a.rho[v] = (a.variant == VAR_AFACC && cpt) ? 0.0 : rho;
-    }
-    if (a.rdof) a.rdof[v] = rd;
+    rho = b - au;
   }
-  block_reduce_store<kBlock>(s, m, a.part_sum, a.part_max);
+  const double rd = dof ? rho : 0.0;
+  if (kind == K_DOF) {  // composite stats (solvers.py:435-443)
+    const double h = (f & F_NEAR) ? a.hA : a.hB;
+    const double t = h * rd;
+    s = s + t * t;
+    m = fmax(m, fabs(rd));
+  }
+  if (a.write) {
+    double d;
+    if (a.variant == VAR_BPX && !is_top) d = a.omega * rd;
+    else d = (a.w_l * rd) / dg;
+    if (a.variant == VAR_JAC && !is_top && dof) {
+      // dtil = ds * ((wt * R~ rho_dof_{l+1}) / diag) (solvers.py:360-363)
+      double bt;
+      if (a.rt_mode == RT_FROM_P) {
+        // ---- batch 2: 7x7 window of rho_dof_{l+1}; R~ weights rebuilt from the
+        // P registers in exactly the order of smoothed_restriction_table
+        // (operators.py:520-531, 546), so the result equals the stored table's.
+        double fx[49];
+#pragma unroll
+        for (int k = 0; k < 49; ++k) {
+          const int fi = 3 * i + k / 7 - 3, fj = 3 * j + k % 7 - 3;
+          fx[k] = in_rng<CHK>(fi, fj, a.Nf) ? LD::ld(a.rdof_f + (size_t)fi * a.Nf + fj) : 0.0;
+        }
+        bt = 0.0;
+#pragma unroll
+        for (int k = 0; k < 49; ++k) {
+          const int ti = k / 7 - 3, tj = k % 7 - 3;
+          if (!in_rng<CHK>(3 * i + ti, 3 * j + tj, a.Nf)) continue;
+          double acc = 0.0;
+#pragma unroll
+          for (int ji = -2; ji <= 2; ++ji) {
+            if (ti - ji < -1 || ti - ji > 1) continue;
+#pragma unroll
+            for (int jj = -2; jj <= 2; ++jj) {
+              if (tj - jj < -1 || tj - jj > 1) continue;
+              acc = acc + pw[(ji + 2) * 5 + (jj + 2)] * c_A1INV[(ti - ji + 1) * 3 + (tj - jj + 1)];
+            }
+          }
+          bt = bt + (acc * a.rt_omega) * fx[k];
+        }
+      } else if (a.rt_mode == RT_GEOM_FAST) {
+        bt = restrict_rt_geom_at<LD, CHK>(a.rdof_f, a.Nf, i, j, a.rt_side, a.rt_mid, a.rt_scale);
+      } else {
+        bt = restrict_rt_table_at<LD, CHK>(a.rdof_f, a.Nf, a.Rt, N, i, j);
+      }
+      d = d - a.ds * ((a.wt * bt) / dg);
+    } else if (a.variant == VAR_JAC && !is_top) {
+      d = d - 0.0;
+    }
+    a.g[v] = d;
+  }
+  if (a.rho) {
+    const bool cpt = (i % 3 == 0) && (j % 3 == 0);
+    a.rho[v] = (a.variant == VAR_AFACC && cpt) ? 0.0 : rho;  // afacc: solvers.py:365-368
+  }
+  if (a.rdof) a.rdof[v] = rd;
 }
 
-// inj = d_l at taken c-points, 0 elsewhere (adafac-pi, solvers.py:377-382)
-__global__ void k_inject_d(double* __restrict__ inj, const uint8_t* __restrict__ flags_c, int Nc,
-                           const double* __restrict__ d, int Nf) {
-  const size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= (size_t)Nc * Nc) return;
-  const int i = (int)(v / Nc), j = (int)(v % Nc);
-  inj[v] = (flags_c[v] & F_TAKE) ? d[(size_t)(3 * i) * Nf + 3 * j] : 0.0;
+// Interior vertices (i, j in [1, N-2]) take the check-free instantiation.
+template <class LD, int TOP>
+__device__ __forceinline__ void down_vertex(const DownArgs& a, int i, int j, double& s, double& m) {
+  if (i >= 1 && j >= 1 && i <= a.N - 2 && j <= a.N - 2)
+    down_vertex_impl<LD, TOP, false>(a, i, j, s, m);
+  else
+    down_vertex_impl<LD, TOP, true>(a, i, j, s, m);
 }
 
-// One level of the coarse -> fine carry (solvers.py:386-395), including the
-// adafac-pi damping (solvers.py:377-384).
-__global__ void __launch_bounds__(kBlock) k_up(UpArgs a) {
-  const size_t nv = (size_t)a.N * a.N;
-  const size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= nv) return;
-  const int i = (int)(v / a.N), j = (int)(v % a.N);
+// advance(), coarse -> fine carry at one vertex (solvers.py:377-395) and the
+// FAS injection of the new value down the chain of taking levels (:283-288).
+template <class LD>
+__device__ __forceinline__ void up_vertex(const UpArgs& a, int i, int j) {
+  const size_t v = (size_t)i * a.N + j;
   const uint8_t f = a.flags[v];
-  double g = a.g[v];
-  if (a.inj) {
-    const double pv = a.boxmg ? prolong_table_at(a.inj, a.P, a.Nc, i, j)
-                              : prolong_dlinear_at(a.inj, a.Nc, i, j);
+  double g = LD::ld(a.g + v);
+  if (a.pi && !a.is_bottom) {
+    // dtil_l = ds * P(inj d_l), inj = d_l at taken c-points (solvers.py:377-384)
+    const uint8_t* fc = a.flags_c;
+    const double* gl = a.g;
+    const int Nc = a.Nc, N = a.N;
+    auto inj = [&](int I, int J) -> double {
+      return (fc[(size_t)I * Nc + J] & F_TAKE) ? LD::ld(gl + (size_t)(3 * I) * N + 3 * J) : 0.0;
+    };
+    const double pv = a.boxmg ? prolong_table_fn<LD>(inj, a.P, Nc, i, j)
+                              : prolong_dlinear_fn(inj, Nc, i, j);
     const double dt = is_dof(f) ? a.ds * pv : 0.0;
     g = g - dt;
   }
   double c = g;
   if (!a.is_bottom) {
-    const double pc = a.boxmg ? prolong_table_at(a.carry_c, a.P, a.Nc, i, j)
-                              : prolong_dlinear_at(a.carry_c, a.Nc, i, j);
+    const double* cc = a.carry_c;
+    const int Nc = a.Nc;
+    auto cv = [&](int I, int J) -> double { return LD::ld(cc + (size_t)I * Nc + J); };
+    const double pc = a.boxmg ? prolong_table_fn<LD>(cv, a.P, Nc, i, j)
+                              : prolong_dlinear_fn(cv, Nc, i, j);
     c = pc + g;
   }
   if ((f & 7) == K_NONE) c = 0.0;
   if (a.carry) a.carry[v] = c;
-  a.u[v] = a.u[v] + c;
+  const double un = a.u[v] + c;
+  a.u[v] = un;
+  int ii = i, jj = j;
+  for (int lc = a.l - 1; lc >= a.l0; --lc) {
+    if (ii % 3 != 0 || jj % 3 != 0) break;
+    ii /= 3;
+    jj /= 3;
+    const size_t vc = (size_t)ii * a.Nl[lc] + jj;
+    if (!(a.fl[lc][vc] & F_TAKE)) break;
+    a.ul[lc][vc] = un;
+  }
 }
 
-// FAS injection (solvers.py:283-288)
+template <int BS>
+__device__ __forceinline__ void block_reduce(double& s, double& m) {
+  __shared__ double ss[BS / 32], sm[BS / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_down_sync(0xffffffffu, s, o);
+    m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+  }
+  const int t = threadIdx.y * blockDim.x + threadIdx.x;
+  const int w = t >> 5, lane = t & 31;
+  if (lane == 0) { ss[w] = s; sm[w] = m; }
+  __syncthreads();
+  if (t == 0) {
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < BS / 32; ++k) { a += ss[k]; b = fmax(b, sm[k]); }
+    s = a;
+    m = b;
+  }
+  __syncthreads();
+}
+
+// Grid kernels use 32 x 8 thread tiles over (j, i): no index division and
+// the 3x3 neighbourhoods of a tile share cache lines.
+template <int TOP>
+__global__ void __launch_bounds__(kBlock) k_down(const __grid_constant__ DownArgs a) {
+  const int j = blockIdx.x * kTileX + threadIdx.x;
+  const int i = blockIdx.y * kTileY + threadIdx.y;
+  double s = 0.0, m = 0.0;
+  if (i < a.N && j < a.N) down_vertex<LdNC, TOP>(a, i, j, s, m);
+  block_reduce<kBlock>(s, m);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    const int b = blockIdx.y * gridDim.x + blockIdx.x;
+    a.part_sum[b] = s;
+    a.part_max[b] = m;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_up(const __grid_constant__ UpArgs a) {
+  const int j = blockIdx.x * kTileX + threadIdx.x;
+  const int i = blockIdx.y * kTileY + threadIdx.y;
+  if (i < a.N && j < a.N) up_vertex<LdNC>(a, i, j);
+}
+
+// Plain loads for the coarse-chain kernel: its level vectors are written and
+// re-read by the same thread block (L1-coherent after __syncthreads).
+struct LdGen {
+  static __device__ __forceinline__ double ld(const double* p) { return *p; }
+};
+
+// The coarse chain lmin..lc in ONE thread block: levels lc..l0 down,
+// deterministic stats finalisation over every partial of the cycle, levels
+// l0..lc up (with the walk-down FAS injection).  Phases are separated by
+// __syncthreads only; the per-level argument blocks live in the kernel's
+// parameter space (__grid_constant__), so field reads are constant-bank hits.
+__global__ void __launch_bounds__(kCoarseBlock) k_coarse(const __grid_constant__ CoarseArgs a) {
+  __shared__ double rs[kCoarseBlock / 32], rm[kCoarseBlock / 32];
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  int nst = 0;
+  auto stamp = [&]() {
+    if (a.stamps && tid == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.stamps[nst] = t;
+    }
+    ++nst;
+  };
+  stamp();
+  double s = 0.0, m = 0.0;
+  for (int l = a.lc; l >= a.l0; --l) {
+    const DownArgs& d = a.down[l - a.l0];
+    const int N = d.N, nv = N * N;
+    if (d.is_top) {
+      for (int v = tid; v < nv; v += nthr) {
+        const int i = v / N;
+        down_vertex<LdGen, 1>(d, i, v - i * N, s, m);
+      }
+    } else {
+      for (int v = tid; v < nv; v += nthr) {
+        const int i = v / N;
+        down_vertex<LdGen, 0>(d, i, v - i * N, s, m);
+      }
+    }
+    __syncthreads();
+    stamp();
+  }
+  // fixed-order reduction of every partial of this cycle -> history slot
+  block_reduce<kCoarseBlock>(s, m);
+  double x = 0.0, y = 0.0;
+  for (int k = tid; k < a.part_base; k += nthr) {
+    x += a.part_sum[k];
+    y = fmax(y, a.part_max[k]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    x += __shfl_down_sync(0xffffffffu, x, o);
+    y = fmax(y, __shfl_down_sync(0xffffffffu, y, o));
+  }
+  if ((tid & 31) == 0) { rs[tid >> 5] = x; rm[tid >> 5] = y; }
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0, u = 0.0;
+    for (int k = 0; k < kCoarseBlock / 32; ++k) { t += rs[k]; u = fmax(u, rm[k]); }
+    t += s;  // the chain's own contribution
+    u = fmax(u, m);
+    const int slot = *a.counter;
+    a.hist[2 * (slot % a.cap)] = sqrt(t);
+    a.hist[2 * (slot % a.cap) + 1] = u;
+    *a.counter = slot + 1;
+  }
+  stamp();
+  if (!a.do_up) return;
+  for (int l = a.l0; l <= a.lc; ++l) {
+    const UpArgs& u = a.up[l - a.l0];
+    const int N = u.N, nv = N * N;
+    for (int v = tid; v < nv; v += nthr) {
+      const int i = v / N;
+      up_vertex<LdGen>(u, i, v - i * N);
+    }
+    __syncthreads();
+    stamp();
+  }
+}
+
+// FAS injection (solvers.py:283-288), standalone update_fas_state()
 __global__ void k_inject_u(double* __restrict__ uc, const uint8_t* __restrict__ flags_c, int Nc,
                            const double* __restrict__ uf, int Nf) {
   const size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -610,31 +909,7 @@ __global__ void k_hang(double* __restrict__ u, const uint8_t* __restrict__ flags
   if (v >= (size_t)N * N) return;
   if ((flags[v] & 7) != K_HANG) return;
   const int i = (int)(v / N), j = (int)(v % N);
-  u[v] = prolong_dlinear_at(uc, Nc, i, j);
-}
-
-// deterministic final reduction of the per-block partials -> history slot
-__global__ void k_finalize(const double* __restrict__ part_sum, const double* __restrict__ part_max,
-                           int nparts, double* __restrict__ hist, int* __restrict__ counter, int cap) {
-  __shared__ double ss[256], sm[256];
-  double s = 0.0, m = 0.0;
-  for (int k = threadIdx.x; k < nparts; k += 256) { s += part_sum[k]; m = fmax(m, part_max[k]); }
-  ss[threadIdx.x] = s;
-  sm[threadIdx.x] = m;
-  __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (threadIdx.x < w) {
-      ss[threadIdx.x] += ss[threadIdx.x + w];
-      sm[threadIdx.x] = fmax(sm[threadIdx.x], sm[threadIdx.x + w]);
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const int slot = *counter;
-    hist[2 * (slot % cap)] = sqrt(ss[0]);
-    hist[2 * (slot % cap) + 1] = sm[0];
-    *counter = slot + 1;
-  }
+  u[v] = prolong_dlinear_at<LdNC>(uc, Nc, i, j);
 }
 
 void upload_constants(cudaStream_t s) {

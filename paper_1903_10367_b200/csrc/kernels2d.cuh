@@ -5,7 +5,10 @@
 
 namespace tmg {
 
-constexpr int kBlock = 256;
+constexpr int kTileX = 32, kTileY = 8;
+constexpr int kBlock = kTileX * kTileY;  // grid kernels
+constexpr int kCoarseBlock = 256;  // the coarse-chain kernel (one block)
+constexpr int kMaxLevels = 16;
 
 enum Variant : int {
   VAR_ADDITIVE = 0,
@@ -17,6 +20,7 @@ enum Variant : int {
   VAR_V10 = 6
 };
 
+// One level of the fine -> coarse sweep (solvers.py:345-375).
 struct DownArgs {
   int N, is_top, variant, write;
   const double* u;
@@ -33,7 +37,7 @@ struct DownArgs {
   const double* P;   // transfers[l] P planes (boxmg)
   const double* Rt;  // transfers[l] R~ planes (RT_TABLE)
   int rt_mode;
-  double rt_side, rt_mid, rt_scale;
+  double rt_side, rt_mid, rt_scale, rt_omega;
   // update parameters
   double w_l, omega, wt, ds;
   double hA, hB;  // hweight next to / away from refined cells
@@ -45,17 +49,42 @@ struct DownArgs {
   double* part_max;
 };
 
+// One level of the coarse -> fine carry (solvers.py:386-395) with the
+// adafac-pi damping (solvers.py:377-384) and the FAS injection of the new
+// values into every coarser level that takes them (solvers.py:283-288).
 struct UpArgs {
-  int N, is_bottom, boxmg;
+  int l, l0, N, is_bottom, boxmg, pi;
   const uint8_t* flags;
   double* u;
-  const double* g;
+  const double* g;  // d - dtil (jac) / d (pi: dtil formed here)
   double* carry;
   int Nc;
   const double* carry_c;
-  const double* P;    // transfers[l-1] P planes (boxmg)
-  const double* inj;  // adafac-pi injected d on the coarse grid, or nullptr
+  const double* P;         // transfers[l-1] P planes (boxmg)
+  const uint8_t* flags_c;  // level l-1 flags (F_TAKE for adafac-pi injection)
   double ds;
+  // injection targets by level (levels l0 .. l-1)
+  double* ul[kMaxLevels];
+  const uint8_t* fl[kMaxLevels];
+  int Nl[kMaxLevels];
+};
+
+// The coarse chain [l0, lc] (at most kMaxChain levels) in one block: down
+// sweep lc -> l0, stats finalisation, up sweep l0 -> lc.  The per-level
+// argument blocks travel by value in the kernel's parameter space.
+constexpr int kMaxChain = 6;
+struct CoarseArgs {
+  int l0, lc;
+  const double* part_sum;  // partials of the grid-level down kernels
+  const double* part_max;
+  int part_base;
+  double* hist;
+  int* counter;
+  int cap;
+  int do_up;
+  unsigned long long* stamps;  // optional per-phase %globaltimer stamps (diagnostics)
+  DownArgs down[kMaxChain];    // index l - l0
+  UpArgs up[kMaxChain];
 };
 
 __global__ void k_flags(uint8_t* flags, int n, const uint8_t* ref_prev, const uint8_t* ref_cur);
@@ -80,13 +109,12 @@ __global__ void k_rap(double* tbl, const uint8_t* flags_c, int nc, const double*
                       const uint8_t* flags_f, const double* P);
 __global__ void k_rtilde(double* Rt, int nc, const double* P, int pconst, const double* tf,
                          const uint8_t* flags_f, const double* diag_f, double omega);
-__global__ void k_down(DownArgs a);
-__global__ void k_inject_d(double* inj, const uint8_t* flags_c, int Nc, const double* d, int Nf);
-__global__ void k_up(UpArgs a);
+template <int TOP>
+__global__ void k_down(const __grid_constant__ DownArgs a);
+__global__ void k_up(const __grid_constant__ UpArgs a);
+__global__ void k_coarse(const __grid_constant__ CoarseArgs a);
 __global__ void k_inject_u(double* uc, const uint8_t* flags_c, int Nc, const double* uf, int Nf);
 __global__ void k_hang(double* u, const uint8_t* flags, int N, const double* uc, int Nc);
-__global__ void k_finalize(const double* part_sum, const double* part_max, int nparts, double* hist,
-                           int* counter, int cap);
 
 void upload_constants(cudaStream_t s);
 
