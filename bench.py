@@ -115,6 +115,12 @@ def bytes_model(eng, wl):
         if l < L:
             Nf = 3 ** (l + 1) + 1
             out[f"k_inject_u_L{l}"] = nv * 1 + 8 * nv * 2         # flags, u_f gather, u write
+    # the coarse-chain kernel runs levels l0..lc (<= 1024 vertices, <= 6 levels) in one block
+    lc = l0
+    for l in range(l0, min(L, l0 + 5) + 1):
+        if (3**l + 1) ** 2 <= 1024:
+            lc = l
+    out["k_coarse"] = sum(out[f"k_down_L{l}"] + out[f"k_up_L{l}"] for l in range(l0, lc + 1))
     # whole-cycle B_alg: fine 24 (+8 eps) per DoF; coarse 48 (+ op)
     # + BoxMG P 8*24/9 per DoF of every level above lmin
     counts = eng.level_counts()
