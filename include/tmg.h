@@ -89,10 +89,30 @@ typedef struct {
   int64_t updates;
 } tmg_stats;
 
+/* 3D regular spacetree (BASELINE configs 3, 5; the reference is 2D only, its
+ * data model carried to d = 3): every cell of levels < depth refined; eps is
+ * the finest level's per-cell material ((3^depth)^3 fp64, [i][j][k]); u[l]
+ * ((3^l+1)^3 fp64) for l in 0..depth (u[l] for l < lmin may be NULL). */
+typedef struct {
+  int32_t lmin;
+  int32_t depth;
+  const double* eps;
+  const double* const* u;
+} tmg_tree3;
+
 /* ReferenceEngine.__init__ + rebuild(): solvers.py:137-141, 145-255.
  * Classifies vertices, builds eff_eps, stencils, BoxMG P, Galerkin rows and
  * R~ on the device and uploads u. */
 int tmg_create(const tmg_tree* tree, const tmg_config* cfg, tmg_handle** out);
+
+/* 3D engine (oracle/mg3d.py semantics): same entry points as 2D after creation;
+ * tmg_get_table returns 27-tap rows (TMG_TABLE_A), 125-offset P rows
+ * (TMG_TABLE_P, fine offsets -2..2) and the cell material (TMG_TABLE_EFFEPS). */
+int tmg3_create(const tmg_tree3* tree, const tmg_config* cfg, tmg_handle** out);
+int tmg3_rebuild(tmg_handle* h, const tmg_tree3* tree);
+
+/* 2 or 3: the dimension of the hierarchy a handle holds. */
+int tmg_dim(tmg_handle* h);
 
 /* ReferenceEngine.rebuild() after a mesh / material change (solvers.py:145-255):
  * rebuilds every operator from the new tree and re-uploads u. rhs is kept. */

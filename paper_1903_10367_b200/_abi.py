@@ -25,7 +25,7 @@ EXPORTS = ("tmg_create", "tmg_rebuild", "tmg_set_rhs", "tmg_set_u", "tmg_get_u",
            "tmg_update_fas_state", "tmg_cycle", "tmg_residual_stats", "tmg_levels",
            "tmg_level_counts", "tmg_get_kinds", "tmg_get_table", "tmg_time_cycles",
            "tmg_profile_cycles", "tmg_launches_per_cycle", "tmg_destroy", "tmg_last_error",
-           "tmg_device_count")
+           "tmg_device_count", "tmg3_create", "tmg3_rebuild", "tmg_dim")
 
 
 class Config(C.Structure):
@@ -39,6 +39,11 @@ class Tree(C.Structure):
     _fields_ = [("lmin", C.c_int32), ("lmax", C.c_int32), ("nlevels", C.c_int32),
                 ("refined", C.POINTER(C.POINTER(C.c_uint8))),
                 ("eps", C.POINTER(C.POINTER(C.c_double))),
+                ("u", C.POINTER(C.POINTER(C.c_double)))]
+
+
+class Tree3(C.Structure):
+    _fields_ = [("lmin", C.c_int32), ("depth", C.c_int32), ("eps", C.POINTER(C.c_double)),
                 ("u", C.POINTER(C.POINTER(C.c_double)))]
 
 
@@ -80,6 +85,9 @@ def lib() -> C.CDLL:
         "tmg_destroy": ([H], None),
         "tmg_last_error": ([], C.c_char_p),
         "tmg_device_count": ([], C.c_int),
+        "tmg3_create": ([P(Tree3), P(Config), P(H)], C.c_int),
+        "tmg3_rebuild": ([H, P(Tree3)], C.c_int),
+        "tmg_dim": ([H], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -119,3 +127,15 @@ class TreeArgs:
         self.eps_arr = (DP * nlev)(*[e.ctypes.data_as(DP) for e in self.eps])
         self.u_arr = (DP * nlev)(*[u.ctypes.data_as(DP) for u in self.u])
         self.struct = Tree(tree.lmin, lmax, nlev, self.ref_arr, self.eps_arr, self.u_arr)
+
+
+class TreeArgs3:
+    """3D regular tree (paper_1903_10367_b200.spacetree3d / oracle mg3d data model)."""
+
+    def __init__(self, tree):
+        L = tree.depth
+        self.eps = np.ascontiguousarray(tree.eps[L], dtype=np.float64)
+        self.u = [np.ascontiguousarray(tree.u[l], dtype=np.float64) for l in range(L + 1)]
+        DP = C.POINTER(C.c_double)
+        self.u_arr = (DP * (L + 1))(*[u.ctypes.data_as(DP) for u in self.u])
+        self.struct = Tree3(tree.lmin, L, self.eps.ctypes.data_as(DP), self.u_arr)

@@ -16,7 +16,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libtmg.so")
-SOURCES = [os.path.join(PKG, "csrc", "engine.cu")]
+SOURCES = [os.path.join(PKG, "csrc", "engine.cu"), os.path.join(PKG, "csrc", "engine3.cu")]
 DEPS = [os.path.join(PKG, "csrc", f) for f in os.listdir(os.path.join(PKG, "csrc"))] + \
     [os.path.join(ROOT, "include", "tmg.h")]
 

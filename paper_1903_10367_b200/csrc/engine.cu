@@ -10,6 +10,7 @@
 
 // single translation unit: the kernels and their __constant__ tables live here too
 #include "kernels2d.cu"
+#include "engine3.h"
 #include "tmg.h"
 
 namespace {
@@ -78,6 +79,7 @@ struct KTimer {
 }  // namespace
 
 struct tmg_handle {
+  Engine3* e3 = nullptr;  // 3D hierarchy (engine3.cu); the 2D fields are unused then
   tmg_config cfg{};
   double wt = 0.0;
   int lmin = 1, lmax = 1, ltop = 0;
@@ -740,7 +742,42 @@ int tmg_create(const tmg_tree* tree, const tmg_config* cfg, tmg_handle** out) {
   return TMG_OK;
 }
 
+int tmg3_create(const tmg_tree3* tree, const tmg_config* cfg, tmg_handle** out) {
+  if (!tree || !cfg || !out) return fail(TMG_EINVAL, "null argument");
+  *out = nullptr;
+  if (cfg->variant < 0 || cfg->variant > 6) return fail(TMG_EINVAL, "unknown solver variant");
+  if (cfg->variant == TMG_MULTIPLICATIVE_V10)
+    return fail(TMG_EINVAL, "multiplicative-v10 (dense two-grid reference) is not offered on the device");
+  if (cfg->flavor != TMG_GEOMETRIC && cfg->flavor != TMG_BOXMG)
+    return fail(TMG_EINVAL, "unknown operator flavor");
+  if (!(cfg->omega > 0.0 && cfg->omega <= 1.0)) return fail(TMG_EINVAL, "omega must lie in (0, 1]");
+  if (!(cfg->omega_hat > 0.0 && cfg->omega_hat < 1.0))
+    return fail(TMG_EINVAL, "omega_hat must lie in (0, 1)");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(TMG_ECUDA, "no CUDA device: the engine has no CPU fallback");
+  if (cfg->device < 0 || cfg->device >= ndev) return fail(TMG_EINVAL, "device index out of range");
+  CK(cudaSetDevice(cfg->device));
+  Engine3* e = nullptr;
+  int rc = e3_create(tree, cfg, &e, g_err);
+  if (rc != TMG_OK) return rc;
+  tmg_handle* h = new tmg_handle();
+  h->cfg = *cfg;
+  h->e3 = e;
+  *out = h;
+  return TMG_OK;
+}
+
+int tmg3_rebuild(tmg_handle* h, const tmg_tree3* tree) {
+  if (!h || !tree || !h->e3) return fail(TMG_EINVAL, "null argument or not a 3D handle");
+  CK(cudaSetDevice(h->cfg.device));
+  return e3_rebuild(h->e3, tree, g_err);
+}
+
+int tmg_dim(tmg_handle* h) { return (h && h->e3) ? 3 : 2; }
+
 int tmg_rebuild(tmg_handle* h, const tmg_tree* tree) {
+  if (h && h->e3) return fail(TMG_EINVAL, "3D handle: use tmg3_rebuild");
   if (!h || !tree) return fail(TMG_EINVAL, "null argument");
   CK(cudaSetDevice(h->cfg.device));
   CK(cudaStreamSynchronize(h->s));
@@ -749,6 +786,7 @@ int tmg_rebuild(tmg_handle* h, const tmg_tree* tree) {
 }
 
 int tmg_set_rhs(tmg_handle* h, int32_t level, const double* rhs) {
+  if (h && h->e3) return e3_set_rhs(h->e3, level, rhs, g_err);
   TRY(check_level(h, level));
   Level& c = h->L[level];
   if (!rhs) {
@@ -765,6 +803,7 @@ int tmg_set_rhs(tmg_handle* h, int32_t level, const double* rhs) {
 }
 
 int tmg_set_u(tmg_handle* h, int32_t level, const double* u) {
+  if (h && h->e3) return u ? e3_set_u(h->e3, level, u, g_err) : fail(TMG_EINVAL, "null array");
   TRY(check_level(h, level, true));
   if (!u) return fail(TMG_EINVAL, "null array");
   double* dst = (level == h->lmin - 1) ? h->u_below : h->L[level].u;
@@ -775,6 +814,7 @@ int tmg_set_u(tmg_handle* h, int32_t level, const double* u) {
 }
 
 int tmg_get_u(tmg_handle* h, int32_t level, double* u) {
+  if (h && h->e3) return u ? e3_get_u(h->e3, level, u, g_err) : fail(TMG_EINVAL, "null array");
   TRY(check_level(h, level, true));
   if (!u) return fail(TMG_EINVAL, "null array");
   const double* src = (level == h->lmin - 1) ? h->u_below : h->L[level].u;
@@ -785,6 +825,7 @@ int tmg_get_u(tmg_handle* h, int32_t level, double* u) {
 }
 
 int tmg_update_fas_state(tmg_handle* h) {
+  if (h && h->e3) return e3_update_fas_state(h->e3, g_err);
   if (!h) return fail(TMG_EINVAL, "null handle");
   TRY(enqueue_fas(h));
   CK(cudaStreamSynchronize(h->s));
@@ -792,6 +833,7 @@ int tmg_update_fas_state(tmg_handle* h) {
 }
 
 int tmg_cycle(tmg_handle* h, int32_t ncycles, tmg_stats* stats) {
+  if (h && h->e3) return e3_cycle(h->e3, ncycles, stats, g_err);
   if (!h) return fail(TMG_EINVAL, "null handle");
   if (ncycles < 0) return fail(TMG_EINVAL, "negative cycle count");
   TRY(ensure_graph(h));
@@ -809,6 +851,7 @@ int tmg_cycle(tmg_handle* h, int32_t ncycles, tmg_stats* stats) {
 }
 
 int tmg_residual_stats(tmg_handle* h, tmg_stats* out) {
+  if (h && h->e3 && out) return e3_residual_stats(h->e3, out, g_err);
   if (!h || !out) return fail(TMG_EINVAL, "null argument");
   TRY(enqueue_down(h, false));
   const long long first = h->host_counter++;
@@ -817,6 +860,7 @@ int tmg_residual_stats(tmg_handle* h, tmg_stats* out) {
 }
 
 int tmg_levels(tmg_handle* h, int32_t* lmin, int32_t* ltop) {
+  if (h && h->e3) return e3_levels(h->e3, lmin, ltop);
   if (!h) return fail(TMG_EINVAL, "null handle");
   if (lmin) *lmin = h->lmin;
   if (ltop) *ltop = h->ltop;
@@ -825,6 +869,7 @@ int tmg_levels(tmg_handle* h, int32_t* lmin, int32_t* ltop) {
 
 int tmg_level_counts(tmg_handle* h, int32_t level, int64_t* dof, int64_t* composite,
                      int64_t* hanging) {
+  if (h && h->e3) return e3_level_counts(h->e3, level, dof, composite, hanging, g_err);
   TRY(check_level(h, level));
   const Level& c = h->L[level];
   if (dof) *dof = c.cnt[tmg::K_DOF] + c.cnt[tmg::K_OVER];
@@ -834,6 +879,7 @@ int tmg_level_counts(tmg_handle* h, int32_t level, int64_t* dof, int64_t* compos
 }
 
 int tmg_get_kinds(tmg_handle* h, int32_t level, int8_t* out) {
+  if (h && h->e3) return e3_get_kinds(h->e3, level, out, g_err);
   TRY(check_level(h, level));
   const Level& c = h->L[level];
   std::vector<uint8_t> f(c.nv);
@@ -844,6 +890,7 @@ int tmg_get_kinds(tmg_handle* h, int32_t level, int8_t* out) {
 }
 
 int tmg_get_table(tmg_handle* h, int32_t which, int32_t level, double* out) {
+  if (h && h->e3) return e3_get_table(h->e3, which, level, out, g_err);
   TRY(check_level(h, level));
   Level& c = h->L[level];
   auto fetch = [&](const double* src, size_t count, std::vector<double>& dst) -> int {
@@ -901,6 +948,7 @@ int tmg_get_table(tmg_handle* h, int32_t which, int32_t level, double* out) {
 }
 
 int tmg_time_cycles(tmg_handle* h, int32_t ncycles, int64_t flush_bytes, float* ms) {
+  if (h && h->e3 && ms) return e3_time_cycles(h->e3, ncycles, flush_bytes, ms, g_err);
   if (!h || !ms) return fail(TMG_EINVAL, "null argument");
   TRY(ensure_graph(h));
   if (flush_bytes > 0 && h->flush_bytes < (size_t)flush_bytes) {
@@ -940,6 +988,7 @@ int tmg_time_cycles(tmg_handle* h, int32_t ncycles, int64_t flush_bytes, float* 
 
 int tmg_profile_cycles(tmg_handle* h, int32_t ncycles, int32_t cap, const char** names, float* ms,
                        int32_t* launches, int32_t* nk) {
+  if (h && h->e3) return e3_profile_cycles(h->e3, ncycles, cap, names, ms, launches, nk, g_err);
   if (!h) return fail(TMG_EINVAL, "null handle");
   std::vector<KTimer> timers;
   h->timers = &timers;
@@ -968,6 +1017,7 @@ int tmg_profile_cycles(tmg_handle* h, int32_t ncycles, int32_t cap, const char**
 }
 
 int tmg_launches_per_cycle(tmg_handle* h, int32_t* n) {
+  if (h && h->e3 && n) return e3_launches_per_cycle(h->e3, n, g_err);
   if (!h || !n) return fail(TMG_EINVAL, "null argument");
   TRY(ensure_graph(h));
   *n = h->launches;
@@ -983,6 +1033,11 @@ int tmg_debug_stamps(tmg_handle* h, unsigned long long* out, int n) {
 
 void tmg_destroy(tmg_handle* h) {
   if (!h) return;
+  if (h->e3) {
+    e3_destroy(h->e3);
+    delete h;
+    return;
+  }
   cudaSetDevice(h->cfg.device);
   if (h->s) cudaStreamSynchronize(h->s);
   free_all(h);

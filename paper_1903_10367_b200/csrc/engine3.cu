@@ -1,0 +1,776 @@
+// Host runtime of the 3D engine (regular spacetrees): level hierarchy in
+// HBM, operator setup, the per-cycle launch sequence captured in a CUDA
+// graph.  Reached through the C ABI of engine.cu (tmg3_create and the
+// dimension-dispatching tmg_* entry points).
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "engine3.h"
+#include "kernels3d.cu"
+
+namespace {
+
+using namespace t3;
+
+struct Lvl3 {
+  int l = 0, N = 0;
+  size_t nv = 0, ncell = 0;
+  double *u = nullptr, *rhs = nullptr, *g = nullptr, *rho = nullptr, *sm = nullptr, *carry = nullptr;
+  double *eff = nullptr, *coef = nullptr, *tbl = nullptr, *P = nullptr;
+  Op3 op{};
+  double w = 0.0;
+  int grid = 0, part_off = 0;
+};
+
+struct KT {
+  const char* name;
+  float ms;
+  int launches;
+};
+
+constexpr int kResident = 148 * 8;  // grid-stride kernels: 8 CTAs per SM
+
+inline unsigned nblk(size_t n, int bs = 256) { return (unsigned)((n + bs - 1) / bs); }
+
+int ipow3(int l) {
+  int r = 1;
+  for (int k = 0; k < l; ++k) r *= 3;
+  return r;
+}
+
+}  // namespace
+
+struct Engine3 {
+  tmg_config cfg{};
+  double wt = 0.0;
+  int lmin = 1, ltop = 1, lc = 1;
+  std::vector<Lvl3> L;
+  cudaStream_t s = nullptr;
+  std::vector<void*> allocs;
+  double *part_sum = nullptr, *part_max = nullptr;
+  int nparts = 0;
+  double* hist = nullptr;
+  int* counter = nullptr;
+  int cap = 1024;
+  long long host_counter = 0;
+  cudaGraphExec_t gexec = nullptr;
+  bool graph_dirty = true;
+  int launches = 0;
+  long long dofs_total = 0, updates = 0;
+  bool profiling = false;
+  std::vector<KT>* timers = nullptr;
+  struct Pending {
+    const char* name;
+    cudaEvent_t e0, e1;
+  };
+  std::vector<cudaEvent_t> ev_pool;
+  int ev_used = 0;
+  std::vector<Pending> pending;
+  void* flush_buf = nullptr;
+  size_t flush_bytes = 0;
+  std::string* err = nullptr;
+};
+
+namespace {
+
+int fail3(Engine3* e, int code, const std::string& msg) {
+  if (e && e->err) *e->err = msg;
+  return code;
+}
+
+#define CK3(call)                                                                         \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail3(e, TMG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+#define CKL3()                                                                            \
+  do {                                                                                    \
+    cudaError_t e_ = cudaGetLastError();                                                  \
+    if (e_ != cudaSuccess)                                                                \
+      return fail3(e, TMG_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define TRY3(expr)                 \
+  do {                             \
+    int rc_ = (expr);              \
+    if (rc_ != TMG_OK) return rc_; \
+  } while (0)
+
+template <class T>
+int alloc3(Engine3* e, T** p, size_t count, bool zero = true) {
+  void* q = nullptr;
+  CK3(cudaMalloc(&q, sizeof(T) * (count ? count : 1)));
+  e->allocs.push_back(q);
+  if (zero) CK3(cudaMemsetAsync(q, 0, sizeof(T) * (count ? count : 1), e->s));
+  *p = (T*)q;
+  return TMG_OK;
+}
+
+void free3(Engine3* e) {
+  if (e->gexec) {
+    cudaGraphExecDestroy(e->gexec);
+    e->gexec = nullptr;
+  }
+  for (void* p : e->allocs) cudaFree(p);
+  e->allocs.clear();
+  e->L.clear();
+  e->graph_dirty = true;
+}
+
+// --- per-launch timing (profile path, no graph) ---------------------------------
+
+int begin_k(Engine3* e, cudaEvent_t* e0) {
+  if (!e->profiling) return TMG_OK;
+  if (e->ev_used + 2 > (int)e->ev_pool.size())
+    for (int k = 0; k < 256; ++k) {
+      cudaEvent_t q;
+      CK3(cudaEventCreate(&q));
+      e->ev_pool.push_back(q);
+    }
+  *e0 = e->ev_pool[e->ev_used++];
+  CK3(cudaEventRecord(*e0, e->s));
+  return TMG_OK;
+}
+
+int end_k(Engine3* e, const char* name, cudaEvent_t e0) {
+  e->launches++;
+  if (!e->profiling) return TMG_OK;
+  cudaEvent_t e1 = e->ev_pool[e->ev_used++];
+  CK3(cudaEventRecord(e1, e->s));
+  e->pending.push_back({name, e0, e1});
+  return TMG_OK;
+}
+
+const char* kname(const char* base, int l) {
+  static char names[4][12][24];
+  static const char* bases[4] = {"k3_down", "k3_smooth", "k3_up", "k3_chain"};
+  int b = 0;
+  while (b < 4 && std::strcmp(bases[b], base) != 0) ++b;
+  if (b >= 4 || l < 0 || l > 11) return base;
+  if (!names[b][l][0]) std::snprintf(names[b][l], 24, "%s_L%d", base, l);
+  return names[b][l];
+}
+
+#define LAUNCH3(name, kernel, grid, block, arg)         \
+  do {                                                  \
+    cudaEvent_t e0_ = nullptr;                          \
+    TRY3(begin_k(e, &e0_));                             \
+    kernel<<<(grid), (block), 0, e->s>>>(arg);          \
+    CKL3();                                             \
+    TRY3(end_k(e, name, e0_));                          \
+  } while (0)
+
+// --- argument blocks ---------------------------------------------------------------
+
+int grid_for(int N, int ilo, int ihi) {
+  const long long t = (long long)((N - 2 + kTX - 1) / kTX) * ((N - 2 + kTY - 1) / kTY) *
+                      ((ihi - ilo + kTZ - 1) / kTZ);
+  return (int)std::max(1LL, std::min<long long>(t, kResident));
+}
+
+Down3 make_down(Engine3* e, int l, bool write) {
+  const int l0 = e->lmin, l1 = e->ltop;
+  Lvl3& c = e->L[l];
+  Down3 a{};
+  a.N = c.N;
+  a.l = l;
+  a.is_top = l == l1;
+  a.variant = e->cfg.variant;
+  a.write = write ? 1 : 0;
+  a.ilo = 1;
+  a.ihi = c.N - 1;
+  a.u = c.u;
+  a.rhs = c.rhs;
+  a.op = c.op;
+  if (l < l1) {
+    Lvl3& f = e->L[l + 1];
+    a.Nf = f.N;
+    a.rho_f = f.rho;
+    a.sm_f = f.sm;
+    a.P = c.P;
+  }
+  a.w = c.w;
+  a.omega = e->cfg.omega;
+  a.wt = e->wt;
+  a.ds = e->cfg.damping_scale;
+  a.hw = std::pow(3.0, -1.5 * l);
+  a.rho = (l > l0) ? c.rho : nullptr;
+  a.g = c.g;
+  a.part_sum = (l > e->lc) ? e->part_sum + c.part_off : nullptr;
+  a.part_max = (l > e->lc) ? e->part_max + c.part_off : nullptr;
+  return a;
+}
+
+Smooth3 make_smooth(Engine3* e, int l) {
+  Lvl3& c = e->L[l];
+  Smooth3 a{};
+  a.N = c.N;
+  a.ilo = 1;
+  a.ihi = c.N - 1;
+  a.x = c.rho;
+  a.sm = c.sm;
+  a.scale = e->cfg.omega * 3.0 / 8.0;  // operators.py:603-605
+  return a;
+}
+
+Up3 make_up(Engine3* e, int l) {
+  const int l0 = e->lmin, l1 = e->ltop;
+  Lvl3& c = e->L[l];
+  Up3 a{};
+  a.N = c.N;
+  a.l = l;
+  a.l0 = l0;
+  a.is_bottom = l == l0;
+  a.pi = e->cfg.variant == VAR_PI;
+  a.ilo = 1;
+  a.ihi = c.N - 1;
+  a.u = c.u;
+  a.g = c.g;
+  a.carry = (l < l1) ? c.carry : nullptr;
+  if (l > l0) {
+    Lvl3& cc = e->L[l - 1];
+    a.Nc = cc.N;
+    a.carry_c = cc.carry;
+    a.P = cc.P;
+  }
+  a.ds = e->cfg.damping_scale;
+  for (int k = l0; k < l; ++k) {
+    a.ul[k] = e->L[k].u;
+    a.Nl[k] = e->L[k].N;
+  }
+  return a;
+}
+
+const bool kJacSmooth = true;
+
+int enqueue_down(Engine3* e, bool write) {
+  const bool jac = e->cfg.variant == VAR_JAC;
+  const dim3 blk(kTX, kTY, kTZ);
+  for (int l = e->ltop; l > e->lc; --l) {
+    Down3 a = make_down(e, l, write);
+    LAUNCH3(kname("k3_down", l), k3_down, e->L[l].grid, blk, a);
+    if (jac && write && l > e->lmin && kJacSmooth) {
+      Smooth3 sa = make_smooth(e, l);
+      LAUNCH3(kname("k3_smooth", l), k3_smooth, e->L[l].grid, blk, sa);
+    }
+  }
+  Chain3 ch{};
+  ch.l0 = e->lmin;
+  ch.lc = e->lc;
+  ch.do_up = write ? 1 : 0;
+  ch.jac = jac ? 1 : 0;
+  ch.part_sum = e->part_sum;
+  ch.part_max = e->part_max;
+  ch.nparts = e->nparts;
+  ch.hist = e->hist;
+  ch.counter = e->counter;
+  ch.cap = e->cap;
+  for (int l = e->lmin; l <= e->lc; ++l) {
+    ch.down[l - e->lmin] = make_down(e, l, write);
+    ch.smooth[l - e->lmin] = make_smooth(e, l);
+    ch.up[l - e->lmin] = make_up(e, l);
+  }
+  LAUNCH3("k3_chain", k3_chain, 1, kChainBlock, ch);
+  return TMG_OK;
+}
+
+int enqueue_cycle(Engine3* e) {
+  TRY3(enqueue_down(e, true));
+  const dim3 blk(kTX, kTY, kTZ);
+  for (int l = e->lc + 1; l <= e->ltop; ++l) {
+    Up3 a = make_up(e, l);
+    LAUNCH3(kname("k3_up", l), k3_up, e->L[l].grid, blk, a);
+  }
+  return TMG_OK;
+}
+
+int ensure_graph(Engine3* e) {
+  if (!e->graph_dirty && e->gexec) return TMG_OK;
+  if (e->gexec) {
+    cudaGraphExecDestroy(e->gexec);
+    e->gexec = nullptr;
+  }
+  cudaGraph_t g;
+  CK3(cudaStreamBeginCapture(e->s, cudaStreamCaptureModeThreadLocal));
+  e->launches = 0;
+  int rc = enqueue_cycle(e);
+  cudaError_t ce = cudaStreamEndCapture(e->s, &g);
+  if (rc != TMG_OK) return rc;
+  CK3(ce);
+  CK3(cudaGraphInstantiate(&e->gexec, g, 0));
+  cudaGraphDestroy(g);
+  e->graph_dirty = false;
+  return TMG_OK;
+}
+
+// --- setup (mg3d.Engine.rebuild) ------------------------------------------------------
+
+int const_of(Engine3* e, const double* arr, size_t n, bool* is_const, double* value) {
+  int* flag;
+  TRY3(alloc3(e, &flag, 1, false));
+  const int one = 1;
+  CK3(cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, e->s));
+  k3_const_check<<<nblk(n), 256, 0, e->s>>>(arr, n, flag);
+  CKL3();
+  int hf = 0;
+  CK3(cudaMemcpyAsync(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost, e->s));
+  CK3(cudaMemcpyAsync(value, arr, sizeof(double), cudaMemcpyDeviceToHost, e->s));
+  CK3(cudaStreamSynchronize(e->s));
+  *is_const = hf != 0;
+  return TMG_OK;
+}
+
+Op3 element_op(double c, bool is_const, const double* coef) {
+  Op3 o{};
+  if (is_const) {
+    o.kind = OP_CONST;
+    o.m = c * C_D8;
+    o.se = c * C_E6;
+    o.sc = c * C_C12;
+    double E = c;  // element_diag of a constant field: 8 equal terms, sequential
+    for (int a = 1; a < 8; ++a) E = E + c;
+    o.cdiag = K_D * E;
+  } else {
+    o.kind = OP_ELEMENT;
+    o.e = coef;
+  }
+  return o;
+}
+
+int build(Engine3* e, const tmg_tree3* t) {
+  const tmg_config& cfg = e->cfg;
+  if (t->lmin < 1) return fail3(e, TMG_EINVAL, "lmin must be at least 1");
+  if (t->depth < t->lmin) return fail3(e, TMG_EINVAL, "tree has no DoF-carrying level at or above lmin");
+  if (t->depth > 7) return fail3(e, TMG_EINVAL, "depth above 7 is not supported in 3D");
+  if (!t->eps || !t->u) return fail3(e, TMG_EINVAL, "tree.eps / tree.u missing");
+  if (cfg.rtilde_true_operator)
+    return fail3(e, TMG_EINVAL, "rtilde_true_operator is not offered in 3D");
+  e->lmin = t->lmin;
+  e->ltop = t->depth;
+  const int l0 = e->lmin, l1 = e->ltop;
+  e->L.assign(l1 + 1, Lvl3{});
+  for (int l = l0; l <= l1; ++l) {
+    Lvl3& c = e->L[l];
+    c.l = l;
+    c.N = ipow3(l) + 1;
+    c.nv = (size_t)c.N * c.N * c.N;
+    c.ncell = (size_t)(c.N - 1) * (c.N - 1) * (c.N - 1);
+    if (!t->u[l]) return fail3(e, TMG_EINVAL, "tree.u missing a level");
+  }
+  // material: eff_eps top-down (child means), coefficient e = eff * h
+  for (int l = l1; l >= l0; --l) {
+    Lvl3& c = e->L[l];
+    TRY3(alloc3(e, &c.eff, c.ncell, false));
+    TRY3(alloc3(e, &c.coef, c.ncell, false));
+    if (l == l1) {
+      CK3(cudaMemcpyAsync(c.eff, t->eps, sizeof(double) * c.ncell, cudaMemcpyHostToDevice, e->s));
+    } else {
+      k3_child_mean<<<nblk(c.ncell), 256, 0, e->s>>>(c.eff, e->L[l + 1].eff, c.N - 1);
+      CKL3();
+    }
+    k3_scale<<<nblk(c.ncell), 256, 0, e->s>>>(c.coef, c.eff, std::pow(3.0, -(double)l), c.ncell);
+    CKL3();
+  }
+  for (int l = l0; l <= l1; ++l) {
+    Lvl3& c = e->L[l];
+    c.w = (cfg.variant == VAR_EXP) ? std::pow(cfg.omega_hat, (double)(l1 - l)) : cfg.omega;
+  }
+  int* deg;
+  TRY3(alloc3(e, &deg, 1));
+  if (cfg.flavor == TMG_GEOMETRIC) {
+    for (int l = l0; l <= l1; ++l) {
+      Lvl3& c = e->L[l];
+      bool kc;
+      double v;
+      TRY3(const_of(e, c.coef, c.ncell, &kc, &v));
+      c.op = element_op(v, kc, c.coef);
+    }
+  } else {
+    Lvl3& top = e->L[l1];
+    bool kc;
+    double v;
+    TRY3(const_of(e, top.coef, top.ncell, &kc, &v));
+    top.op = element_op(v, kc, top.coef);
+    Rows raw{top.N, nullptr, top.coef};
+    for (int l = l1 - 1; l >= l0; --l) {
+      Lvl3& c = e->L[l];
+      const int nc = c.N - 1;
+      TRY3(alloc3(e, &c.P, 125 * c.nv, false));
+      k3_p_init<<<nblk(c.nv), 256, 0, e->s>>>(c.P, c.nv);
+      CKL3();
+      for (int ax = 0; ax < 3; ++ax) {
+        k3_edges<<<nblk((size_t)nc * c.N * c.N, 128), 128, 0, e->s>>>(c.P, nc, ax, raw, deg);
+        CKL3();
+      }
+      for (int nx = 0; nx < 3; ++nx) {
+        k3_faces<<<nblk((size_t)c.N * nc * nc, 128), 128, 0, e->s>>>(c.P, nc, nx, raw);
+        CKL3();
+      }
+      k3_cells<<<nblk((size_t)nc * nc * nc, 128), 128, 0, e->s>>>(c.P, nc, raw);
+      CKL3();
+      TRY3(alloc3(e, &c.tbl, 27 * c.nv, false));
+      k3_assemble<<<nblk(c.nv), 256, 0, e->s>>>(c.tbl, Rows{c.N, nullptr, c.coef});
+      CKL3();
+      if (c.N > 2) {
+        const size_t ni = (size_t)(c.N - 2) * (c.N - 2) * (c.N - 2);
+        k3_rap<<<nblk(ni, 128), 128, 0, e->s>>>(c.tbl, nc, c.P, raw);
+        CKL3();
+      }
+      c.op = Op3{};
+      c.op.kind = OP_TABLE;
+      c.op.tbl = c.tbl;
+      raw = Rows{c.N, c.tbl, nullptr};
+    }
+  }
+  int hdeg = 0;
+  CK3(cudaMemcpyAsync(&hdeg, deg, sizeof(int), cudaMemcpyDeviceToHost, e->s));
+  CK3(cudaStreamSynchronize(e->s));
+  if (hdeg) return fail3(e, TMG_EDEGENERATE, "degenerate collapsed stencil in face-point solve");
+
+  // counts (solvers.py:449-459)
+  long long sum = 0, lt = 0, gt = 0;
+  for (int l = l0; l <= l1; ++l) {
+    const long long d = (long long)(e->L[l].N - 2) * (e->L[l].N - 2) * (e->L[l].N - 2);
+    sum += d;
+    if (l < l1) lt += d;
+    if (l > l0) gt += d;
+  }
+  e->dofs_total = (long long)(e->L[l1].N - 2) * (e->L[l1].N - 2) * (e->L[l1].N - 2);
+  e->updates = sum + (cfg.variant == VAR_JAC ? lt : 0) + (cfg.variant == VAR_PI ? gt : 0);
+
+  // chain levels: <= 1024 vertices, at most kMaxChain
+  e->lc = l0;
+  for (int l = l0; l <= l1 && l - l0 < kMaxChain; ++l)
+    if (e->L[l].nv <= 1024) e->lc = l;
+  // work vectors
+  const bool jac = cfg.variant == VAR_JAC;
+  int parts = 0;
+  for (int l = l0; l <= l1; ++l) {
+    Lvl3& c = e->L[l];
+    TRY3(alloc3(e, &c.u, c.nv, false));
+    CK3(cudaMemcpyAsync(c.u, t->u[l], sizeof(double) * c.nv, cudaMemcpyHostToDevice, e->s));
+    TRY3(alloc3(e, &c.g, c.nv));
+    if (l > l0) TRY3(alloc3(e, &c.rho, c.nv));
+    if (l > l0 && jac) TRY3(alloc3(e, &c.sm, c.nv));
+    if (l < l1) TRY3(alloc3(e, &c.carry, c.nv));
+    c.grid = grid_for(c.N, 1, c.N - 1);
+    if (l > e->lc) {
+      c.part_off = parts;
+      parts += c.grid;
+    }
+  }
+  e->nparts = parts;
+  TRY3(alloc3(e, &e->part_sum, parts));
+  TRY3(alloc3(e, &e->part_max, parts));
+  TRY3(alloc3(e, &e->hist, 2 * e->cap));
+  TRY3(alloc3(e, &e->counter, 1));
+  e->host_counter = 0;
+  CK3(cudaStreamSynchronize(e->s));
+  e->graph_dirty = true;
+  return TMG_OK;
+}
+
+int check_level(Engine3* e, int level) {
+  if (level < e->lmin || level > e->ltop)
+    return fail3(e, TMG_EINVAL, "level " + std::to_string(level) + " outside [lmin, ltop]");
+  return TMG_OK;
+}
+
+int read_stats(Engine3* e, long long first, int count, tmg_stats* out) {
+  std::vector<double> hh(2 * e->cap);
+  CK3(cudaMemcpyAsync(hh.data(), e->hist, sizeof(double) * hh.size(), cudaMemcpyDeviceToHost, e->s));
+  CK3(cudaStreamSynchronize(e->s));
+  for (int k = 0; k < count; ++k) {
+    const long long slot = (first + k) % e->cap;
+    out[k].l2h = hh[2 * slot];
+    out[k].linf = hh[2 * slot + 1];
+    out[k].dofs = e->dofs_total;
+    out[k].updates = e->updates;
+  }
+  return TMG_OK;
+}
+
+struct ErrScope {
+  Engine3* e;
+  ErrScope(Engine3* e_, std::string& err) : e(e_) { e->err = &err; }
+  ~ErrScope() { e->err = nullptr; }
+};
+
+}  // namespace
+
+// ============================================================================
+// internal interface (engine3.h)
+// ============================================================================
+
+int e3_create(const tmg_tree3* t, const tmg_config* cfg, Engine3** out, std::string& err) {
+  Engine3* e = new Engine3();
+  ErrScope es(e, err);
+  e->cfg = *cfg;
+  e->wt = std::isnan(cfg->omega_tilde) ? cfg->omega : cfg->omega_tilde;
+  if (cudaStreamCreateWithFlags(&e->s, cudaStreamNonBlocking) != cudaSuccess) {
+    err = "stream creation failed";
+    delete e;
+    return TMG_ECUDA;
+  }
+  int rc = build(e, t);
+  if (rc != TMG_OK) {
+    e->err = nullptr;
+    e3_destroy(e);
+    return rc;
+  }
+  *out = e;
+  return TMG_OK;
+}
+
+int e3_rebuild(Engine3* e, const tmg_tree3* t, std::string& err) {
+  ErrScope es(e, err);
+  CK3(cudaStreamSynchronize(e->s));
+  free3(e);
+  return build(e, t);
+}
+
+void e3_destroy(Engine3* e) {
+  if (!e) return;
+  if (e->s) cudaStreamSynchronize(e->s);
+  free3(e);
+  for (auto q : e->ev_pool) cudaEventDestroy(q);
+  if (e->flush_buf) cudaFree(e->flush_buf);
+  if (e->s) cudaStreamDestroy(e->s);
+  delete e;
+}
+
+int e3_set_rhs(Engine3* e, int level, const double* rhs, std::string& err) {
+  ErrScope es(e, err);
+  TRY3(check_level(e, level));
+  Lvl3& c = e->L[level];
+  if (!rhs) {
+    if (c.rhs) {
+      c.rhs = nullptr;
+      e->graph_dirty = true;
+    }
+    return TMG_OK;
+  }
+  if (!c.rhs) {
+    TRY3(alloc3(e, &c.rhs, c.nv, false));
+    e->graph_dirty = true;
+  }
+  CK3(cudaMemcpyAsync(c.rhs, rhs, sizeof(double) * c.nv, cudaMemcpyHostToDevice, e->s));
+  CK3(cudaStreamSynchronize(e->s));
+  return TMG_OK;
+}
+
+int e3_set_u(Engine3* e, int level, const double* u, std::string& err) {
+  ErrScope es(e, err);
+  TRY3(check_level(e, level));
+  CK3(cudaMemcpyAsync(e->L[level].u, u, sizeof(double) * e->L[level].nv, cudaMemcpyHostToDevice, e->s));
+  CK3(cudaStreamSynchronize(e->s));
+  return TMG_OK;
+}
+
+int e3_get_u(Engine3* e, int level, double* u, std::string& err) {
+  ErrScope es(e, err);
+  TRY3(check_level(e, level));
+  CK3(cudaMemcpyAsync(u, e->L[level].u, sizeof(double) * e->L[level].nv, cudaMemcpyDeviceToHost, e->s));
+  CK3(cudaStreamSynchronize(e->s));
+  return TMG_OK;
+}
+
+int e3_update_fas_state(Engine3* e, std::string& err) {
+  ErrScope es(e, err);
+  for (int l = e->ltop - 1; l >= e->lmin; --l) {
+    const int n = e->L[l].N - 2;
+    if (n <= 0) continue;
+    k3_inject<<<nblk((size_t)n * n * n), 256, 0, e->s>>>(e->L[l].u, e->L[l].N, e->L[l + 1].u, e->L[l + 1].N);
+    CKL3();
+  }
+  CK3(cudaStreamSynchronize(e->s));
+  return TMG_OK;
+}
+
+int e3_cycle(Engine3* e, int ncycles, tmg_stats* stats, std::string& err) {
+  ErrScope es(e, err);
+  if (ncycles < 0) return fail3(e, TMG_EINVAL, "negative cycle count");
+  TRY3(ensure_graph(e));
+  int done = 0;
+  while (done < ncycles) {
+    const int chunk = std::min(ncycles - done, e->cap);
+    const long long first = e->host_counter;
+    for (int k = 0; k < chunk; ++k) CK3(cudaGraphLaunch(e->gexec, e->s));
+    e->host_counter += chunk;
+    if (stats) TRY3(read_stats(e, first, chunk, stats + done));
+    else CK3(cudaStreamSynchronize(e->s));
+    done += chunk;
+  }
+  return TMG_OK;
+}
+
+int e3_residual_stats(Engine3* e, tmg_stats* out, std::string& err) {
+  ErrScope es(e, err);
+  TRY3(enqueue_down(e, false));
+  const long long first = e->host_counter++;
+  return read_stats(e, first, 1, out);
+}
+
+int e3_levels(Engine3* e, int32_t* lmin, int32_t* ltop) {
+  if (lmin) *lmin = e->lmin;
+  if (ltop) *ltop = e->ltop;
+  return TMG_OK;
+}
+
+int e3_level_counts(Engine3* e, int level, int64_t* dof, int64_t* composite, int64_t* hanging,
+                    std::string& err) {
+  ErrScope es(e, err);
+  TRY3(check_level(e, level));
+  const long long n = e->L[level].N - 2;
+  if (dof) *dof = n * n * n;
+  if (composite) *composite = (level == e->ltop) ? n * n * n : 0;
+  if (hanging) *hanging = 0;
+  return TMG_OK;
+}
+
+int e3_get_kinds(Engine3* e, int level, int8_t* out, std::string& err) {
+  ErrScope es(e, err);
+  TRY3(check_level(e, level));
+  const int N = e->L[level].N;
+  const int8_t inner = (level == e->ltop) ? 1 : 4;  // INTERIOR_DOF / COARSE_OVERLAPPED
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < N; ++j)
+      for (int k = 0; k < N; ++k) {
+        const bool b = i == 0 || j == 0 || k == 0 || i == N - 1 || j == N - 1 || k == N - 1;
+        out[((size_t)i * N + j) * N + k] = b ? 2 : inner;
+      }
+  return TMG_OK;
+}
+
+int e3_get_table(Engine3* e, int which, int level, double* out, std::string& err) {
+  ErrScope es(e, err);
+  TRY3(check_level(e, level));
+  Lvl3& c = e->L[level];
+  auto fetch = [&](const double* src, size_t count, std::vector<double>& dst) -> int {
+    dst.resize(count);
+    CK3(cudaMemcpyAsync(dst.data(), src, sizeof(double) * count, cudaMemcpyDeviceToHost, e->s));
+    CK3(cudaStreamSynchronize(e->s));
+    return TMG_OK;
+  };
+  std::vector<double> buf;
+  switch (which) {
+    case TMG_TABLE_EFFEPS:
+      TRY3(fetch(c.eff, c.ncell, buf));
+      std::memcpy(out, buf.data(), sizeof(double) * c.ncell);
+      return TMG_OK;
+    case TMG_TABLE_A: {
+      const double* src = c.tbl;
+      if (!src) {
+        double* tmp;
+        TRY3(alloc3(e, &tmp, 27 * c.nv, false));
+        k3_assemble<<<nblk(c.nv), 256, 0, e->s>>>(tmp, Rows{c.N, nullptr, c.coef});
+        CKL3();
+        src = tmp;
+      }
+      TRY3(fetch(src, 27 * c.nv, buf));
+      for (size_t v = 0; v < c.nv; ++v)
+        for (int k = 0; k < 27; ++k) out[v * 27 + k] = buf[k * c.nv + v];
+      return TMG_OK;
+    }
+    case TMG_TABLE_P: {
+      if (!c.P) return fail3(e, TMG_EINVAL, "no P table on this level");
+      TRY3(fetch(c.P, 125 * c.nv, buf));
+      for (size_t v = 0; v < c.nv; ++v)
+        for (int k = 0; k < 125; ++k) out[v * 125 + k] = buf[k * c.nv + v];
+      return TMG_OK;
+    }
+    default:
+      return fail3(e, TMG_EINVAL, "table not available in 3D");
+  }
+}
+
+int e3_time_cycles(Engine3* e, int ncycles, int64_t flush_bytes, float* ms, std::string& err) {
+  ErrScope es(e, err);
+  TRY3(ensure_graph(e));
+  if (flush_bytes > 0 && e->flush_bytes < (size_t)flush_bytes) {
+    if (e->flush_buf) cudaFree(e->flush_buf);
+    e->flush_buf = nullptr;
+    CK3(cudaMalloc(&e->flush_buf, (size_t)flush_bytes));
+    e->flush_bytes = (size_t)flush_bytes;
+  }
+  const int ne = flush_bytes > 0 ? 2 * ncycles : 2;
+  std::vector<cudaEvent_t> ev(ne);
+  for (auto& q : ev) CK3(cudaEventCreate(&q));
+  CK3(cudaStreamSynchronize(e->s));
+  if (flush_bytes > 0) {
+    for (int k = 0; k < ncycles; ++k) {
+      CK3(cudaMemsetAsync(e->flush_buf, k & 0xff, (size_t)flush_bytes, e->s));
+      CK3(cudaEventRecord(ev[2 * k], e->s));
+      CK3(cudaGraphLaunch(e->gexec, e->s));
+      CK3(cudaEventRecord(ev[2 * k + 1], e->s));
+    }
+  } else {
+    CK3(cudaEventRecord(ev[0], e->s));
+    for (int k = 0; k < ncycles; ++k) CK3(cudaGraphLaunch(e->gexec, e->s));
+    CK3(cudaEventRecord(ev[1], e->s));
+  }
+  CK3(cudaStreamSynchronize(e->s));
+  e->host_counter += ncycles;
+  float total = 0.f;
+  for (int k = 0; k < ne / 2; ++k) {
+    float t = 0.f;
+    CK3(cudaEventElapsedTime(&t, ev[2 * k], ev[2 * k + 1]));
+    total += t;
+  }
+  *ms = total;
+  for (auto& q : ev) cudaEventDestroy(q);
+  return TMG_OK;
+}
+
+int e3_profile_cycles(Engine3* e, int ncycles, int cap, const char** names, float* ms,
+                      int32_t* launches, int32_t* nk, std::string& err) {
+  ErrScope es(e, err);
+  std::vector<KT> timers;
+  e->profiling = true;
+  int rc = TMG_OK;
+  for (int k = 0; k < ncycles && rc == TMG_OK; ++k) {
+    rc = enqueue_cycle(e);
+    e->host_counter++;
+  }
+  e->profiling = false;
+  if (rc == TMG_OK) {
+    if (cudaStreamSynchronize(e->s) != cudaSuccess) rc = fail3(e, TMG_ECUDA, "profile sync failed");
+    for (auto& p : e->pending) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, p.e0, p.e1);
+      bool found = false;
+      for (auto& q : timers)
+        if (std::strcmp(q.name, p.name) == 0) {
+          q.ms += t;
+          q.launches++;
+          found = true;
+          break;
+        }
+      if (!found) timers.push_back({p.name, t, 1});
+    }
+  }
+  e->pending.clear();
+  e->ev_used = 0;
+  if (rc != TMG_OK) return rc;
+  int n = 0;
+  for (auto& q : timers) {
+    if (n >= cap) break;
+    names[n] = q.name;
+    ms[n] = q.ms;
+    launches[n] = q.launches;
+    ++n;
+  }
+  *nk = n;
+  return TMG_OK;
+}
+
+int e3_launches_per_cycle(Engine3* e, int32_t* n, std::string& err) {
+  ErrScope es(e, err);
+  TRY3(ensure_graph(e));
+  *n = e->launches;
+  return TMG_OK;
+}

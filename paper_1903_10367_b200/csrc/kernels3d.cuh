@@ -1,0 +1,107 @@
+// 3D engine (regular spacetrees, BASELINE configs 3 and 5): argument blocks
+// and fp64 device helpers.
+//
+// There is no 3D reference; the per-element expression DAGs are the ones
+// oracle/mg3d.py defines (and documents), so the kernels reproduce the
+// oracle's iterates bit for bit.  Compiled with --fmad=false.
+//
+// Layout: level l, N = 3^l + 1 vertices per axis, vertex v = (i*N + j)*N + k
+// (k contiguous); cells n = N-1 per axis, (ci*n + cj)*n + ck.  Every cycle
+// kernel works on interior vertices only (boundary vertices are Dirichlet:
+// their work vectors stay 0 and their u never changes), so no stencil,
+// restriction or prolongation footprint ever leaves the grid.
+//
+// Multi-GPU: kernels take the vertex-plane range [ilo, ihi) they own and
+// plane-shifted base pointers, so a slab with halo planes is addressed with
+// global indices.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace t3 {
+
+constexpr int kTX = 32, kTY = 4, kTZ = 2;  // threads along k, j, i
+constexpr int kBlock = kTX * kTY * kTZ;
+constexpr int kChainBlock = 512;
+constexpr int kMaxLevels = 10;
+
+enum OpKind : int { OP_CONST = 0, OP_ELEMENT = 1, OP_TABLE = 2 };
+enum Variant : int { VAR_ADDITIVE = 0, VAR_EXP = 1, VAR_BPX = 2, VAR_AFACC = 3, VAR_PI = 4, VAR_JAC = 5 };
+
+constexpr double K_D = 1.0 / 3.0;
+constexpr double K_E = 1.0 / 12.0;
+constexpr double C_D8 = 8.0 / 3.0;
+constexpr double C_E6 = 1.0 / 6.0;
+constexpr double C_C12 = 1.0 / 12.0;
+
+// A level operator (oracle mg3d.Op).
+struct Op3 {
+  int kind;
+  double m, se, sc;   // const: c*(8/3), c*(1/6), c*(1/12)
+  double cdiag;       // const: K_D * (c + c + ... 8 times, sequential)
+  const double* e;    // element: per-cell coefficient eff*h
+  const double* tbl;  // table: 27 planes over the vertex grid, plane tap = (di+1)*9+(dj+1)*3+(dk+1)
+};
+
+struct Grid {
+  int N;               // vertices per axis
+  size_t nv;           // N^3 (plane stride for tables)
+};
+
+// One level of the fine -> coarse sweep (oracle Engine.advance, solvers.py:345-375).
+struct Down3 {
+  int N, l, is_top, variant, write;
+  int ilo, ihi;        // interior vertex planes computed: [ilo, ihi)
+  const double* u;
+  const double* rhs;   // or nullptr
+  Op3 op;
+  // finer level (restriction sources), when !is_top
+  int Nf;
+  const double* rho_f;   // rho_{l+1} (= rdof on regular trees)
+  const double* sm_f;    // A1(rdof_{l+1}) * s (adaFACx)
+  const double* P;       // 125 planes over this level's vertex grid (boxmg) or nullptr (d-linear)
+  double w, omega, wt, ds, hw;
+  double* rho;           // this level's rho (l > l0) or nullptr
+  double* g;             // d - dtil
+  double* part_sum;
+  double* part_max;
+};
+
+// R~ smoothing of a level's rdof: sm = A1(rdof) * ((omega*3)/8) at interior vertices.
+struct Smooth3 {
+  int N, ilo, ihi;
+  const double* x;
+  double* sm;
+  double scale;
+};
+
+// One level of the coarse -> fine carry (solvers.py:377-395) + FAS injection walk-down.
+struct Up3 {
+  int N, l, l0, is_bottom, pi, ilo, ihi;
+  double* u;
+  const double* g;
+  double* carry;        // this level's carry (l < top) or nullptr
+  int Nc;
+  const double* carry_c;
+  const double* P;      // level l-1's P planes (boxmg) or nullptr
+  double ds;
+  double* ul[kMaxLevels];  // u of the coarser levels for the injection walk-down
+  int Nl[kMaxLevels];
+};
+
+constexpr int kMaxChain = 3;
+struct Chain3 {
+  int l0, lc, do_up, jac;
+  const double* part_sum;
+  const double* part_max;
+  int nparts;
+  double* hist;
+  int* counter;
+  int cap;
+  Down3 down[kMaxChain];
+  Smooth3 smooth[kMaxChain];
+  Up3 up[kMaxChain];
+};
+
+}  // namespace t3

@@ -121,7 +121,9 @@ class _TableView:
         self.eng, self.l = eng, l
 
     def table(self) -> np.ndarray:
-        return self.eng._get_table(_abi.TABLE_A, self.l, (9,)).reshape(self.eng._nv_shape(self.l) + (3, 3))
+        d = self.eng.dim
+        return self.eng._get_table(_abi.TABLE_A, self.l, (3**d,)).reshape(
+            self.eng._nv_shape(self.l) + (3,) * d)
 
     def diag(self) -> np.ndarray:
         return self.eng._get_table(_abi.TABLE_DIAG, self.l, ()).reshape(self.eng._nv_shape(self.l))
@@ -138,10 +140,15 @@ class _TransferView:
     def p_table(self):
         if self.eng.cfg.flavor != "boxmg":
             return None
+        if self.eng.dim == 3:  # fine offsets -2..2 (the +-3 rows of the 2D layout are empty)
+            return self.eng._get_table(_abi.TABLE_P, self.l, (125,)).reshape(
+                self.eng._nv_shape(self.l) + (5, 5, 5))
         return self.eng._get_table(_abi.TABLE_P, self.l, (49,)).reshape(self.eng._nv_shape(self.l) + (7, 7))
 
     @property
     def rtilde(self):
+        if self.eng.dim == 3:  # 3D applies R~ as R(A1 x * s) without a table
+            return None
         try:
             return self.eng._get_table(_abi.TABLE_RT, self.l, (49,)).reshape(
                 self.eng._nv_shape(self.l) + (7, 7))
@@ -153,6 +160,7 @@ class GpuEngine:
     """B200 engine behind the ReferenceEngine protocol (solvers.py:129-492)."""
 
     def __init__(self, tree, cfg: SolverConfig, device: int = 0, sync: str = "eager"):
+        self.dim = 3 if np.ndim(tree.u[-1]) == 3 else 2
         if sync not in ("eager", "lazy"):
             raise ValueError("sync must be 'eager' or 'lazy'")
         if cfg.variant == "multiplicative-v10":
@@ -177,9 +185,13 @@ class GpuEngine:
 
     def _create(self) -> None:
         L = _abi.lib()
-        targs = _abi.TreeArgs(self.tree)
         cs = self._cfg_struct()
-        _abi.check(L.tmg_create(C.byref(targs.struct), C.byref(cs), C.byref(self._h)))
+        if self.dim == 3:
+            targs = _abi.TreeArgs3(self.tree)
+            _abi.check(L.tmg3_create(C.byref(targs.struct), C.byref(cs), C.byref(self._h)))
+        else:
+            targs = _abi.TreeArgs(self.tree)
+            _abi.check(L.tmg_create(C.byref(targs.struct), C.byref(cs), C.byref(self._h)))
         self._after_build()
 
     def _after_build(self) -> None:
@@ -213,15 +225,19 @@ class GpuEngine:
 
     def rebuild(self) -> None:
         """(Re)build stencils, transfers and masks from the tree (solvers.py:145-255)."""
-        targs = _abi.TreeArgs(self.tree)
-        _abi.check(_abi.lib().tmg_rebuild(self._h, C.byref(targs.struct)))
+        if self.dim == 3:
+            targs = _abi.TreeArgs3(self.tree)
+            _abi.check(_abi.lib().tmg3_rebuild(self._h, C.byref(targs.struct)))
+        else:
+            targs = _abi.TreeArgs(self.tree)
+            _abi.check(_abi.lib().tmg_rebuild(self._h, C.byref(targs.struct)))
         self._after_build()
 
     # -- host <-> device state ---------------------------------------------------
     def push(self) -> None:
         """Upload every level of tree.u (host authoritative)."""
         L = _abi.lib()
-        for l in range(self.lmin - 1, self.ltop + 1):
+        for l in range(self.lmin - (1 if self.dim == 2 else 0), self.ltop + 1):
             a = np.ascontiguousarray(self.tree.u[l], dtype=np.float64)
             _abi.check(L.tmg_set_u(self._h, l, _abi.ptr(a)))
         self._host_stale = False
@@ -324,7 +340,7 @@ class GpuEngine:
 
     def eff_eps(self, l: int) -> np.ndarray:
         n = 3**l
-        return self._get_table(_abi.TABLE_EFFEPS, l, (), cells=True).reshape(n, n)
+        return self._get_table(_abi.TABLE_EFFEPS, l, (), cells=True).reshape((n,) * self.dim)
 
     def level_counts(self) -> dict:
         return {l: (self._level_dofs[l], self._composite[l], self._hanging[l])
@@ -332,11 +348,11 @@ class GpuEngine:
 
     def _nv_shape(self, l):
         N = 3**l + 1
-        return (N, N)
+        return (N,) * self.dim
 
     def _get_table(self, which, l, tail, cells=False):
         n = 3**l
-        count = n * n if cells else (n + 1) ** 2
+        count = n**self.dim if cells else (n + 1) ** self.dim
         out = np.empty((count,) + tuple(tail))
         _abi.check(_abi.lib().tmg_get_table(self._h, which, l, _abi.ptr(out)))
         return out

@@ -23,8 +23,10 @@ from dataclasses import dataclass, field as dc_field
 import numpy as np
 
 from .spacetree import CellId, Spacetree, VertexKind, build_regular
+from .spacetree3d import Spacetree3
 
-__all__ = ["Workload", "config1", "config2", "config4", "annulus_tree", "seeded_rhs", "by_name"]
+__all__ = ["Workload", "config1", "config2", "config3", "config4", "config5", "annulus_tree",
+           "seeded_rhs", "by_name"]
 
 
 @dataclass
@@ -44,7 +46,13 @@ class Workload:
 
     def fine_dofs(self) -> int:
         """N_fine: composite DoFs of the finest level (the metric's numerator)."""
+        if getattr(self.tree, "dim", 2) == 3:
+            return (3**self.ltop - 1) ** 3
         return int((self.tree.vertex_kinds(self.ltop) == VertexKind.INTERIOR_DOF).sum())
+
+    @property
+    def dim(self) -> int:
+        return getattr(self.tree, "dim", 2)
 
 
 def _zero_u(tree: Spacetree) -> None:
@@ -143,11 +151,55 @@ def config4(base: int = 4, lmax: int = 8, seed: int = 0, cycles: int = 200,
                     cycles, target, seeded_rhs(tree, rng), seed)
 
 
+def seeded_rhs3(tree: Spacetree3, rng: np.random.Generator) -> dict:
+    """b = h^3 f on the interior vertices of the finest level (the only composite DoFs)."""
+    L = tree.depth
+    n = 3**L
+    f = rng.uniform(-1.0, 1.0, (n - 1,) * 3)
+    h = 3.0 ** -L
+    b = np.zeros((n + 1,) * 3)
+    b[1:-1, 1:-1, 1:-1] = (h * h * h) * f
+    return {L: b}
+
+
+def config3(levels: int = 5, seed: int = 0, cycles: int = 100) -> Workload:
+    """3D Poisson, eps = 1, regular depth 5, adaFACx, d-linear (BASELINE configs[2])."""
+    tree = Spacetree3(levels)
+    rng = np.random.default_rng(seed)
+    return Workload(f"c3-poisson3d-L{levels}-adafacjac-geometric", tree, "adafac-jac", "geometric",
+                    cycles, None, seeded_rhs3(tree, rng), seed)
+
+
+def config5(levels: int = 6, block: int | None = None, seed: int = 0, cycles: int = 20) -> Workload:
+    """3D adaFACx + BoxMG, eps log-uniform in [1e-2, 1e2] per 27^3-cell block (BASELINE configs[4]).
+
+    ``block`` defaults to 27 cells at depth 6 and scales as 3**(levels-3), so
+    smaller depths keep 27^3 blocks of the domain.
+    """
+    tree = Spacetree3(levels)
+    rng = np.random.default_rng(seed)
+    n = 3**levels
+    blk = block if block is not None else 3 ** max(levels - 3, 0)
+    nb = n // blk
+    blocks = 10.0 ** rng.uniform(-2.0, 2.0, (nb, nb, nb))
+    eps = np.empty((n, n, n))
+    eps.reshape(nb, blk, nb, blk, nb, blk)[...] = blocks[:, None, :, None, :, None]
+    tree.eps[levels] = eps
+    return Workload(f"c5-blocks3d-L{levels}-adafacjac-boxmg", tree, "adafac-jac", "boxmg",
+                    cycles, None, seeded_rhs3(tree, rng), seed)
+
+
 def by_name(name: str) -> Workload:
     table = {
         "config1": config1, "config2": config2, "config4": config4,
         "config2-small": lambda: config2(levels=4, cycles=30),
         "config4-small": lambda: config4(base=2, lmax=5, cycles=30),
+        "config3": config3, "config5": config5,
+        "config3-small": lambda: config3(levels=3, cycles=30),
+        "config5-small": lambda: config5(levels=3, cycles=10),
+        "config5-L4": lambda: config5(levels=4, cycles=10),
+        "config3-L4": lambda: config3(levels=4, cycles=12),
+        "config5-L5": lambda: config5(levels=5, cycles=10),
     }
     if name not in table:
         raise ValueError(f"unknown workload {name!r}; choose from {sorted(table)}")

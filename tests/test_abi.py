@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     txt = open(os.path.join(ROOT, "include", "tmg.h")).read()
-    return sorted(set(re.findall(r"\b(tmg_[a-z_0-9]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(tmg3?_[a-z_0-9]+)\s*\(", txt)))
 
 
 def test_library_builds_and_exports_header_symbols():

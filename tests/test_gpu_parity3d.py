@@ -1,0 +1,119 @@
+"""GPU parity of the 3D engine (libtmg.so through GpuEngine) against the 3D oracle.
+
+There is no 3D reference (treemg is 2D only); the oracle ``oracle/mg3d.py``
+defines the fp64 expression DAG of every 3D operation and the kernels evaluate
+the same DAG, so the bar is **bitwise**: final ``u`` on every level with
+``array_equal``, P and Galerkin tables with ``array_equal``; the residual
+norms differ only by the reduction order of the sum of squares (rtol 1e-13).
+Larger sizes are checked against committed fixtures (tests/golden3d, made by
+tests/golden3d/make_golden3d.py from the oracle): per-cycle history and
+SHA-256 of the final iterate.
+"""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import mg3d
+from paper_1903_10367_b200 import GpuEngine, SolverConfig, workloads
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def oracle_run(wl, n, variant=None, flavor=None, **kw):
+    t = mg3d.Tree(wl.tree.depth, wl.tree.lmin)
+    t.eps[wl.tree.depth] = wl.tree.eps[wl.tree.depth].copy()
+    for l in range(len(t.u)):
+        t.u[l] = wl.tree.u[l].copy()
+    cfg = mg3d.Config(variant=variant or wl.variant, flavor=flavor or wl.flavor, **kw)
+    e = mg3d.Engine(t, cfg)
+    e.rhs.update({l: b.copy() for l, b in wl.rhs.items()})
+    hist = [e.advance() for _ in range(n)]
+    return t, e, hist
+
+
+def gpu_run(wl, n, variant=None, flavor=None, **kw):
+    cfg = SolverConfig(variant=variant or wl.variant, flavor=flavor or wl.flavor, **kw)
+    eng = GpuEngine(wl.tree, cfg, sync="lazy")
+    eng.rhs.update(wl.rhs)
+    hist = eng.advance_many(n)
+    eng.pull()
+    return eng, hist
+
+
+def check(wl, eng, hist, t, e, ohist):
+    np.testing.assert_allclose([s.l2h for s in hist], [s.l2h for s in ohist], rtol=1e-13, atol=0)
+    np.testing.assert_allclose([s.linf for s in hist], [s.linf for s in ohist], rtol=0, atol=0)
+    assert [s.dofs for s in hist] == [s.dofs for s in ohist]
+    assert [s.updates for s in hist] == [s.updates for s in ohist]
+    for l in range(wl.tree.lmin, wl.tree.depth + 1):
+        assert np.array_equal(wl.tree.u[l], t.u[l]), f"u level {l} not bitwise equal"
+
+
+VARIANTS = ["additive", "additive-exp", "bpx", "afacc", "adafac-pi", "adafac-jac"]
+
+
+@pytest.mark.parametrize("flavor", ["geometric", "boxmg"])
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_3d_small_all_variants_bitwise(variant, flavor):
+    wl = workloads.config5(levels=2, block=3) if flavor == "boxmg" else workloads.config3(levels=2)
+    t, e, oh = oracle_run(wl, 6, variant, flavor)
+    eng, h = gpu_run(wl, 6, variant, flavor)
+    check(wl, eng, h, t, e, oh)
+
+
+@pytest.mark.parametrize("name", ["config3-small", "config5-small"])
+def test_3d_level3_bitwise(name):
+    wl = workloads.by_name(name)
+    t, e, oh = oracle_run(wl, 8)
+    eng, h = gpu_run(wl, 8)
+    check(wl, eng, h, t, e, oh)
+    rs = eng.residual_stats()
+    ors = e.residual_stats()
+    np.testing.assert_allclose([rs.l2h, rs.linf], [ors.l2h, ors.linf], rtol=1e-13)
+
+
+def test_3d_boxmg_tables_bitwise():
+    wl = workloads.config5(levels=3)
+    t, e, _ = oracle_run(wl, 0)
+    eng = GpuEngine(wl.tree, SolverConfig(variant=wl.variant, flavor=wl.flavor))
+    for l in range(wl.tree.lmin, wl.tree.depth):
+        assert np.array_equal(eng.transfers[l].p_table, e.tr[l].p), f"P level {l}"
+        got = eng.ops[l].table().reshape(e.ops[l].tbl.shape)
+        assert np.array_equal(got, e.ops[l].tbl), f"A level {l}"
+    for l in range(wl.tree.lmin, wl.tree.depth + 1):
+        assert np.array_equal(eng.eff_eps(l), e.eff[l]), f"eff level {l}"
+
+
+def test_3d_ds0_equals_additive_and_kinds():
+    wl = workloads.config5(levels=3)
+    e1, h1 = gpu_run(wl, 4, "adafac-jac", damping_scale=0.0)
+    wl2 = workloads.config5(levels=3)
+    e2, h2 = gpu_run(wl2, 4, "additive")
+    assert [s.l2h for s in h1] == [s.l2h for s in h2]
+    assert np.array_equal(wl.tree.u[3], wl2.tree.u[3])
+    for l in (1, 2, 3):
+        assert np.array_equal(e1.kinds(l), wl.tree.vertex_kinds(l))
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+FIXTURES = sorted(f[:-5] for f in os.listdir(os.path.join(HERE, "golden3d")) if f.endswith(".json"))
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_3d_fixture_history_and_sha(name):
+    fx = json.load(open(os.path.join(HERE, "golden3d", name + ".json")))
+    wl = workloads.by_name(fx["workload"])
+    eng, h = gpu_run(wl, fx["cycles"])
+    np.testing.assert_allclose([s.l2h for s in h], fx["l2h"], rtol=1e-13)
+    np.testing.assert_allclose([s.linf for s in h], fx["linf"], rtol=0)
+    for l, sha in fx["u_sha256"].items():
+        assert _sha(wl.tree.u[int(l)]) == sha, f"u level {l}"
