@@ -133,6 +133,52 @@ def bytes_model(eng, wl):
     return out
 
 
+def bytes_model3(eng, wl):
+    """Algorithmic bytes per launch of every 3D cycle kernel and the cycle B_alg.
+
+    Per interior vertex: fp64 = 8 B; the finer level's rho / sm are read once
+    (27 fine per coarse vertex); BoxMG P = 124 stored weights per coarse vertex
+    (8*124/27 = 36.74 B per fine DoF); Galerkin rows 27*8 B; element
+    coefficient 8 B per cell (~ per vertex).
+    """
+    L, l0 = wl.ltop, eng.lmin
+    boxmg = wl.flavor == "boxmg"
+    jac = wl.variant == "adafac-jac"
+    dofs = {l: (3**l - 1) ** 3 for l in range(l0, L + 1)}
+    elem_top = bool(np.any(wl.tree.eps[L] != wl.tree.eps[L].flat[0]))
+    out = {}
+    for l in range(l0, L + 1):
+        n = dofs[l]
+        if l == L:
+            op = 8 if elem_top else 0
+        else:
+            op = 216 if boxmg else (8 if elem_top else 0)
+        b = n * (8 + op + 8 + (8 if l in wl.rhs else 0)) + (n * 8 if l > l0 else 0)
+        if l < L:
+            b += dofs[l + 1] * 8 * (2 if jac else 1) + (n * 992 if boxmg else 0)
+        out[f"k3_down_L{l}"] = b
+        if jac and l > l0:
+            out[f"k3_smooth_L{l}"] = 16 * n
+        up = n * (16 + 8 + (8 if l < L else 0))
+        if l > l0:
+            up += dofs[l - 1] * (8 + (992 if boxmg else 0))
+        out[f"k3_up_L{l}"] = up
+    lc = l0
+    for l in range(l0, min(L, l0 + 2) + 1):
+        if (3**l + 1) ** 3 <= 1024:
+            lc = l
+    out["k3_chain"] = sum(out.get(f"k3_{k}_L{l}", 0) for l in range(l0, lc + 1)
+                          for k in ("down", "smooth", "up"))
+    fine = dofs[L]
+    coarse = sum(dofs[l] for l in range(l0, L))
+    b_alg = fine * (24 + (8 if elem_top else 0))
+    b_alg += coarse * (48 + (16 if jac else 0) + (216 if boxmg else (8 if elem_top else 0)))
+    if boxmg:
+        b_alg += sum(dofs[l] for l in range(l0 + 1, L + 1)) * 8 * 124 / 27
+    out["cycle"] = b_alg
+    return out
+
+
 # ---------------------------------------------------------------------------
 
 class ClockSampler:
@@ -179,8 +225,49 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sms)}
 
 
+CPU_SAMPLE_3D = {"config3": "config3-L4", "config5": "config5-L4"}
+
+
+def oracle_engine(wl):
+    """The CPU oracle engine on the workload's inputs (checker / CPU baseline only)."""
+    if wl.dim == 3:
+        from oracle import mg3d
+        t = mg3d.Tree(wl.tree.depth, wl.tree.lmin)
+        t.eps[wl.tree.depth] = wl.tree.eps[wl.tree.depth].copy()
+        eng = mg3d.Engine(t, mg3d.Config(variant=wl.variant, flavor=wl.flavor))
+        eng.rhs.update({l: b.copy() for l, b in wl.rhs.items()})
+        return eng
+    from oracle import mg2d
+    t = mg2d.Tree(lmin=wl.tree.lmin, lmax=wl.tree.lmax)
+    t.refined = [r.copy() for r in wl.tree.refined]
+    t.u = [u.copy() for u in wl.tree.u]
+    t.eps = [e.copy() for e in wl.tree.eps]
+    eng = mg2d.Engine(t, mg2d.Config(variant=wl.variant, flavor=wl.flavor))
+    eng.rhs.update(wl.rhs)
+    return eng
+
+
 def cpu_port_time(wl_name: str, cycles: int, budget_s: float = 20.0):
-    """Oracle (numpy restatement of the reference) on 1 core: seconds per cycle."""
+    """Oracle (numpy restatement of the reference; 3D: the d-generic restatement) on
+    1 core, on a bounded sample: seconds per cycle of the sample workload."""
+    from paper_1903_10367_b200 import workloads
+    wl_name = CPU_SAMPLE_3D.get(wl_name, wl_name)
+    wl = workloads.by_name(wl_name)
+    t0 = time.perf_counter()
+    eng = oracle_engine(wl)
+    setup = time.perf_counter() - t0
+    eng.advance()  # warm-up
+    done, t0 = 0, time.perf_counter()
+    while done < cycles:
+        eng.advance()
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = (time.perf_counter() - t0) / done
+    return dt, done, setup, wl
+
+
+def _unused_cpu_port_time2(wl_name: str, cycles: int, budget_s: float = 20.0):
     from oracle import mg2d
     from paper_1903_10367_b200 import workloads
     wl = workloads.by_name(wl_name)
@@ -206,17 +293,14 @@ def cpu_port_time(wl_name: str, cycles: int, budget_s: float = 20.0):
 def run_reference(args, dist: Dist):
     if dist.rank != 0:
         return
-    from oracle import mg2d
     from paper_1903_10367_b200 import workloads
-    wl = workloads.by_name(args.workload)
+    full = workloads.by_name(args.workload)
+    sample = CPU_SAMPLE_3D.get(args.workload)
+    wl = workloads.by_name(sample) if sample else full
     n_fine = wl.fine_dofs()
-    # time K steps on one engine (each step = one cycle of the port)
-    t = mg2d.Tree(lmin=wl.tree.lmin, lmax=wl.tree.lmax)
-    t.refined = [r.copy() for r in wl.tree.refined]
-    t.u = [u.copy() for u in wl.tree.u]
-    t.eps = [e.copy() for e in wl.tree.eps]
-    eng = mg2d.Engine(t, mg2d.Config(variant=wl.variant, flavor=wl.flavor))
-    eng.rhs.update(wl.rhs)
+    # time K steps on one engine (each step = one cycle of the port; 3D: one cycle
+    # of the bounded sample, the same structure at depth 4)
+    eng = oracle_engine(wl)
     for _ in range(args.warmup):
         eng.advance()
     t0 = time.perf_counter()
@@ -229,12 +313,14 @@ def run_reference(args, dist: Dist):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, SURVEY.md §8(d))",
-        "config": {"workload": wl.name, "levels": f"{wl.tree.lmin}..{wl.ltop}",
-                   "variant": wl.variant, "flavor": wl.flavor, "n_fine": n_fine},
+        "config": {"workload": full.name, "levels": f"{full.tree.lmin}..{full.ltop}",
+                   "variant": full.variant, "flavor": full.flavor, "n_fine": full.fine_dofs()},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
                          "sample": f"{args.steps} cycles of {wl.name} after {args.warmup} warm-up; "
-                                   "oracle/mg2d.py (numpy restatement of treemg, bit-identical "
-                                   "iterates), single thread"},
+                                   + ("oracle/mg3d.py (3D restatement, no 3D reference exists; "
+                                      "same structure at depth 4, DoF/s of the sample)"
+                                      if sample else "oracle/mg2d.py (numpy restatement of treemg, "
+                                      "bit-identical iterates)") + ", single thread"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -275,8 +361,8 @@ def run_ours(args, dist: Dist):
     value = dist.ws * n_fine / (ms_step * 1e-3)
 
     # ---- per-kernel times (roofline of the dominant kernel) --------------------
-    prof = eng.profile_cycles(max(args.steps, 5))
-    bm = bytes_model(eng, wl)
+    prof = eng.profile_cycles(max(min(args.steps, 10), 3))
+    bm = bytes_model3(eng, wl) if wl.dim == 3 else bytes_model(eng, wl)
     top = max(prof.items(), key=lambda kv: kv[1][0])
     kname, (kms, kcnt) = top
     total_prof = sum(v[0] for v in prof.values())
@@ -306,7 +392,7 @@ def run_ours(args, dist: Dist):
     eng.close()
 
     # ---- end to end through the drop-in API -------------------------------------
-    wl2 = workloads.by_name(args.workload)
+    wl2 = wl if wl.dim == 3 else workloads.by_name(args.workload)
     tree = wl2.tree
     for l in range(len(tree.u)):  # pinned host memory for tree.u
         pin = torch.empty(tree.u[l].shape, dtype=torch.float64, pin_memory=True).numpy()
@@ -326,7 +412,7 @@ def run_ours(args, dist: Dist):
         e2.advance()       # one cycle + D2H of every level of tree.u and the stats
     torch.cuda.synchronize()
     t_e2e = dist.max(time.perf_counter() - t0)
-    h2d = sum(tree.u[l].nbytes for l in range(e2.lmin - 1, e2.ltop + 1))
+    h2d = sum(tree.u[l].nbytes for l in range(e2.lmin - (1 if wl.dim == 2 else 0), e2.ltop + 1))
     d2h = sum(tree.u[l].nbytes for l in range(e2.lmin, e2.ltop + 1)) + 32
     e2e = {"value": dist.ws * n_fine * args.steps / t_e2e, "unit": UNIT,
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -336,11 +422,13 @@ def run_ours(args, dist: Dist):
     # ---- CPU baseline (rank 0 at N=1 only) ---------------------------------------
     cpu = None
     if dist.rank == 0 and dist.ws == 1 and not args.no_cpu:
-        dt, done, setup, _ = cpu_port_time(args.workload, 400, budget_s=args.cpu_budget)
-        cpu = {"value": n_fine / dt, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"{done} cycles of {wl.name} (after 1 warm-up) in "
-                         f"{dt * done:.1f} s; oracle/mg2d.py numpy restatement, 1 thread; "
-                         f"setup {setup:.2f} s"}
+        dt, done, setup, swl = cpu_port_time(args.workload, 400, budget_s=args.cpu_budget)
+        cpu = {"value": swl.fine_dofs() / dt, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"{done} cycles of {swl.name} (after 1 warm-up) in "
+                         f"{dt * done:.1f} s; "
+                         + ("oracle/mg3d.py 3D restatement (no 3D reference), same structure at "
+                            "depth 4" if swl.dim == 3 else "oracle/mg2d.py numpy restatement")
+                         + f", 1 thread; setup {setup:.2f} s"}
 
     if dist.rank == 0:
         line = {
