@@ -9,6 +9,7 @@
 
 #include "engine3.h"
 #include "kernels3d.cu"
+#include "kernels3d_fast.cu"
 
 namespace {
 
@@ -22,6 +23,9 @@ struct Lvl3 {
   Op3 op{};
   double w = 0.0;
   int grid = 0, part_off = 0;
+  int s_chunk = 0, s_blocks = 0;  // 2.5D tiling (k3_top / k3_smooth_s)
+  int c_grid = 0;                 // k3_down_c grid
+  int u_grid = 0;                 // k3_up_cell grid (this level as the coarse one)
 };
 
 struct KT {
@@ -200,8 +204,8 @@ Down3 make_down(Engine3* e, int l, bool write) {
   a.hw = std::pow(3.0, -1.5 * l);
   a.rho = (l > l0) ? c.rho : nullptr;
   a.g = c.g;
-  a.part_sum = (l > e->lc) ? e->part_sum + c.part_off : nullptr;
-  a.part_max = (l > e->lc) ? e->part_max + c.part_off : nullptr;
+  a.part_sum = nullptr;  // grid partials come from k3_top only
+  a.part_max = nullptr;
   return a;
 }
 
@@ -245,17 +249,58 @@ Up3 make_up(Engine3* e, int l) {
   return a;
 }
 
-const bool kJacSmooth = true;
+Top3 make_top(Engine3* e, int l) {
+  Lvl3& c = e->L[l];
+  Top3 a{};
+  a.N = c.N;
+  a.ilo = 1;
+  a.ihi = c.N - 1;
+  a.chunk = c.s_chunk;
+  a.u = c.u;
+  a.rhs = c.rhs;
+  a.op = c.op;
+  a.w = c.w;
+  a.hw = std::pow(3.0, -1.5 * l);
+  a.g = c.g;
+  a.rho = (l > e->lmin) ? c.rho : nullptr;
+  a.part_sum = e->part_sum;
+  a.part_max = e->part_max;
+  return a;
+}
+
+SmoothS make_smooth_s(Engine3* e, int l) {
+  Lvl3& c = e->L[l];
+  SmoothS a{};
+  a.N = c.N;
+  a.ilo = 1;
+  a.ihi = c.N - 1;
+  a.chunk = c.s_chunk;
+  a.x = c.rho;
+  a.sm = c.sm;
+  a.scale = e->cfg.omega * 3.0 / 8.0;
+  return a;
+}
 
 int enqueue_down(Engine3* e, bool write) {
   const bool jac = e->cfg.variant == VAR_JAC;
-  const dim3 blk(kTX, kTY, kTZ);
+  const bool boxmg = e->cfg.flavor == TMG_BOXMG;
+  const dim3 sblk(kSX, kSY);
   for (int l = e->ltop; l > e->lc; --l) {
-    Down3 a = make_down(e, l, write);
-    LAUNCH3(kname("k3_down", l), k3_down, e->L[l].grid, blk, a);
-    if (jac && write && l > e->lmin && kJacSmooth) {
-      Smooth3 sa = make_smooth(e, l);
-      LAUNCH3(kname("k3_smooth", l), k3_smooth, e->L[l].grid, blk, sa);
+    Lvl3& c = e->L[l];
+    if (l == e->ltop) {
+      Top3 a = make_top(e, l);
+      if (c.op.kind == OP_CONST) LAUNCH3(kname("k3_down", l), k3_top<OP_CONST>, c.s_blocks, sblk, a);
+      else LAUNCH3(kname("k3_down", l), k3_top<OP_ELEMENT>, c.s_blocks, sblk, a);
+    } else {
+      Down3 a = make_down(e, l, write);
+      if (boxmg && jac) LAUNCH3(kname("k3_down", l), (k3_down_c<true, true>), c.c_grid, 128, a);
+      else if (boxmg) LAUNCH3(kname("k3_down", l), (k3_down_c<true, false>), c.c_grid, 128, a);
+      else if (jac) LAUNCH3(kname("k3_down", l), (k3_down_c<false, true>), c.c_grid, 128, a);
+      else LAUNCH3(kname("k3_down", l), (k3_down_c<false, false>), c.c_grid, 128, a);
+    }
+    if (jac && write && l > e->lmin) {
+      SmoothS sa = make_smooth_s(e, l);
+      LAUNCH3(kname("k3_smooth", l), k3_smooth_s, c.s_blocks, sblk, sa);
     }
   }
   Chain3 ch{};
@@ -280,10 +325,15 @@ int enqueue_down(Engine3* e, bool write) {
 
 int enqueue_cycle(Engine3* e) {
   TRY3(enqueue_down(e, true));
+  const bool boxmg = e->cfg.flavor == TMG_BOXMG;
+  const bool pi = e->cfg.variant == VAR_PI;
   const dim3 blk(kTX, kTY, kTZ);
   for (int l = e->lc + 1; l <= e->ltop; ++l) {
     Up3 a = make_up(e, l);
-    LAUNCH3(kname("k3_up", l), k3_up, e->L[l].grid, blk, a);
+    const int g = e->L[l - 1].u_grid;
+    if (pi) LAUNCH3(kname("k3_up", l), k3_up, e->L[l].grid, blk, a);
+    else if (boxmg) LAUNCH3(kname("k3_up", l), k3_up_cell<true>, g, 128, a);
+    else LAUNCH3(kname("k3_up", l), k3_up_cell<false>, g, 128, a);
   }
   return TMG_OK;
 }
@@ -458,9 +508,21 @@ int build(Engine3* e, const tmg_tree3* t) {
     if (l > l0 && jac) TRY3(alloc3(e, &c.sm, c.nv));
     if (l < l1) TRY3(alloc3(e, &c.carry, c.nv));
     c.grid = grid_for(c.N, 1, c.N - 1);
-    if (l > e->lc) {
-      c.part_off = parts;
-      parts += c.grid;
+    {
+      const int tiles = ((c.N - 2 + kSX - 1) / kSX) * ((c.N - 2 + kSY - 1) / kSY);
+      int nch = (148 * 16 + tiles - 1) / tiles;
+      nch = std::max(1, std::min(nch, std::max(1, (c.N - 2) / 4)));
+      c.s_chunk = (c.N - 2 + nch - 1) / nch;
+      const int chunks = (c.N - 2 + c.s_chunk - 1) / c.s_chunk;
+      c.s_blocks = tiles * chunks;
+      const size_t ni = (size_t)(c.N - 2) * (c.N - 2) * (c.N - 2);
+      const size_t ncell = (size_t)(c.N - 1) * (c.N - 1) * (c.N - 1);
+      c.c_grid = (int)std::max<size_t>(1, std::min<size_t>((ni + 127) / 128, 148 * 32));
+      c.u_grid = (int)std::max<size_t>(1, std::min<size_t>((9 * ncell + 127) / 128, 148 * 64));
+    }
+    if (l == l1 && l > e->lc) {
+      c.part_off = 0;
+      parts = c.s_blocks;
     }
   }
   e->nparts = parts;

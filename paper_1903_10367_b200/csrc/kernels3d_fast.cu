@@ -1,0 +1,378 @@
+// 3D cycle kernels specialised for the large levels (same per-element DAGs as
+// kernels3d.cu / oracle/mg3d.py, different data movement):
+//
+// * k3_top<KIND>   finest-level down sweep, 2.5D: a CTA owns a 32 (k) x 8 (j)
+//                  column and marches a chunk of i-planes, keeping a ring of
+//                  three u-planes (+halo) and two cell-coefficient planes in
+//                  shared memory, so each u / coefficient value is read from
+//                  HBM once per sweep instead of 27 / 8 times through L1.
+// * k3_smooth_s    R~ smoothing sm = A1(rho) * s with the same 2.5D scheme.
+// * k3_down_c      coarse-level down sweep: operator apply + FAS RHS +
+//                  Jacobi + adaFACx damping; R and R~ share one pass over
+//                  the 124 BoxMG weight planes (each weight loaded once).
+// * k3_up_cell     prolongation owned by coarse cells: thread W updates the
+//                  27 fine vertices 3W + r, reading every P weight exactly
+//                  once with warp-coalesced plane loads.
+#include "kernels3d.cuh"
+
+namespace t3 {
+
+constexpr int kSX = 32, kSY = 8;           // 2.5D tile (k, j)
+constexpr int kSB = kSX * kSY;
+constexpr int kRowU = kSX + 2, kColU = kSY + 2;  // u plane with halo
+constexpr int kRowC = kSX + 1, kColC = kSY + 1;  // cell plane with halo (cells k-1.., j-1..)
+
+struct Top3 {
+  int N, ilo, ihi, chunk;  // planes [ilo, ihi) split in chunks
+  const double* u;
+  const double* rhs;
+  Op3 op;
+  double w, hw;
+  double* g;
+  double* rho;  // or nullptr
+  double* part_sum;
+  double* part_max;
+};
+
+// 2.5D streaming.  A CTA owns a kSX x kSY column of (k, j) and marches the
+// planes i in [ia, ib).  Halo planes of u (and of the cell coefficients) are
+// staged into a kStages-deep shared-memory ring with cp.async (8-byte
+// copies, zero-filled outside the grid), kStages-2 planes ahead of the plane
+// being consumed; each thread keeps its 3x3 neighbourhood of planes i-1 and
+// i in registers and reads only plane i+1 from shared memory.
+constexpr int kStages = 6;
+
+__device__ __forceinline__ void cp_async8(void* smem, const double* gmem, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int Np>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(Np) : "memory"); }
+
+struct Column {
+  static constexpr int kPU = (kColU * kRowU + kSB - 1) / kSB;
+  static constexpr int kPC = (kColC * kRowC + kSB - 1) / kSB;
+  int N, k0, j0, ia, ib, lt;
+  // in-plane offsets of the halo positions this thread stages (-1: outside / none)
+  long long ou[kPU], oc[kPC];
+  __device__ Column(int N_, int ilo, int ihi, int chunk) : N(N_) {
+    const int tilesx = (N - 2 + kSX - 1) / kSX, tilesy = (N - 2 + kSY - 1) / kSY;
+    int b = blockIdx.x;
+    const int tx = b % tilesx;
+    b /= tilesx;
+    const int ty = b % tilesy;
+    const int tz = b / tilesy;
+    k0 = 1 + tx * kSX;
+    j0 = 1 + ty * kSY;
+    ia = ilo + tz * chunk;
+    ib = min(ihi, ia + chunk);
+    lt = threadIdx.y * kSX + threadIdx.x;
+    const int n = N - 1;
+#pragma unroll
+    for (int p = 0; p < kPU; ++p) {
+      const int q = lt + p * kSB;
+      const int jj = q / kRowU, kk = q - jj * kRowU;
+      const int j = j0 - 1 + jj, k = k0 - 1 + kk;
+      ou[p] = (q < kColU * kRowU) ? ((j < N && k < N) ? (long long)j * N + k : -1) : -2;
+    }
+#pragma unroll
+    for (int p = 0; p < kPC; ++p) {
+      const int q = lt + p * kSB;
+      const int jj = q / kRowC, kk = q - jj * kRowC;
+      const int cj = j0 - 1 + jj, ck = k0 - 1 + kk;
+      oc[p] = (q < kColC * kRowC) ? ((cj < n && ck < n) ? (long long)cj * n + ck : -1) : -2;
+    }
+  }
+  // stage vertex plane p (halo kColU x kRowU) of x into buf; zero outside
+  __device__ __forceinline__ void stage_v(double* buf, const double* x, int p) const {
+    const bool okp = p >= 0 && p < N;
+    const double* base = x + (size_t)(okp ? p : 0) * N * N;
+#pragma unroll
+    for (int q = 0; q < kPU; ++q) {
+      if (ou[q] == -2) continue;
+      const bool ok = okp && ou[q] >= 0;
+      cp_async8(buf + lt + q * kSB, ok ? base + ou[q] : x, ok);
+    }
+  }
+  // stage cell plane c (halo kColC x kRowC) of e (n = N-1 cells per axis)
+  __device__ __forceinline__ void stage_c(double* buf, const double* e, int c) const {
+    const int n = N - 1;
+    const bool okp = c >= 0 && c < n;
+    const double* base = e + (size_t)(okp ? c : 0) * n * n;
+#pragma unroll
+    for (int q = 0; q < kPC; ++q) {
+      if (oc[q] == -2) continue;
+      const bool ok = okp && oc[q] >= 0;
+      cp_async8(buf + lt + q * kSB, ok ? base + oc[q] : e, ok);
+    }
+  }
+};
+
+// The streaming driver: stages planes kStages-2 ahead with cp.async and runs
+// body(i, xm, x0, xp, em, e0) for i in [ia, ib), where xm / x0 / xp are the
+// thread's 3x3 neighbourhoods of planes i-1, i, i+1 and em / e0 the four
+// cells (j-c1, k-c2) of cell planes i-1 and i.  The loop is unrolled by
+// kStages (a multiple of 3) so every ring slot and register rotation is a
+// compile-time constant: no register moves, no modulo arithmetic.
+template <bool CELLS, class Body>
+__device__ __forceinline__ void stream25(const Column& col, const double* x, const double* e,
+                                         double (*us)[kColU * kRowU], double (*cs)[kColC * kRowC],
+                                         Body&& body) {
+  static_assert(kStages % 3 == 0, "register rotation needs kStages % 3 == 0");
+  const int tj = threadIdx.y + 1, tk = threadIdx.x + 1;
+  const int ia = col.ia, ib = col.ib;
+  auto issue = [&](int g, int slot) {
+    col.stage_v(us[slot], x, ia - 1 + g);
+    if (CELLS) col.stage_c(cs[slot], e, ia - 1 + g);
+    cp_commit();
+  };
+#pragma unroll
+  for (int g = 0; g < kStages; ++g) issue(g, g);
+  double X[3][9], E[3][4];
+  cp_wait<kStages - 2>();
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    X[0][t] = us[0][(tj + t / 3 - 1) * kRowU + tk + t % 3 - 1];
+    X[1][t] = us[1][(tj + t / 3 - 1) * kRowU + tk + t % 3 - 1];
+  }
+  if (CELLS) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) E[0][c] = cs[0][(tj - (c & 1)) * kRowC + tk - ((c >> 1) & 1)];
+  }
+  for (int i0 = ia; i0 < ib; i0 += kStages) {
+#pragma unroll
+    for (int u = 0; u < kStages; ++u) {
+      const int i = i0 + u;
+      if (i < ib) {
+        cp_wait<kStages - 3>();
+        __syncthreads();
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int su = (u + 2) % kStages, sc = (u + 1) % kStages;
+        double* xp = X[(u + 2) % 3];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) xp[t] = us[su][(tj + t / 3 - 1) * kRowU + tk + t % 3 - 1];
+        if (CELLS) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) E[(u + 1) % 3][c] = cs[sc][(tj - (c & 1)) * kRowC + tk - ((c >> 1) & 1)];
+        }
+        issue(kStages + (i - ia), u);  // the slot of plane i-1, consumed two steps ago
+        body(i, X[u % 3], X[(u + 1) % 3], X[(u + 2) % 3], E[u % 3], E[(u + 1) % 3]);
+      }
+    }
+  }
+  cp_wait<0>();
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kSB, 2) k3_top(const __grid_constant__ Top3 a) {
+  __shared__ double us[kStages][kColU * kRowU];
+  __shared__ double cs[KIND == OP_ELEMENT ? kStages : 1][kColC * kRowC];
+  const Column col(a.N, a.ilo, a.ihi, a.chunk);
+  const int N = a.N;
+  const size_t NN = (size_t)N * N;
+  const int k = col.k0 + threadIdx.x, j = col.j0 + threadIdx.y;
+  const bool own = k <= N - 2 && j <= N - 2;
+  const size_t col_off = (size_t)j * N + k;
+  double rhs_n = (own && a.rhs) ? __ldg(a.rhs + (size_t)col.ia * NN + col_off) : 0.0;
+  double s = 0.0, mx = 0.0;
+  stream25<KIND == OP_ELEMENT>(col, a.u, a.op.e, us, cs,
+      [&](int i, const double* xm, const double* x0, const double* xp, const double* em,
+          const double* e0) {
+        const double rhs = rhs_n;
+        if (own && a.rhs && i + 1 < col.ib) rhs_n = __ldg(a.rhs + (size_t)(i + 1) * NN + col_off);
+        if (!own) return;
+        double x[27];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+          x[t] = xm[t];
+          x[9 + t] = x0[t];
+          x[18 + t] = xp[t];
+        }
+        double au, dg;
+        if (KIND == OP_CONST) {
+          au = const_from(x, a.op.m, a.op.se, a.op.sc);
+          dg = a.op.cdiag;
+        } else {
+          double ec[8], E, T;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) ec[c] = (c & 1) ? em[c >> 1] : e0[c >> 1];  // cell (i-c0, j-c1, k-c2)
+          element_ET(x, ec, E, T);
+          dg = K_D * E;
+          au = (dg * x[13]) - (K_E * T);
+        }
+        const double rho = rhs - au;
+        const double t = a.hw * rho;
+        s = s + t * t;
+        mx = fmax(mx, fabs(rho));
+        const size_t v = (size_t)i * NN + col_off;
+        a.g[v] = (a.w * rho) / dg;
+        if (a.rho) a.rho[v] = rho;
+      });
+  // block reduction of the stats partials
+  __shared__ double rs[kSB / 32], rm[kSB / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_down_sync(0xffffffffu, s, o);
+    mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+  }
+  if ((col.lt & 31) == 0) { rs[col.lt >> 5] = s; rm[col.lt >> 5] = mx; }
+  __syncthreads();
+  if (col.lt == 0) {
+    double A = 0.0, B = 0.0;
+    for (int q = 0; q < kSB / 32; ++q) { A += rs[q]; B = fmax(B, rm[q]); }
+    a.part_sum[blockIdx.x] = A;
+    a.part_max[blockIdx.x] = B;
+  }
+}
+
+struct SmoothS {
+  int N, ilo, ihi, chunk;
+  const double* x;
+  double* sm;
+  double scale;
+};
+
+__global__ void __launch_bounds__(kSB, 3) k3_smooth_s(const __grid_constant__ SmoothS a) {
+  __shared__ double xs[kStages][kColU * kRowU];
+  const Column col(a.N, a.ilo, a.ihi, a.chunk);
+  const int N = a.N;
+  const size_t NN = (size_t)N * N;
+  const int k = col.k0 + threadIdx.x, j = col.j0 + threadIdx.y;
+  const bool own = k <= N - 2 && j <= N - 2;
+  const size_t col_off = (size_t)j * N + k;
+  stream25<false>(col, a.x, nullptr, xs, nullptr,
+      [&](int i, const double* xm, const double* x0, const double* xp, const double*, const double*) {
+        if (!own) return;
+        double x[27];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+          x[t] = xm[t];
+          x[9 + t] = x0[t];
+          x[18 + t] = xp[t];
+        }
+        double v = const_from(x, C_D8, C_E6, C_C12);
+        v = v * a.scale;
+        a.sm[(size_t)i * NN + col_off] = v;
+      });
+}
+
+// Coarse-level down sweep with the restriction of rho and (adaFACx) sm of the
+// finer level in one pass over the P planes.  Thread per interior vertex,
+// k fastest (P planes and coarse vectors coalesced).
+template <bool BOXMG, bool JAC>
+__global__ void __launch_bounds__(128) k3_down_c(const __grid_constant__ Down3 a) {
+  const int N = a.N, n = N - 2;
+  const size_t cnt = (size_t)(a.ihi - a.ilo) * n * n;
+  double s = 0.0, m = 0.0;
+  for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < cnt;
+       q += (size_t)gridDim.x * blockDim.x) {
+    const int k = 1 + (int)(q % n);
+    const size_t r = q / n;
+    const int j = 1 + (int)(r % n), i = a.ilo + (int)(r / n);
+    const size_t v = vid(N, i, j, k);
+    double au, dg;
+    op_apply<LdNC>(a.op, a.u, N, i, j, k, au, dg);
+    const bool cpt0 = a.variant == VAR_AFACC;
+    double bR, bT = 0.0;
+    if (BOXMG) {
+      const int Nf = a.Nf;
+      const size_t nvc = (size_t)N * N * N;
+      const size_t fc = vid(Nf, 3 * i, 3 * j, 3 * k);
+      const long long sN = Nf, sNN = (long long)Nf * Nf;
+      double accR = 0.0, accT = 0.0;
+#pragma unroll 5
+      for (int o = 0; o < 125; ++o) {
+        const int oa = o / 25 - 2, ob = (o / 5) % 5 - 2, oc = o % 5 - 2;
+        const long long fo = (long long)fc + oa * sNN + ob * sN + oc;
+        const double w = (o == 62) ? 1.0 : __ldg(a.P + (size_t)o * nvc + v);
+        double x = __ldg(a.rho_f + fo);
+        if (o == 62 && cpt0) x = 0.0;
+        accR = accR + w * x;
+        if (JAC) accT = accT + w * __ldg(a.sm_f + fo);
+      }
+      bR = accR;
+      bT = accT;
+    } else {
+      bR = restrict_dlinear<LdNC>(a.rho_f, a.Nf, i, j, k, cpt0);
+      if (JAC) bT = restrict_dlinear<LdNC>(a.sm_f, a.Nf, i, j, k, false);
+    }
+    const double rhs = a.rhs ? __ldg(a.rhs + v) : 0.0;
+    double b = bR + rhs;
+    b = b + au;
+    const double rho = b - au;
+    if (a.write) {
+      double d;
+      if (a.variant == VAR_BPX) d = a.omega * rho;
+      else d = (a.w * rho) / dg;
+      if (JAC) d = d - a.ds * ((a.wt * bT) / dg);
+      a.g[v] = d;
+    }
+    if (a.rho) a.rho[v] = rho;
+  }
+  (void)s;
+  (void)m;
+}
+
+// Prolongation owned by coarse cells (solvers.py:386-395 + FAS walk-down):
+// thread (W, ri, rj) updates the three fine vertices 3W + (ri, rj, 0..2);
+// warps run along K, so every P plane / coarse carry load is coalesced and
+// every P weight is read exactly once.
+template <bool BOXMG>
+__global__ void __launch_bounds__(128) k3_up_cell(const __grid_constant__ Up3 a) {
+  const int Nc = a.Nc, nc = Nc - 1, N = a.N;
+  const size_t ncube = (size_t)nc * nc * nc;
+  const size_t cnt = 9 * ncube;
+  const size_t nvc = (size_t)Nc * Nc * Nc;
+  const double* cc = a.carry_c;
+  for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < cnt;
+       q += (size_t)gridDim.x * blockDim.x) {
+    const int rr = (int)(q / ncube);
+    const size_t w = q - (size_t)rr * ncube;
+    const int K = (int)(w % nc);
+    const size_t w2 = w / nc;
+    const int J = (int)(w2 % nc), I = (int)(w2 / nc);
+    const int ri = rr / 3, rj = rr - 3 * ri;
+    const int i = 3 * I + ri, j = 3 * J + rj;
+    if (i < a.ilo || i >= a.ihi || j < 1) continue;
+#pragma unroll
+    for (int rk = 0; rk < 3; ++rk) {
+      const int k = 3 * K + rk;
+      if (k < 1) continue;
+      double pc;
+      if (BOXMG) {
+        double acc = 0.0;
+#pragma unroll
+        for (int d = 7; d >= 0; --d) {
+          const int di = (d >> 2) & 1, dj = (d >> 1) & 1, dk = d & 1;
+          if ((di && !ri) || (dj && !rj) || (dk && !rk)) continue;
+          const size_t wv = vid(Nc, I + di, J + dj, K + dk);
+          const int sl = pslot(ri - 3 * di, rj - 3 * dj, rk - 3 * dk);
+          const double wt = (sl == 62) ? 1.0 : __ldg(a.P + (size_t)sl * nvc + wv);
+          acc = acc + wt * __ldg(cc + wv);
+        }
+        pc = acc;
+      } else {
+        auto cv = [&](int x, int y, int z) -> double { return __ldg(cc + vid(Nc, x, y, z)); };
+        pc = prolong_dlinear(cv, Nc, i, j, k);
+      }
+      const size_t v = vid(N, i, j, k);
+      const double c = pc + __ldg(a.g + v);
+      if (a.carry) a.carry[v] = c;
+      const double un = a.u[v] + c;
+      a.u[v] = un;
+      int ii = i, jj = j, kk = k;
+      for (int lc = a.l - 1; lc >= a.l0; --lc) {
+        if (ii % 3 || jj % 3 || kk % 3) break;
+        ii /= 3;
+        jj /= 3;
+        kk /= 3;
+        a.ul[lc][vid(a.Nl[lc], ii, jj, kk)] = un;
+      }
+    }
+  }
+}
+
+}  // namespace t3
