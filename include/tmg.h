@@ -114,6 +114,35 @@ int tmg3_rebuild(tmg_handle* h, const tmg_tree3* tree);
 /* 2 or 3: the dimension of the hierarchy a handle holds. */
 int tmg_dim(tmg_handle* h);
 
+/* ---- multi-GPU slab sharding of a 3D handle ----
+ * Every rank builds the full hierarchy (setup is redundant, cycles are not);
+ * tmg3_shard restricts the cycle of levels >= ls to the vertex planes
+ * [lo[l], hi[l]) (axis 0, the slowest) this rank owns; levels < ls are
+ * replicated.  The host (paper_1903_10367_b200/sharding.py) runs the cycle
+ * phase by phase and exchanges halo planes / gathers / reduces with NCCL on
+ * the handle's stream between phases.  No reference counterpart: the
+ * reference is serial. */
+#define TMG_PH_DOWN 0   /* level l >= ls: down sweep on owned planes           */
+#define TMG_PH_SMOOTH 1 /* level l >= ls: adaFACx R~ smoothing on owned planes  */
+#define TMG_PH_REPL 2   /* levels lmin..ls-1 (replicated): down, stats, up      */
+#define TMG_PH_UP 3     /* level l >= ls: carry + update on owned planes        */
+#define TMG_PH_INJECT 4 /* FAS injection ls -> lmin on the replicated levels    */
+#define TMG_PH_REDUCE 5 /* fold this cycle's stats partials into TMG_F_PART     */
+#define TMG_F_U 0
+#define TMG_F_RHO 1
+#define TMG_F_SM 2
+#define TMG_F_CARRY 3
+#define TMG_F_G 4
+#define TMG_F_PART 5 /* 2 doubles: sum of squares, max (all-reduced across ranks) */
+int tmg3_shard(tmg_handle* h, int32_t ls, const int32_t* lo, const int32_t* hi);
+int tmg3_phase(tmg_handle* h, int32_t phase, int32_t level);
+/* device address and element count of a field of a level (zero-copy views) */
+int tmg3_field(tmg_handle* h, int32_t field, int32_t level, uint64_t* ptr, int64_t* count);
+/* the cudaStream_t every phase is enqueued on */
+int tmg3_stream(tmg_handle* h, uint64_t* stream);
+/* the last `count` per-cycle residual stats of a sharded run */
+int tmg3_history(tmg_handle* h, int32_t count, tmg_stats* out);
+
 /* ReferenceEngine.rebuild() after a mesh / material change (solvers.py:145-255):
  * rebuilds every operator from the new tree and re-uploads u. rhs is kept. */
 int tmg_rebuild(tmg_handle* h, const tmg_tree* tree);

@@ -20,12 +20,15 @@ VARIANT_IDS = {"additive": 0, "additive-exp": 1, "bpx": 2, "afacc": 3, "adafac-p
                "adafac-jac": 5, "multiplicative-v10": 6}
 FLAVOR_IDS = {"geometric": 0, "boxmg": 1}
 TABLE_A, TABLE_DIAG, TABLE_P, TABLE_RT, TABLE_EFFEPS = 0, 1, 2, 3, 4
+PH_DOWN, PH_SMOOTH, PH_REPL, PH_UP, PH_INJECT, PH_REDUCE = 0, 1, 2, 3, 4, 5
+F_U, F_RHO, F_SM, F_CARRY, F_G, F_PART = 0, 1, 2, 3, 4, 5
 
 EXPORTS = ("tmg_create", "tmg_rebuild", "tmg_set_rhs", "tmg_set_u", "tmg_get_u",
            "tmg_update_fas_state", "tmg_cycle", "tmg_residual_stats", "tmg_levels",
            "tmg_level_counts", "tmg_get_kinds", "tmg_get_table", "tmg_time_cycles",
            "tmg_profile_cycles", "tmg_launches_per_cycle", "tmg_destroy", "tmg_last_error",
-           "tmg_device_count", "tmg3_create", "tmg3_rebuild", "tmg_dim")
+           "tmg_device_count", "tmg3_create", "tmg3_rebuild", "tmg_dim", "tmg3_shard", "tmg3_phase",
+           "tmg3_field", "tmg3_stream", "tmg3_history")
 
 
 class Config(C.Structure):
@@ -88,6 +91,11 @@ def lib() -> C.CDLL:
         "tmg3_create": ([P(Tree3), P(Config), P(H)], C.c_int),
         "tmg3_rebuild": ([H, P(Tree3)], C.c_int),
         "tmg_dim": ([H], C.c_int),
+        "tmg3_shard": ([H, C.c_int32, P(C.c_int32), P(C.c_int32)], C.c_int),
+        "tmg3_phase": ([H, C.c_int32, C.c_int32], C.c_int),
+        "tmg3_field": ([H, C.c_int32, C.c_int32, P(C.c_uint64), P(C.c_int64)], C.c_int),
+        "tmg3_stream": ([H, P(C.c_uint64)], C.c_int),
+        "tmg3_history": ([H, C.c_int32, C.c_void_p], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

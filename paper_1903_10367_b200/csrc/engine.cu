@@ -776,6 +776,31 @@ int tmg3_rebuild(tmg_handle* h, const tmg_tree3* tree) {
 
 int tmg_dim(tmg_handle* h) { return (h && h->e3) ? 3 : 2; }
 
+int tmg3_shard(tmg_handle* h, int32_t ls, const int32_t* lo, const int32_t* hi) {
+  if (!h || !h->e3 || !lo || !hi) return fail(TMG_EINVAL, "null argument or not a 3D handle");
+  return e3_shard(h->e3, ls, lo, hi, g_err);
+}
+
+int tmg3_phase(tmg_handle* h, int32_t phase, int32_t level) {
+  if (!h || !h->e3) return fail(TMG_EINVAL, "null argument or not a 3D handle");
+  return e3_phase(h->e3, phase, level, g_err);
+}
+
+int tmg3_field(tmg_handle* h, int32_t field, int32_t level, uint64_t* ptr, int64_t* count) {
+  if (!h || !h->e3 || !ptr || !count) return fail(TMG_EINVAL, "null argument or not a 3D handle");
+  return e3_field(h->e3, field, level, ptr, count, g_err);
+}
+
+int tmg3_stream(tmg_handle* h, uint64_t* stream) {
+  if (!h || !h->e3 || !stream) return fail(TMG_EINVAL, "null argument or not a 3D handle");
+  return e3_stream(h->e3, stream);
+}
+
+int tmg3_history(tmg_handle* h, int32_t count, tmg_stats* out) {
+  if (!h || !h->e3 || !out) return fail(TMG_EINVAL, "null argument or not a 3D handle");
+  return e3_history(h->e3, count, out, g_err);
+}
+
 int tmg_rebuild(tmg_handle* h, const tmg_tree* tree) {
   if (h && h->e3) return fail(TMG_EINVAL, "3D handle: use tmg3_rebuild");
   if (!h || !tree) return fail(TMG_EINVAL, "null argument");

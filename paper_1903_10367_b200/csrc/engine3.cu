@@ -75,6 +75,14 @@ struct Engine3 {
   void* flush_buf = nullptr;
   size_t flush_bytes = 0;
   std::string* err = nullptr;
+  // sharded (multi-GPU slab) mode: levels >= ls restricted to owned vertex planes
+  bool sharded = false;
+  int ls = 0;
+  std::vector<int> own_lo, own_hi;  // by level
+  std::vector<int> own_blocks;      // k3_top / k3_smooth_s blocks for the owned range
+  std::vector<int> own_chunk;
+  double* red = nullptr;            // {sum, max} of this cycle's stats
+  int top_parts = 0;
 };
 
 namespace {
@@ -159,11 +167,11 @@ const char* kname(const char* base, int l) {
   return names[b][l];
 }
 
-#define LAUNCH3(name, kernel, grid, block, arg)         \
+#define LAUNCH3(name, kernel, grid, block, ...)         \
   do {                                                  \
     cudaEvent_t e0_ = nullptr;                          \
     TRY3(begin_k(e, &e0_));                             \
-    kernel<<<(grid), (block), 0, e->s>>>(arg);          \
+    kernel<<<(grid), (block), 0, e->s>>>(__VA_ARGS__);  \
     CKL3();                                             \
     TRY3(end_k(e, name, e0_));                          \
   } while (0)
@@ -562,7 +570,210 @@ struct ErrScope {
   ~ErrScope() { e->err = nullptr; }
 };
 
+// --- sharded mode ---------------------------------------------------------------
+
+// 2.5D tiling of the interior planes [ilo, ihi) of an N^3 level
+void tiling(int N, int ilo, int ihi, int* chunk, int* blocks) {
+  const int tiles = ((N - 2 + kSX - 1) / kSX) * ((N - 2 + kSY - 1) / kSY);
+  const int np = std::max(1, ihi - ilo);
+  int nch = (148 * 16 + tiles - 1) / tiles;
+  nch = std::max(1, std::min(nch, std::max(1, np / 4)));
+  *chunk = (np + nch - 1) / nch;
+  *blocks = tiles * ((np + *chunk - 1) / *chunk);
+}
+
+int interior_lo(Engine3* e, int l) { return std::max(1, e->own_lo[l]); }
+int interior_hi(Engine3* e, int l) { return std::min(e->L[l].N - 1, e->own_hi[l]); }
+
+int phase3(Engine3* e, int phase, int l) {
+  const bool jac = e->cfg.variant == VAR_JAC;
+  const bool boxmg = e->cfg.flavor == TMG_BOXMG;
+  const bool pi = e->cfg.variant == VAR_PI;
+  const dim3 sblk(kSX, kSY);
+  switch (phase) {
+    case TMG_PH_DOWN: {
+      if (l < e->ls || l > e->ltop) return fail3(e, TMG_EINVAL, "DOWN: level is not sharded");
+      const int lo = interior_lo(e, l), hi = interior_hi(e, l);
+      if (hi <= lo) return TMG_OK;
+      Lvl3& c = e->L[l];
+      if (l == e->ltop) {
+        Top3 a = make_top(e, l);
+        a.ilo = lo;
+        a.ihi = hi;
+        a.chunk = e->own_chunk[l];
+        e->top_parts = e->own_blocks[l];
+        if (c.op.kind == OP_CONST) LAUNCH3(kname("k3_down", l), k3_top<OP_CONST>, e->own_blocks[l], sblk, a);
+        else LAUNCH3(kname("k3_down", l), k3_top<OP_ELEMENT>, e->own_blocks[l], sblk, a);
+      } else {
+        Down3 a = make_down(e, l, true);
+        a.ilo = lo;
+        a.ihi = hi;
+        if (boxmg && jac) LAUNCH3(kname("k3_down", l), (k3_down_c<true, true>), c.c_grid, 128, a);
+        else if (boxmg) LAUNCH3(kname("k3_down", l), (k3_down_c<true, false>), c.c_grid, 128, a);
+        else if (jac) LAUNCH3(kname("k3_down", l), (k3_down_c<false, true>), c.c_grid, 128, a);
+        else LAUNCH3(kname("k3_down", l), (k3_down_c<false, false>), c.c_grid, 128, a);
+      }
+      return TMG_OK;
+    }
+    case TMG_PH_SMOOTH: {
+      if (!jac || l <= e->lmin) return TMG_OK;
+      const int lo = interior_lo(e, l), hi = interior_hi(e, l);
+      if (hi <= lo) return TMG_OK;
+      SmoothS a = make_smooth_s(e, l);
+      a.ilo = lo;
+      a.ihi = hi;
+      a.chunk = e->own_chunk[l];
+      LAUNCH3(kname("k3_smooth", l), k3_smooth_s, e->own_blocks[l], sblk, a);
+      return TMG_OK;
+    }
+    case TMG_PH_REDUCE: {
+      LAUNCH3("k3_reduce_parts", k3_reduce_parts, 1, 512, e->part_sum, e->part_max, e->top_parts, e->red);
+      return TMG_OK;
+    }
+    case TMG_PH_REPL: {
+      const dim3 blk(kTX, kTY, kTZ);
+      const int lcs = std::min(e->lc, e->ls - 1);  // the one-block chain stays below ls
+      for (int q = e->ls - 1; q > lcs; --q) {
+        Lvl3& c = e->L[q];
+        Down3 a = make_down(e, q, true);
+        if (boxmg && jac) LAUNCH3(kname("k3_down", q), (k3_down_c<true, true>), c.c_grid, 128, a);
+        else if (boxmg) LAUNCH3(kname("k3_down", q), (k3_down_c<true, false>), c.c_grid, 128, a);
+        else if (jac) LAUNCH3(kname("k3_down", q), (k3_down_c<false, true>), c.c_grid, 128, a);
+        else LAUNCH3(kname("k3_down", q), (k3_down_c<false, false>), c.c_grid, 128, a);
+        if (jac && q > e->lmin) {
+          SmoothS sa = make_smooth_s(e, q);
+          LAUNCH3(kname("k3_smooth", q), k3_smooth_s, c.s_blocks, sblk, sa);
+        }
+      }
+      Chain3 ch{};
+      ch.l0 = e->lmin;
+      ch.lc = lcs;
+      ch.do_up = 1;
+      ch.jac = jac ? 1 : 0;
+      ch.part_sum = e->red;
+      ch.part_max = e->red + 1;
+      ch.nparts = 1;
+      ch.hist = e->hist;
+      ch.counter = e->counter;
+      ch.cap = e->cap;
+      for (int q = e->lmin; q <= lcs; ++q) {
+        ch.down[q - e->lmin] = make_down(e, q, true);
+        ch.smooth[q - e->lmin] = make_smooth(e, q);
+        ch.up[q - e->lmin] = make_up(e, q);
+      }
+      LAUNCH3("k3_chain", k3_chain, 1, kChainBlock, ch);
+      for (int q = lcs + 1; q < e->ls; ++q) {
+        Up3 a = make_up(e, q);
+        const int g = e->L[q - 1].u_grid;
+        if (pi) LAUNCH3(kname("k3_up", q), k3_up, e->L[q].grid, blk, a);
+        else if (boxmg) LAUNCH3(kname("k3_up", q), k3_up_cell<true>, g, 128, a);
+        else LAUNCH3(kname("k3_up", q), k3_up_cell<false>, g, 128, a);
+      }
+      e->host_counter++;
+      return TMG_OK;
+    }
+    case TMG_PH_UP: {
+      if (l < e->ls || l > e->ltop) return fail3(e, TMG_EINVAL, "UP: level is not sharded");
+      const int lo = interior_lo(e, l), hi = interior_hi(e, l);
+      if (hi <= lo) return TMG_OK;
+      Up3 a = make_up(e, l);
+      a.ilo = lo;
+      a.ihi = hi;
+      a.l0 = e->ls;  // walk-down injection stays on the sharded levels
+      const int g = e->L[l - 1].u_grid;
+      if (pi) {
+        const dim3 blk(kTX, kTY, kTZ);
+        LAUNCH3(kname("k3_up", l), k3_up, e->L[l].grid, blk, a);
+      } else if (boxmg) LAUNCH3(kname("k3_up", l), k3_up_cell<true>, g, 128, a);
+      else LAUNCH3(kname("k3_up", l), k3_up_cell<false>, g, 128, a);
+      return TMG_OK;
+    }
+    case TMG_PH_INJECT: {
+      for (int q = e->ls - 1; q >= e->lmin; --q) {
+        const int n = e->L[q].N - 2;
+        if (n <= 0) continue;
+        k3_inject<<<nblk((size_t)n * n * n), 256, 0, e->s>>>(e->L[q].u, e->L[q].N, e->L[q + 1].u, e->L[q + 1].N);
+        CKL3();
+        e->launches++;
+      }
+      return TMG_OK;
+    }
+    default:
+      return fail3(e, TMG_EINVAL, "unknown phase");
+  }
+}
+
 }  // namespace
+
+int e3_shard(Engine3* e, int ls, const int32_t* lo, const int32_t* hi, std::string& err) {
+  ErrScope es(e, err);
+  if (ls <= e->lmin || ls > e->ltop) return fail3(e, TMG_EINVAL, "shard level must lie in (lmin, ltop]");
+  e->own_lo.assign(e->ltop + 1, 0);
+  e->own_hi.assign(e->ltop + 1, 0);
+  e->own_blocks.assign(e->ltop + 1, 0);
+  e->own_chunk.assign(e->ltop + 1, 1);
+  int maxb = 0;
+  for (int l = ls; l <= e->ltop; ++l) {
+    if (lo[l] < 0 || hi[l] > e->L[l].N || lo[l] > hi[l]) return fail3(e, TMG_EINVAL, "bad owned plane range");
+    e->own_lo[l] = lo[l];
+    e->own_hi[l] = hi[l];
+    const int a = std::max(1, lo[l]), b = std::min(e->L[l].N - 1, hi[l]);
+    tiling(e->L[l].N, a, std::max(a + 1, b), &e->own_chunk[l], &e->own_blocks[l]);
+    maxb = std::max(maxb, e->own_blocks[l]);
+  }
+  e->ls = ls;
+  e->sharded = true;
+  if (maxb > e->nparts) {
+    TRY3(alloc3(e, &e->part_sum, maxb));
+    TRY3(alloc3(e, &e->part_max, maxb));
+    e->nparts = maxb;
+  }
+  if (!e->red) TRY3(alloc3(e, &e->red, 2));
+  CK3(cudaStreamSynchronize(e->s));
+  return TMG_OK;
+}
+
+int e3_phase(Engine3* e, int phase, int level, std::string& err) {
+  ErrScope es(e, err);
+  if (!e->sharded) return fail3(e, TMG_EINVAL, "handle is not sharded (tmg3_shard)");
+  return phase3(e, phase, level);
+}
+
+int e3_field(Engine3* e, int field, int level, uint64_t* ptr, int64_t* count, std::string& err) {
+  ErrScope es(e, err);
+  if (field == TMG_F_PART) {
+    if (!e->red) return fail3(e, TMG_EINVAL, "no reduction buffer (tmg3_shard first)");
+    *ptr = (uint64_t)(uintptr_t)e->red;
+    *count = 2;
+    return TMG_OK;
+  }
+  TRY3(check_level(e, level));
+  Lvl3& c = e->L[level];
+  double* p = nullptr;
+  switch (field) {
+    case TMG_F_U: p = c.u; break;
+    case TMG_F_RHO: p = c.rho; break;
+    case TMG_F_SM: p = c.sm; break;
+    case TMG_F_CARRY: p = c.carry; break;
+    case TMG_F_G: p = c.g; break;
+    default: return fail3(e, TMG_EINVAL, "unknown field");
+  }
+  if (!p) return fail3(e, TMG_EINVAL, "field not allocated on this level");
+  *ptr = (uint64_t)(uintptr_t)p;
+  *count = (int64_t)c.nv;
+  return TMG_OK;
+}
+
+int e3_stream(Engine3* e, uint64_t* s) {
+  *s = (uint64_t)(uintptr_t)e->s;
+  return TMG_OK;
+}
+
+int e3_history(Engine3* e, int count, tmg_stats* out, std::string& err) {
+  ErrScope es(e, err);
+  if (count < 0 || count > e->cap || count > e->host_counter) return fail3(e, TMG_EINVAL, "bad history count");
+  return read_stats(e, e->host_counter - count, count, out);
+}
 
 // ============================================================================
 // internal interface (engine3.h)

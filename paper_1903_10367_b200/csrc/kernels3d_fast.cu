@@ -323,7 +323,9 @@ __global__ void __launch_bounds__(128) k3_down_c(const __grid_constant__ Down3 a
 template <bool BOXMG>
 __global__ void __launch_bounds__(128) k3_up_cell(const __grid_constant__ Up3 a) {
   const int Nc = a.Nc, nc = Nc - 1, N = a.N;
-  const size_t ncube = (size_t)nc * nc * nc;
+  // coarse cell planes whose fine vertices 3I + ri intersect [ilo, ihi)
+  const int Ilo = a.ilo / 3, Ihi = min(nc, (a.ihi + 2) / 3);
+  const size_t ncube = (size_t)(Ihi - Ilo) * nc * nc;
   const size_t cnt = 9 * ncube;
   const size_t nvc = (size_t)Nc * Nc * Nc;
   const double* cc = a.carry_c;
@@ -333,7 +335,7 @@ __global__ void __launch_bounds__(128) k3_up_cell(const __grid_constant__ Up3 a)
     const size_t w = q - (size_t)rr * ncube;
     const int K = (int)(w % nc);
     const size_t w2 = w / nc;
-    const int J = (int)(w2 % nc), I = (int)(w2 / nc);
+    const int J = (int)(w2 % nc), I = Ilo + (int)(w2 / nc);
     const int ri = rr / 3, rj = rr - 3 * ri;
     const int i = 3 * I + ri, j = 3 * J + rj;
     if (i < a.ilo || i >= a.ihi || j < 1) continue;
@@ -372,6 +374,29 @@ __global__ void __launch_bounds__(128) k3_up_cell(const __grid_constant__ Up3 a)
         a.ul[lc][vid(a.Nl[lc], ii, jj, kk)] = un;
       }
     }
+  }
+}
+
+// Fold the stats partials of the finest-level launch into red[0] (sum, fixed
+// order) and red[1] (max); sharded runs then all-reduce red across ranks.
+__global__ void __launch_bounds__(512) k3_reduce_parts(const double* ps, const double* pm, int n, double* red) {
+  __shared__ double rs[16], rm[16];
+  double x = 0.0, y = 0.0;
+  for (int q = threadIdx.x; q < n; q += blockDim.x) {
+    x += ps[q];
+    y = fmax(y, pm[q]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    x += __shfl_down_sync(0xffffffffu, x, o);
+    y = fmax(y, __shfl_down_sync(0xffffffffu, y, o));
+  }
+  if ((threadIdx.x & 31) == 0) { rs[threadIdx.x >> 5] = x; rm[threadIdx.x >> 5] = y; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0, u = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { t += rs[q]; u = fmax(u, rm[q]); }
+    red[0] = t;
+    red[1] = u;
   }
 }
 

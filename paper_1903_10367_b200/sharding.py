@@ -1,0 +1,313 @@
+"""Multi-GPU slab sharding of the 3D cycle.
+
+The finest levels ``ls..ltop`` are cut into slabs of vertex planes along
+axis 0 (i, the slowest index, so a slab and every halo plane are contiguous
+in memory); level ``ls`` is chosen so every rank owns the same number (>= 3)
+of interior planes there, and the cut is refined by 3 per level above it, so
+a fine plane ``3A + r`` is owned by the owner of coarse plane ``A``.  Levels
+below ``ls`` (a few MB) are replicated and computed redundantly on every
+rank.  One process per GPU; the reference is serial, so this
+module has no reference counterpart.
+
+Per cycle, phase by phase (``tmg3_phase``), with the data exchanges between
+phases:
+
+==========================  ==================================================
+phase                       exchange after it
+==========================  ==================================================
+DOWN(l), l = ltop..ls       rho_l: planes a-2, a-1 from rank r-1, b from r+1
+SMOOTH(l) (adaFACx)         sm_l: planes a-2, a-1 from rank r-1
+(l == ls)                   all-gather rho_ls, sm_ls (the replicated level
+                            ls-1 restricts from them)
+REDUCE                      all-reduce (sum of squares, max) of the residual
+REPL (levels lmin..ls-1)    --
+UP(l), l = ls..ltop         before it: carry_{l-1} plane B from rank r+1
+(after all UP)              u_l: planes a-1 from r-1 and b from r+1, every l;
+                            all-gather u_ls, then INJECT into the replicated
+                            levels
+==========================  ==================================================
+
+The exchanges are P2P send/recv and collectives on zero-copy torch views of
+the engine's device buffers, issued on the engine's own CUDA stream, so
+kernels and transfers are ordered without host synchronisation.  The same
+schedule drives CPU numpy shards over ``gloo`` in the tests
+(tests/test_sharding.py), which is how the host logic is checked without
+several GPUs.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+
+__all__ = ["choose_ls", "plan", "Plan", "DistTransport", "LocalTransport", "GpuShard",
+           "ShardedEngine3"]
+
+
+def choose_ls(depth: int, world: int, lmin: int = 1) -> int:
+    """Coarsest level with >= 3 interior planes per rank and an even split (else the
+    coarsest with >= 3 per rank)."""
+    cands = [l for l in range(lmin + 1, depth + 1) if 3**l - 1 >= 3 * world]
+    if not cands:
+        raise ValueError(f"depth {depth} is too shallow to shard over {world} ranks")
+    for l in cands:
+        if (3**l - 1) % world == 0:
+            return l
+    return cands[0]
+
+
+@dataclass
+class Plan:
+    depth: int
+    world: int
+    ls: int
+    own: dict  # level -> list of (lo, hi) vertex-plane ranges, one per rank
+
+    def rng(self, level: int, rank: int) -> tuple[int, int]:
+        return self.own[level][rank]
+
+    def interior(self, level: int, rank: int) -> tuple[int, int]:
+        lo, hi = self.own[level][rank]
+        N = 3**level + 1
+        return max(lo, 1), min(hi, N - 1)
+
+    def balanced(self, level: int) -> bool:
+        sizes = {self.interior(level, r)[1] - self.interior(level, r)[0] for r in range(self.world)}
+        return len(sizes) == 1
+
+
+def plan(depth: int, world: int, lmin: int = 1, ls: int | None = None) -> Plan:
+    ls = choose_ls(depth, world, lmin) if ls is None else ls
+    n = 3**ls - 1
+    q, rem = divmod(n, world)
+    sizes = [q + (1 if r < rem else 0) for r in range(world)]
+    if min(sizes) < 3:
+        raise ValueError("every rank must own at least 3 interior planes at the shard level")
+    cuts = [0]
+    acc = 1
+    for r in range(world - 1):
+        acc += sizes[r]
+        cuts.append(acc)
+    cuts.append(3**ls + 1)
+    own = {}
+    for l in range(ls, depth + 1):
+        f = 3 ** (l - ls)
+        N = 3**l + 1
+        own[l] = [(cuts[r] * f, min(cuts[r + 1] * f, N)) for r in range(world)]
+    return Plan(depth, world, ls, own)
+
+
+# ---------------------------------------------------------------------------
+# transports: how halo planes, gathers and reductions move between shards
+
+
+class DistTransport:
+    """torch.distributed (NCCL on GPUs, gloo on CPU) for one rank per process."""
+
+    def __init__(self, pl: Plan, rank: int):
+        import torch.distributed as dist
+        self.dist, self.pl, self.rank = dist, pl, rank
+
+    def halo(self, views, level: int, w_dn: int, w_up: int) -> None:
+        """views[0]: this rank's (N,N,N) field view.  Receive w_dn planes below
+        the owned range from rank-1 and w_up above it from rank+1."""
+        d, r, R = self.dist, self.rank, self.pl.world
+        v = views[0]
+        a, b = self.pl.rng(level, r)
+        ops = []
+        if r > 0:
+            if w_up:
+                ops.append(d.P2POp(d.isend, v[a:a + w_up], r - 1))
+            if w_dn:
+                ops.append(d.P2POp(d.irecv, v[a - w_dn:a], r - 1))
+        if r < R - 1:
+            if w_dn:
+                ops.append(d.P2POp(d.isend, v[b - w_dn:b], r + 1))
+            if w_up:
+                ops.append(d.P2POp(d.irecv, v[b:b + w_up], r + 1))
+        if ops:
+            for req in d.batch_isend_irecv(ops):
+                req.wait()
+
+    def gather(self, views, level: int) -> None:
+        """Fill every interior plane of views[0] from its owner."""
+        import torch
+        d, pl, r = self.dist, self.pl, self.rank
+        v = views[0]
+        N = v.shape[0]
+        lo, hi = pl.interior(level, r)
+        if pl.balanced(level):
+            d.all_gather_into_tensor(v[1:N - 1], v[lo:hi].clone())
+            return
+        m = max(pl.interior(level, q)[1] - pl.interior(level, q)[0] for q in range(pl.world))
+        send = torch.zeros((m,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device)
+        send[:hi - lo] = v[lo:hi]
+        out = torch.empty((pl.world * m,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device)
+        d.all_gather_into_tensor(out, send)
+        for q in range(pl.world):
+            ql, qh = pl.interior(level, q)
+            v[ql:qh] = out[q * m:q * m + (qh - ql)]
+
+    def reduce(self, parts) -> None:
+        d = self.dist
+        p = parts[0]
+        d.all_reduce(p[0:1], op=d.ReduceOp.SUM)
+        d.all_reduce(p[1:2], op=d.ReduceOp.MAX)
+
+
+class LocalTransport:
+    """All shards in one process (tests on one GPU or on CPU): views is the list of
+    every shard's view, in rank order; copies are plain tensor / array copies."""
+
+    def __init__(self, pl: Plan, sync=None):
+        self.pl, self.sync = pl, sync
+
+    def _s(self):
+        if self.sync:
+            self.sync()
+
+    def halo(self, views, level: int, w_dn: int, w_up: int) -> None:
+        self._s()
+        R = self.pl.world
+        for r in range(R):
+            a, b = self.pl.rng(level, r)
+            if r > 0 and w_dn:
+                views[r][a - w_dn:a] = views[r - 1][a - w_dn:a]
+            if r < R - 1 and w_up:
+                views[r][b:b + w_up] = views[r + 1][b:b + w_up]
+        self._s()
+
+    def gather(self, views, level: int) -> None:
+        self._s()
+        for r in range(self.pl.world):
+            for q in range(self.pl.world):
+                if q != r:
+                    lo, hi = self.pl.interior(level, q)
+                    views[r][lo:hi] = views[q][lo:hi]
+        self._s()
+
+    def reduce(self, parts) -> None:
+        self._s()
+        s = sum(float(p[0]) for p in parts)
+        m = max(float(p[1]) for p in parts)
+        for p in parts:
+            p[0] = s
+            p[1] = m
+        self._s()
+
+
+# ---------------------------------------------------------------------------
+# the GPU shard: one GpuEngine (3D) restricted to its slab
+
+
+class _CAI:
+    def __init__(self, ptr: int, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8",
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+class GpuShard:
+    """Phase-level access to a sharded 3D GpuEngine."""
+
+    def __init__(self, eng, pl: Plan, rank: int):
+        import ctypes as C
+        import torch
+        self.eng, self.pl, self.rank = eng, pl, rank
+        L = _abi.lib()
+        top = eng.ltop
+        lo = (C.c_int32 * (top + 1))()
+        hi = (C.c_int32 * (top + 1))()
+        for l in range(pl.ls, top + 1):
+            lo[l], hi[l] = pl.rng(l, rank)
+        _abi.check(L.tmg3_shard(eng._h, pl.ls, lo, hi))
+        s = C.c_uint64()
+        _abi.check(L.tmg3_stream(eng._h, C.byref(s)))
+        self.stream = torch.cuda.ExternalStream(s.value, device=torch.device("cuda", eng.device))
+        self._views = {}
+
+    def view(self, field: int, level: int):
+        key = (field, level)
+        if key not in self._views:
+            import ctypes as C
+            import torch
+            p, n = C.c_uint64(), C.c_int64()
+            _abi.check(_abi.lib().tmg3_field(self.eng._h, field, level, C.byref(p), C.byref(n)))
+            if field == _abi.F_PART:
+                shape = (2,)
+            else:
+                N = 3**level + 1
+                shape = (N, N, N)
+            self._views[key] = torch.as_tensor(_CAI(p.value, shape), device=f"cuda:{self.eng.device}")
+        return self._views[key]
+
+    def phase(self, ph: int, level: int = 0) -> None:
+        _abi.check(_abi.lib().tmg3_phase(self.eng._h, ph, level))
+
+    def history(self, n: int):
+        import ctypes as C
+        out = (_abi.Stats * max(n, 1))()
+        _abi.check(_abi.lib().tmg3_history(self.eng._h, n, C.cast(out, C.c_void_p)))
+        return [self.eng._stats(out[k]) for k in range(n)]
+
+
+class ShardedEngine3:
+    """The sharded cycle (schedule above) over a list of local shards and a transport.
+
+    ``shards`` holds this process's shard(s): one with DistTransport (one rank
+    per process), all of them with LocalTransport.
+    """
+
+    def __init__(self, shards, transport, variant: str, lmin: int = 1):
+        self.shards, self.tr = shards, transport
+        self.pl = shards[0].pl
+        self.jac = variant == "adafac-jac"
+        self.lmin = lmin
+
+    def _views(self, field, level):
+        return [s.view(field, level) for s in self.shards]
+
+    def cycle(self) -> None:
+        pl, tr = self.pl, self.tr
+        ls, top = pl.ls, pl.depth
+        for l in range(top, ls - 1, -1):
+            for s in self.shards:
+                s.phase(_abi.PH_DOWN, l)
+            tr.halo(self._views(_abi.F_RHO, l), l, 2, 1)
+            if self.jac:
+                for s in self.shards:
+                    s.phase(_abi.PH_SMOOTH, l)
+                if l > ls:
+                    tr.halo(self._views(_abi.F_SM, l), l, 2, 0)
+            if l == ls:
+                tr.gather(self._views(_abi.F_RHO, l), l)
+                if self.jac:
+                    tr.gather(self._views(_abi.F_SM, l), l)
+        for s in self.shards:
+            s.phase(_abi.PH_REDUCE)
+        tr.reduce(self._views(_abi.F_PART, 0))
+        for s in self.shards:
+            s.phase(_abi.PH_REPL)
+        for l in range(ls, top + 1):
+            if l - 1 >= ls:
+                tr.halo(self._views(_abi.F_CARRY, l - 1), l - 1, 0, 1)
+            for s in self.shards:
+                s.phase(_abi.PH_UP, l)
+        for l in range(ls, top + 1):
+            tr.halo(self._views(_abi.F_U, l), l, 1, 1)
+        tr.gather(self._views(_abi.F_U, ls), ls)
+        for s in self.shards:
+            s.phase(_abi.PH_INJECT)
+
+    def run(self, n: int):
+        for _ in range(n):
+            self.cycle()
+        return self.shards[0].history(n)
+
+
+def owned_u(pl: Plan, level: int, rank: int, u: np.ndarray) -> np.ndarray:
+    """The planes of u a rank owns (for assembling a global iterate in tests)."""
+    lo, hi = pl.rng(level, rank)
+    return u[lo:hi]

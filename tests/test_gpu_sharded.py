@@ -1,0 +1,91 @@
+"""Sharded 3D cycle on the GPU kernels (one B200 available).
+
+Several GpuShards (each a full GpuEngine restricted to its slab with
+tmg3_shard) run in ONE process on cuda:0 and exchange planes with
+LocalTransport (device copies between their buffers, streams synchronised at
+every exchange), so no rank ever waits on another rank's kernel.  The result
+must equal the unsharded GPU engine bit for bit (u on every owned plane);
+the residual norms differ only by the per-rank partial sums (1e-13).  A
+world-size-1 NCCL process group exercises DistTransport's collectives on
+zero-copy views of the engine buffers on the engine's stream.
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1903_10367_b200 import GpuEngine, SolverConfig, sharding, workloads
+
+pytestmark = pytest.mark.gpu
+
+
+def serial(wl, n, variant):
+    eng = GpuEngine(wl.tree, SolverConfig(variant=variant, flavor=wl.flavor), sync="lazy")
+    eng.rhs.update(wl.rhs)
+    h = eng.advance_many(n)
+    eng.pull()
+    return h
+
+
+def sharded_local(mk, world, n, variant):
+    wl0 = mk()
+    pl = sharding.plan(wl0.tree.depth, world)
+    shards, wls = [], []
+    for r in range(world):
+        wl = mk()
+        eng = GpuEngine(wl.tree, SolverConfig(variant=variant, flavor=wl.flavor), sync="lazy")
+        eng.rhs.update(wl.rhs)
+        eng._flush_rhs()
+        shards.append(sharding.GpuShard(eng, pl, r))
+        wls.append(wl)
+    se = sharding.ShardedEngine3(shards, sharding.LocalTransport(pl, sync=torch.cuda.synchronize), variant)
+    h = se.run(n)
+    for s in shards:
+        s.eng.pull()
+    return pl, wls, shards, h
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name,variant", [("config5-L4", "adafac-jac"), ("config3-L4", "adafac-jac"),
+                                          ("config5-L4", "additive"), ("config3-L4", "afacc")])
+def test_gpu_sharded_equals_serial(world, name, variant):
+    mk = lambda: workloads.by_name(name)  # noqa: E731
+    wl = mk()
+    n = 4
+    hs = serial(wl, n, variant)
+    pl, wls, shards, h = sharded_local(mk, world, n, variant)
+    np.testing.assert_allclose([s.l2h for s in h], [s.l2h for s in hs], rtol=1e-13)
+    assert [s.linf for s in h] == [s.linf for s in hs]
+    top = wl.tree.depth
+    for r in range(world):
+        for l in range(pl.ls, top + 1):
+            lo, hi = pl.rng(l, r)
+            assert np.array_equal(wls[r].tree.u[l][lo:hi], wl.tree.u[l][lo:hi]), f"rank {r} level {l}"
+        for l in range(wl.tree.lmin, pl.ls):
+            assert np.array_equal(wls[r].tree.u[l], wl.tree.u[l]), f"rank {r} replicated level {l}"
+
+
+def test_gpu_dist_transport_world1_nccl():
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29631")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        wl = workloads.by_name("config5-L4")
+        hs = serial(wl, 3, wl.variant)
+        wl2 = workloads.by_name("config5-L4")
+        pl = sharding.plan(wl2.tree.depth, 1)
+        eng = GpuEngine(wl2.tree, SolverConfig(variant=wl2.variant, flavor=wl2.flavor), sync="lazy")
+        eng.rhs.update(wl2.rhs)
+        eng._flush_rhs()
+        sh = sharding.GpuShard(eng, pl, 0)
+        se = sharding.ShardedEngine3([sh], sharding.DistTransport(pl, 0), wl2.variant)
+        with torch.cuda.stream(sh.stream):
+            h = se.run(3)
+        eng.pull()
+        np.testing.assert_allclose([s.l2h for s in h], [s.l2h for s in hs], rtol=1e-13)
+        assert np.array_equal(wl2.tree.u[4], wl.tree.u[4])
+    finally:
+        dist.destroy_process_group()
