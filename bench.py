@@ -1,29 +1,36 @@
 """Benchmark: fine-grid DoF updates/s per adaFACx cycle (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload config2|config1|config4|config2-small|config4-small]
+                    [--workload config5|config3|config2|config1|config4|...-small]
 
 A step is one additive cycle (ReferenceEngine.advance, solvers.py:334-399)
-over the resident level hierarchy.  Default workload: BASELINE configs[1]
-(2D adaFACx + BoxMG/Galerkin, depth 6, per-block log-uniform eps, seeded).
+over the resident level hierarchy.  Default workload: BASELINE configs[4],
+the 3D depth-6 adaFACx + BoxMG config the north star's targets (>= 70 % of
+HBM on 1 GPU, >= 80 % parallel efficiency at 8) are stated on: 385.8 M fine
+DoFs, eps log-uniform per 27^3-cell block, seeded.  configs[1] (2D, 0.53 M
+fine DoFs, L2-resident and latency-bound) is ``--workload config2``.
 
 * value      -- N_fine / t_cycle, device time (CUDA events on the engine's
-                stream, graph replay), L2 flushed (256 MiB write) before every
-                timed cycle; N_fine = composite DoFs of the finest level.
+                stream, graph replay); 2D: L2 flushed (256 MiB write) before
+                every timed cycle; 3D config5: inputs 60x larger than L2.
 * e2e        -- same metric through the drop-in API (GpuEngine, sync="eager"):
                 every step uploads tree.u (all levels, pinned host memory),
                 runs one cycle, downloads tree.u and the cycle's stats.
 * roofline   -- dominant kernel: algorithmic bytes per launch / mean launch
-                time (events around each launch, tmg_profile_cycles).
-* cpu_baseline -- the CPU oracle port (oracle/mg2d.py, numpy, 1 core) on a
-                bounded sample of the same workload.
-* --impl reference -- the reference's CPU algorithm (oracle port; the
+                time (events around each launch, tmg_profile_cycles); also the
+                whole-cycle B_alg / t_cycle.
+* cpu_baseline -- the CPU oracle port on 1 core on a bounded sample (2D:
+                oracle/mg2d.py on the workload itself; 3D: oracle/mg3d.py on
+                the same structure at depth 4 -- there is no 3D reference).
+* --impl reference -- the reference's CPU algorithm (the oracle port; the
                 reference is pure Python and cannot travel to the box) on the
-                same workload; rank 0 only.
+                same workload (3D: the depth-4 sample); rank 0 only.
 
-Multi-GPU: the 2D workloads do not shard (replicas only);
-under torchrun every rank runs an independent replica on its own GPU, timing
-is the max over ranks and value counts the DoFs of all replicas.
+Multi-GPU (torchrun, one process per GPU): 3D workloads are slab-sharded
+over the ranks with NCCL (paper_1903_10367_b200/sharding.py; strong
+scaling, max-over-ranks device time); the 2D workloads do not shard
+(replicas only): every rank runs an independent replica and
+value counts the DoFs of all replicas.
 """
 
 from __future__ import annotations
@@ -53,29 +60,39 @@ def dist_env():
 
 
 class Dist:
-    def __init__(self):
+    """One process per GPU.  NCCL when the workload shards (3D), gloo for the 2D
+    replicas (whose only collectives are the barrier and the timing max)."""
+
+    def __init__(self, nccl: bool = False, force: bool = False):
         self.ws, self.rank, self.local = dist_env()
-        self.pg = None
-        if self.ws > 1:
+        self.nccl = nccl and (self.ws > 1 or force)
+        self.td = None
+        if self.ws > 1 or (force and nccl):
+            import torch
             import torch.distributed as td
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            td.init_process_group("gloo")
+            if self.nccl:
+                torch.cuda.set_device(self.local)
+                td.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                td.init_process_group("gloo")
             self.td = td
 
     def barrier(self):
-        if self.ws > 1:
+        if self.td is not None:
             self.td.barrier()
 
     def max(self, x: float) -> float:
-        if self.ws == 1:
+        if self.td is None:
             return x
         import torch
-        t = torch.tensor([x], dtype=torch.float64)
+        dev = torch.device("cuda", self.local) if self.nccl else torch.device("cpu")
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
         self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
         return float(t.item())
 
     def close(self):
-        if self.ws > 1:
+        if self.td is not None:
             self.td.destroy_process_group()
 
 
@@ -449,22 +466,131 @@ def run_ours(args, dist: Dist):
         print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, dist: Dist):
+    """3D workload slab-sharded over the ranks (strong scaling)."""
+    import torch
+
+    from paper_1903_10367_b200 import GpuEngine, SolverConfig, sharding, workloads
+    from paper_1903_10367_b200 import build as b
+
+    if dist.rank == 0:
+        b.build()
+    dist.barrier()
+    dev = dist.local
+    torch.cuda.set_device(dev)
+    wl = workloads.by_name(args.workload)
+    n_fine = wl.fine_dofs()
+    pl = sharding.plan(wl.tree.depth, dist.ws)
+    eng = GpuEngine(wl.tree, SolverConfig(variant=wl.variant, flavor=wl.flavor), device=dev,
+                    sync="lazy")
+    eng.rhs.update(wl.rhs)
+    eng._flush_rhs()
+    sh = sharding.GpuShard(eng, pl, dist.rank)
+    se = sharding.ShardedEngine3([sh], sharding.DistTransport(pl, dist.rank), wl.variant)
+    st = sh.stream
+    with torch.cuda.stream(st):
+        for _ in range(max(args.warmup, 3)):
+            se.cycle()
+        torch.cuda.synchronize()
+        clk = ClockSampler(dev)
+        clk.start()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(args.steps):
+            se.cycle()
+        e1.record(st)
+        torch.cuda.synchronize()
+        dist.barrier()
+        clocks = clk.stop()
+        ms = e0.elapsed_time(e1)
+        hist = sh.history(1)
+        # e2e: every step uploads this rank's owned u planes (all sharded levels) from
+        # pinned host memory, runs one cycle and reads them back with the stats
+        views = {l: sh.view(0, l) for l in range(pl.ls, wl.ltop + 1)}
+        host = {l: torch.empty_like(views[l][slice(*pl.rng(l, dist.rank))], device="cpu").pin_memory()
+                for l in views}
+        for l in views:
+            host[l].copy_(views[l][slice(*pl.rng(l, dist.rank))])
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            for l in views:
+                views[l][slice(*pl.rng(l, dist.rank))].copy_(host[l], non_blocking=True)
+            se.cycle()
+            for l in views:
+                host[l].copy_(views[l][slice(*pl.rng(l, dist.rank))], non_blocking=True)
+            sh.history(1)
+        torch.cuda.synchronize()
+        t_e2e = dist.max(time.perf_counter() - t0)
+    ms_max = dist.max(ms)
+    ms_step = ms_max / args.steps
+    value = n_fine / (ms_step * 1e-3)
+    bm = bytes_model3(eng, wl)
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    per_gpu = bm["cycle"] / dist.ws / (ms_step * 1e-3) / 1e9
+    jac = wl.variant == "adafac-jac"
+    lcs = min(2, pl.ls - 1)
+    launches = (wl.ltop - pl.ls + 1) * (3 if jac else 2) + 1 + 2 * (pl.ls - 1 - lcs) * (1 + jac) + 1 \
+        + (pl.ls - wl.tree.lmin)
+    hb = sum(host[l].numel() * 8 for l in host)
+    if dist.rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, SURVEY.md §8(d))",
+            "config": {"workload": wl.name, "levels": f"{wl.tree.lmin}..{wl.ltop}",
+                       "variant": wl.variant, "flavor": wl.flavor, "n_fine": n_fine,
+                       "parallelism": f"slab{dist.ws} (levels {pl.ls}..{wl.ltop} sharded on axis 0, "
+                                      f"levels {wl.tree.lmin}..{pl.ls - 1} replicated)",
+                       "l2": "inputs larger than L2 (no flush)",
+                       "l2h_last": hist[0].l2h},
+            "roofline": {"bound": "hbm", "kernel": "cycle (per GPU)", "achieved": per_gpu, "peak": peak,
+                         "unit": "GB/s", "frac": per_gpu / peak, "traffic": None,
+                         "cycle_B_alg": bm["cycle"]},
+            "cpu_baseline": None,
+            "e2e": {"value": n_fine * args.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": hb,
+                    "d2h_bytes_per_step": hb + 32, "ms_per_step": 1e3 * t_e2e / args.steps,
+                    "api": "ShardedEngine3.cycle() with owned u planes copied in/out per step (rank 0's bytes)"},
+            "clocks": clocks, "gpu_launches": launches * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    # release every torch object tied to the engine's stream before the engine (and its
+    # stream) goes away: pinned blocks record events on the streams that used them
+    del host, views
+    sh.close()
+    torch.cuda.synchronize()
+    eng.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--workload", default="config2")
+    ap.add_argument("--workload", default="config5")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--force-shard", action="store_true",
+                    help="3D: run the sharded (NCCL) path even on one rank (testing)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    dist = Dist()
+    three_d = args.workload.startswith(("config3", "config5"))
+    ws = dist_env()[0]
+    dist = Dist(nccl=three_d and args.impl == "ours" and (ws > 1 or args.force_shard),
+                force=args.force_shard)
     try:
         if args.impl == "reference":
             run_reference(args, dist)
+        elif three_d and (dist.ws > 1 or args.force_shard):
+            run_sharded(args, dist)
         else:
             run_ours(args, dist)
     finally:

@@ -92,9 +92,9 @@ __global__ void k_eff(double* __restrict__ eff, double* __restrict__ epsm, doubl
 // arr[0] > 0 and every entry equals arr[0].
 __global__ void k_const_check(const double* __restrict__ arr, size_t n, int* __restrict__ flag) {
   const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
   const double first = arr[0];
-  if (!(first > 0.0) || arr[c] != first) atomicAnd(flag, 0);
+  const bool bad = c < n && (!(first > 0.0) || arr[c] != first);
+  if (__ballot_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicAnd(flag, 0);
 }
 
 // counts of each kind + hanging (for masks sums, solvers.py:443, 449-459)

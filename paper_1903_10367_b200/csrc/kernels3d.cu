@@ -463,9 +463,10 @@ __global__ void k3_scale(double* out, const double* in, double h, size_t n) {
 
 __global__ void k3_const_check(const double* arr, size_t n, int* flag) {
   const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
   const double first = arr[0];
-  if (!(first > 0.0) || arr[c] != first) atomicAnd(flag, 0);
+  const bool bad = c < n && (!(first > 0.0) || arr[c] != first);
+  // one atomic per warp that saw a mismatch (not one per element)
+  if (__ballot_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicAnd(flag, 0);
 }
 
 // Source of fine 27-point rows: a stored table, or assembled on the fly from

@@ -246,6 +246,10 @@ class GpuShard:
     def phase(self, ph: int, level: int = 0) -> None:
         _abi.check(_abi.lib().tmg3_phase(self.eng._h, ph, level))
 
+    def close(self) -> None:
+        """Drop the zero-copy views (call before the engine is closed)."""
+        self._views.clear()
+
     def history(self, n: int):
         import ctypes as C
         out = (_abi.Stats * max(n, 1))()
