@@ -3,13 +3,16 @@
 // graph.  Reached through the C ABI of engine.cu (tmg3_create and the
 // dimension-dispatching tmg_* entry points).
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
 #include "engine3.h"
 #include "kernels3d.cu"
 #include "kernels3d_fast.cu"
+#include "kernels3d_ffp.cu"
 
 namespace {
 
@@ -20,6 +23,7 @@ struct Lvl3 {
   size_t nv = 0, ncell = 0;
   double *u = nullptr, *rhs = nullptr, *g = nullptr, *rho = nullptr, *sm = nullptr, *carry = nullptr;
   double *eff = nullptr, *coef = nullptr, *tbl = nullptr, *P = nullptr;
+  double *bR = nullptr, *bT = nullptr;  // level ltop-1: restrictions from the fused fine pass
   Op3 op{};
   double w = 0.0;
   int grid = 0, part_off = 0;
@@ -83,6 +87,15 @@ struct Engine3 {
   std::vector<int> own_chunk;
   double* red = nullptr;            // {sum, max} of this cycle's stats
   int top_parts = 0;
+  // fused fine pass (pipelined schedule): the finest level's u and g are double
+  // buffered; after a cycle the finest level carries a pending correction
+  // P carry_{ltop-1} + g that the next cycle's fused pass (or flush) applies
+  bool ffp = false, fpend = false;
+  int pu = 0, pg = 0;
+  double* ubuf[2] = {nullptr, nullptr};
+  double* gbuf[2] = {nullptr, nullptr};
+  int ffp_tiles = 0, ffp_chunk = 0, ffp_blocks = 0;
+  std::map<int, cudaGraphExec_t> gcache;
 };
 
 namespace {
@@ -123,10 +136,12 @@ int alloc3(Engine3* e, T** p, size_t count, bool zero = true) {
 }
 
 void free3(Engine3* e) {
-  if (e->gexec) {
-    cudaGraphExecDestroy(e->gexec);
-    e->gexec = nullptr;
-  }
+  if (e->gexec && e->gcache.empty()) cudaGraphExecDestroy(e->gexec);
+  e->gexec = nullptr;
+  for (auto& kv : e->gcache) cudaGraphExecDestroy(kv.second);
+  e->gcache.clear();
+  e->ffp = e->fpend = false;
+  e->pu = e->pg = 0;
   for (void* p : e->allocs) cudaFree(p);
   e->allocs.clear();
   e->L.clear();
@@ -331,7 +346,116 @@ int enqueue_down(Engine3* e, bool write) {
   return TMG_OK;
 }
 
+Ffp3 make_ffp(Engine3* e, bool apply) {
+  const int l1 = e->ltop, lC = l1 - 1;
+  Lvl3& c = e->L[l1];
+  Lvl3& cc = e->L[lC];
+  Ffp3 a{};
+  a.N = c.N;
+  a.Nc = cc.N;
+  a.tiles = e->ffp_tiles;
+  a.chunk = e->ffp_chunk;
+  a.apply = apply ? 1 : 0;
+  a.variant = e->cfg.variant;
+  a.jac = e->cfg.variant == VAR_JAC;
+  a.u_in = e->ubuf[e->pu];
+  a.u_out = e->ubuf[e->pu ^ 1];
+  a.g_in = e->gbuf[e->pg];
+  a.g_out = e->gbuf[e->pg ^ 1];
+  a.carry_c = cc.carry;
+  a.P = cc.P;
+  a.op = c.op;
+  a.rhs = c.rhs;
+  a.w = c.w;
+  a.hw = std::pow(3.0, -1.5 * l1);
+  a.scale = e->cfg.omega * 3.0 / 8.0;
+  a.bR = cc.bR;
+  a.bT = cc.bT;
+  a.l = l1;
+  a.l0 = e->lmin;
+  for (int k = e->lmin; k < l1; ++k) {
+    a.ul[k] = e->L[k].u;
+    a.Nl[k] = e->L[k].N;
+  }
+  a.part_sum = e->part_sum;
+  a.part_max = e->part_max;
+  return a;
+}
+
+// One cycle with the fused fine pass: FFP (finest level), then the coarse levels.
+int enqueue_cycle_ffp(Engine3* e, bool apply) {
+  const bool jac = e->cfg.variant == VAR_JAC;
+  const dim3 sblk(kSX, kSY);
+  Ffp3 f = make_ffp(e, apply);
+  {
+    cudaEvent_t e0_ = nullptr;
+    TRY3(begin_k(e, &e0_));
+    k3_ffp<<<e->ffp_blocks, kFThreads, kFfpSmem, e->s>>>(f);
+    CKL3();
+    TRY3(end_k(e, kname("k3_down", e->ltop), e0_));
+  }
+  for (int l = e->ltop - 1; l > e->lc; --l) {
+    Lvl3& c = e->L[l];
+    Down3 a = make_down(e, l, true);
+    if (l == e->ltop - 1) {
+      a.bR = c.bR;
+      a.bT = c.bT;
+      if (jac) LAUNCH3(kname("k3_down", l), (k3_down_c<true, true, true>), c.c_grid, 128, a);
+      else LAUNCH3(kname("k3_down", l), (k3_down_c<true, false, true>), c.c_grid, 128, a);
+    } else if (jac) {
+      LAUNCH3(kname("k3_down", l), (k3_down_c<true, true>), c.c_grid, 128, a);
+    } else {
+      LAUNCH3(kname("k3_down", l), (k3_down_c<true, false>), c.c_grid, 128, a);
+    }
+    if (jac && l > e->lmin) {
+      SmoothS sa = make_smooth_s(e, l);
+      LAUNCH3(kname("k3_smooth", l), k3_smooth_s, c.s_blocks, sblk, sa);
+    }
+  }
+  Chain3 ch{};
+  ch.l0 = e->lmin;
+  ch.lc = e->lc;
+  ch.do_up = 1;
+  ch.jac = jac ? 1 : 0;
+  ch.part_sum = e->part_sum;
+  ch.part_max = e->part_max;
+  ch.nparts = e->ffp_blocks;
+  ch.hist = e->hist;
+  ch.counter = e->counter;
+  ch.cap = e->cap;
+  for (int l = e->lmin; l <= e->lc; ++l) {
+    ch.down[l - e->lmin] = make_down(e, l, true);
+    ch.smooth[l - e->lmin] = make_smooth(e, l);
+    ch.up[l - e->lmin] = make_up(e, l);
+  }
+  LAUNCH3("k3_chain", k3_chain, 1, kChainBlock, ch);
+  for (int l = e->lc + 1; l <= e->ltop - 1; ++l) {
+    Up3 a = make_up(e, l);
+    LAUNCH3(kname("k3_up", l), k3_up_cell<true>, e->L[l - 1].u_grid, 128, a);
+  }
+  return TMG_OK;
+}
+
+// after a fused cycle: swap the finest level's buffers, the correction is pending
+void ffp_advance(Engine3* e, bool applied) {
+  if (applied) e->pu ^= 1;
+  e->pg ^= 1;
+  e->fpend = true;
+  e->L[e->ltop].u = e->ubuf[e->pu];
+  e->L[e->ltop].g = e->gbuf[e->pg];
+}
+
+// apply the pending correction of the finest level (+ its FAS injection) in place
+int ffp_flush(Engine3* e) {
+  if (!e->ffp || !e->fpend) return TMG_OK;
+  Up3 a = make_up(e, e->ltop);  // u = current buffer, g = latest d
+  LAUNCH3(kname("k3_up", e->ltop), k3_up_cell<true>, e->L[e->ltop - 1].u_grid, 128, a);
+  e->fpend = false;
+  return TMG_OK;
+}
+
 int enqueue_cycle(Engine3* e) {
+  if (e->ffp) return enqueue_cycle_ffp(e, e->fpend);
   TRY3(enqueue_down(e, true));
   const bool boxmg = e->cfg.flavor == TMG_BOXMG;
   const bool pi = e->cfg.variant == VAR_PI;
@@ -347,11 +471,34 @@ int enqueue_cycle(Engine3* e) {
 }
 
 int ensure_graph(Engine3* e) {
-  if (!e->graph_dirty && e->gexec) return TMG_OK;
-  if (e->gexec) {
-    cudaGraphExecDestroy(e->gexec);
+  if (e->graph_dirty) {
+    if (e->gexec && e->gcache.empty()) cudaGraphExecDestroy(e->gexec);
     e->gexec = nullptr;
+    for (auto& kv : e->gcache) cudaGraphExecDestroy(kv.second);
+    e->gcache.clear();
   }
+  if (e->ffp) {
+    // one graph per (pending, u parity, g parity) state of the double buffers
+    const int key = (e->fpend ? 4 : 0) + e->pu * 2 + e->pg;
+    auto it = e->gcache.find(key);
+    if (it == e->gcache.end()) {
+      cudaGraph_t g;
+      CK3(cudaStreamBeginCapture(e->s, cudaStreamCaptureModeThreadLocal));
+      e->launches = 0;
+      int rc = enqueue_cycle(e);
+      cudaError_t ce = cudaStreamEndCapture(e->s, &g);
+      if (rc != TMG_OK) return rc;
+      CK3(ce);
+      cudaGraphExec_t x;
+      CK3(cudaGraphInstantiate(&x, g, 0));
+      cudaGraphDestroy(g);
+      it = e->gcache.emplace(key, x).first;
+    }
+    e->gexec = it->second;
+    e->graph_dirty = false;
+    return TMG_OK;
+  }
+  if (!e->graph_dirty && e->gexec) return TMG_OK;
   cudaGraph_t g;
   CK3(cudaStreamBeginCapture(e->s, cudaStreamCaptureModeThreadLocal));
   e->launches = 0;
@@ -533,6 +680,34 @@ int build(Engine3* e, const tmg_tree3* t) {
       parts = c.s_blocks;
     }
   }
+  // fused fine pass: BoxMG, every variant but adafac-pi, a grid level below the top
+  {
+    // opt-in (TMG_FFP=1) until it beats the phase-by-phase cycle (profiles/r01_ffp_*)
+    const char* env = std::getenv("TMG_FFP");
+    const bool want = env && std::strcmp(env, "1") == 0;
+    e->ffp = want && cfg.flavor == TMG_BOXMG && cfg.variant != VAR_PI && l1 - 1 > e->lc;
+    e->fpend = false;
+    e->pu = e->pg = 0;
+    if (e->ffp) {
+      CK3(cudaFuncSetAttribute(k3_ffp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFfpSmem));
+      Lvl3& c = e->L[l1];
+      Lvl3& cc = e->L[l1 - 1];
+      e->ubuf[0] = c.u;
+      TRY3(alloc3(e, &e->ubuf[1], c.nv, false));
+      CK3(cudaMemcpyAsync(e->ubuf[1], c.u, sizeof(double) * c.nv, cudaMemcpyDeviceToDevice, e->s));
+      e->gbuf[0] = c.g;
+      TRY3(alloc3(e, &e->gbuf[1], c.nv));
+      TRY3(alloc3(e, &cc.bR, cc.nv));
+      TRY3(alloc3(e, &cc.bT, cc.nv));
+      e->ffp_tiles = (c.N - 1 + 3 * kFT - 1) / (3 * kFT);
+      const int t2 = e->ffp_tiles * e->ffp_tiles;
+      int nch = (8 * 148 + t2 - 1) / t2;
+      nch = std::max(1, std::min(nch, std::max(1, cc.N / 8)));
+      e->ffp_chunk = (cc.N + nch - 1) / nch;
+      e->ffp_blocks = t2 * ((cc.N + e->ffp_chunk - 1) / e->ffp_chunk);
+      parts = std::max(parts, e->ffp_blocks);
+    }
+  }
   e->nparts = parts;
   TRY3(alloc3(e, &e->part_sum, parts));
   TRY3(alloc3(e, &e->part_max, parts));
@@ -707,6 +882,11 @@ int phase3(Engine3* e, int phase, int l) {
 
 int e3_shard(Engine3* e, int ls, const int32_t* lo, const int32_t* hi, std::string& err) {
   ErrScope es(e, err);
+  TRY3(ffp_flush(e));
+  if (e->ffp) {  // sharded runs use the phase kernels on buffer 'current'
+    e->ffp = false;
+    e->graph_dirty = true;
+  }
   if (ls <= e->lmin || ls > e->ltop) return fail3(e, TMG_EINVAL, "shard level must lie in (lmin, ltop]");
   e->own_lo.assign(e->ltop + 1, 0);
   e->own_hi.assign(e->ltop + 1, 0);
@@ -775,6 +955,15 @@ int e3_history(Engine3* e, int count, tmg_stats* out, std::string& err) {
   return read_stats(e, e->host_counter - count, count, out);
 }
 
+// one cycle from the graph of the current state (+ the fused-pass state machine)
+int launch_cycle(Engine3* e) {
+  TRY3(ensure_graph(e));
+  const bool applied = e->fpend;
+  CK3(cudaGraphLaunch(e->gexec, e->s));
+  if (e->ffp) ffp_advance(e, applied);
+  return TMG_OK;
+}
+
 // ============================================================================
 // internal interface (engine3.h)
 // ============================================================================
@@ -839,7 +1028,10 @@ int e3_set_rhs(Engine3* e, int level, const double* rhs, std::string& err) {
 int e3_set_u(Engine3* e, int level, const double* u, std::string& err) {
   ErrScope es(e, err);
   TRY3(check_level(e, level));
+  TRY3(ffp_flush(e));
   CK3(cudaMemcpyAsync(e->L[level].u, u, sizeof(double) * e->L[level].nv, cudaMemcpyHostToDevice, e->s));
+  if (e->ffp && level == e->ltop)  // both buffers: the boundary values are never rewritten
+    CK3(cudaMemcpyAsync(e->ubuf[e->pu ^ 1], u, sizeof(double) * e->L[level].nv, cudaMemcpyHostToDevice, e->s));
   CK3(cudaStreamSynchronize(e->s));
   return TMG_OK;
 }
@@ -847,6 +1039,7 @@ int e3_set_u(Engine3* e, int level, const double* u, std::string& err) {
 int e3_get_u(Engine3* e, int level, double* u, std::string& err) {
   ErrScope es(e, err);
   TRY3(check_level(e, level));
+  TRY3(ffp_flush(e));
   CK3(cudaMemcpyAsync(u, e->L[level].u, sizeof(double) * e->L[level].nv, cudaMemcpyDeviceToHost, e->s));
   CK3(cudaStreamSynchronize(e->s));
   return TMG_OK;
@@ -854,6 +1047,7 @@ int e3_get_u(Engine3* e, int level, double* u, std::string& err) {
 
 int e3_update_fas_state(Engine3* e, std::string& err) {
   ErrScope es(e, err);
+  TRY3(ffp_flush(e));
   for (int l = e->ltop - 1; l >= e->lmin; --l) {
     const int n = e->L[l].N - 2;
     if (n <= 0) continue;
@@ -872,7 +1066,7 @@ int e3_cycle(Engine3* e, int ncycles, tmg_stats* stats, std::string& err) {
   while (done < ncycles) {
     const int chunk = std::min(ncycles - done, e->cap);
     const long long first = e->host_counter;
-    for (int k = 0; k < chunk; ++k) CK3(cudaGraphLaunch(e->gexec, e->s));
+    for (int k = 0; k < chunk; ++k) TRY3(launch_cycle(e));
     e->host_counter += chunk;
     if (stats) TRY3(read_stats(e, first, chunk, stats + done));
     else CK3(cudaStreamSynchronize(e->s));
@@ -883,6 +1077,7 @@ int e3_cycle(Engine3* e, int ncycles, tmg_stats* stats, std::string& err) {
 
 int e3_residual_stats(Engine3* e, tmg_stats* out, std::string& err) {
   ErrScope es(e, err);
+  TRY3(ffp_flush(e));
   TRY3(enqueue_down(e, false));
   const long long first = e->host_counter++;
   return read_stats(e, first, 1, out);
@@ -978,12 +1173,12 @@ int e3_time_cycles(Engine3* e, int ncycles, int64_t flush_bytes, float* ms, std:
     for (int k = 0; k < ncycles; ++k) {
       CK3(cudaMemsetAsync(e->flush_buf, k & 0xff, (size_t)flush_bytes, e->s));
       CK3(cudaEventRecord(ev[2 * k], e->s));
-      CK3(cudaGraphLaunch(e->gexec, e->s));
+      TRY3(launch_cycle(e));
       CK3(cudaEventRecord(ev[2 * k + 1], e->s));
     }
   } else {
     CK3(cudaEventRecord(ev[0], e->s));
-    for (int k = 0; k < ncycles; ++k) CK3(cudaGraphLaunch(e->gexec, e->s));
+    for (int k = 0; k < ncycles; ++k) TRY3(launch_cycle(e));
     CK3(cudaEventRecord(ev[1], e->s));
   }
   CK3(cudaStreamSynchronize(e->s));
@@ -1006,7 +1201,9 @@ int e3_profile_cycles(Engine3* e, int ncycles, int cap, const char** names, floa
   e->profiling = true;
   int rc = TMG_OK;
   for (int k = 0; k < ncycles && rc == TMG_OK; ++k) {
+    const bool applied = e->fpend;
     rc = enqueue_cycle(e);
+    if (e->ffp) ffp_advance(e, applied);
     e->host_counter++;
   }
   e->profiling = false;
@@ -1047,3 +1244,5 @@ int e3_launches_per_cycle(Engine3* e, int32_t* n, std::string& err) {
   *n = e->launches;
   return TMG_OK;
 }
+
+int e3_uses_ffp(Engine3* e) { return e->ffp ? 1 : 0; }

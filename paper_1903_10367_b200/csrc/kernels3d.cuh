@@ -62,6 +62,8 @@ struct Down3 {
   const double* sm_f;    // A1(rdof_{l+1}) * s (adaFACx)
   const double* P;       // 125 planes over this level's vertex grid (boxmg) or nullptr (d-linear)
   double w, omega, wt, ds, hw;
+  const double* bR;      // precomputed R rho_{l+1} / R sm_{l+1} (fused fine pass) or nullptr
+  const double* bT;
   double* rho;           // this level's rho (l > l0) or nullptr
   double* g;             // d - dtil
   double* part_sum;
@@ -102,6 +104,42 @@ struct Chain3 {
   Down3 down[kMaxChain];
   Smooth3 smooth[kMaxChain];
   Up3 up[kMaxChain];
+};
+
+}  // namespace t3
+
+namespace t3 {
+
+// Fused fine pass (kernels3d_ffp.cu): completes the previous cycle's update of
+// the finest level and runs this cycle's finest-level down sweep and its
+// restriction to level ltop-1 in one 2.5D sweep.
+constexpr int kFT = 8;                 // coarse tile (J, K) per CTA
+constexpr int kFU = 3 * kFT + 6;       // u_new window (fine offset -4)
+constexpr int kFR = 3 * kFT + 4;       // rho window (offset -3)
+constexpr int kFS = 3 * kFT + 2;       // sm / restriction window (offset -2)
+constexpr int kFC = 3 * kFT + 5;       // cell window (offset -4)
+constexpr int kFThreads = 256;
+
+struct Ffp3 {
+  int N, Nc, tiles, chunk;  // tiles per axis, coarse planes per i-chunk
+  int apply;                // 1: u_new = u + (P carry_c + g_in); 0: u_new = u
+  int variant, jac;
+  const double* u_in;
+  double* u_out;
+  const double* g_in;
+  double* g_out;
+  const double* carry_c;
+  const double* P;
+  Op3 op;
+  const double* rhs;
+  double w, hw, scale;
+  double* bR;   // R rho_top at interior coarse vertices
+  double* bT;   // R sm_top
+  int l, l0;
+  double* ul[kMaxLevels];
+  int Nl[kMaxLevels];
+  double* part_sum;
+  double* part_max;
 };
 
 }  // namespace t3

@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kSB, 3) k3_smooth_s(const __grid_constant__ Sm
 // Coarse-level down sweep with the restriction of rho and (adaFACx) sm of the
 // finer level in one pass over the P planes.  Thread per interior vertex,
 // k fastest (P planes and coarse vectors coalesced).
-template <bool BOXMG, bool JAC>
+template <bool BOXMG, bool JAC, bool PRE = false>
 __global__ void __launch_bounds__(128) k3_down_c(const __grid_constant__ Down3 a) {
   const int N = a.N, n = N - 2;
   const size_t cnt = (size_t)(a.ihi - a.ilo) * n * n;
@@ -277,7 +277,10 @@ __global__ void __launch_bounds__(128) k3_down_c(const __grid_constant__ Down3 a
     op_apply<LdNC>(a.op, a.u, N, i, j, k, au, dg);
     const bool cpt0 = a.variant == VAR_AFACC;
     double bR, bT = 0.0;
-    if (BOXMG) {
+    if (PRE) {  // restrictions already formed by the fused fine pass
+      bR = __ldg(a.bR + v);
+      if (JAC) bT = __ldg(a.bT + v);
+    } else if (BOXMG) {
       const int Nf = a.Nf;
       const size_t nvc = (size_t)N * N * N;
       const size_t fc = vid(Nf, 3 * i, 3 * j, 3 * k);
