@@ -167,6 +167,101 @@ __device__ __forceinline__ void stream25(const Column& col, const double* x, con
   cp_wait<0>();
 }
 
+// Variant of stream25 that keeps no register window: the body reads its 27
+// neighbours straight from the shared-memory ring (three live planes), which
+// frees ~60 registers per thread for occupancy.  Same stage depth.
+template <bool CELLS, class Body>
+__device__ __forceinline__ void stream25s(const Column& col, const double* x, const double* e,
+                                          double (*us)[kColU * kRowU], double (*cs)[kColC * kRowC],
+                                          Body&& body) {
+  const int ia = col.ia, ib = col.ib;
+  auto issue = [&](int g, int slot) {
+    col.stage_v(us[slot], x, ia - 1 + g);
+    if (CELLS) col.stage_c(cs[slot], e, ia - 1 + g);
+    cp_commit();
+  };
+#pragma unroll
+  for (int g = 0; g < kStages - 1; ++g) issue(g, g);
+  for (int i0 = ia; i0 < ib; i0 += kStages) {
+#pragma unroll
+    for (int u = 0; u < kStages; ++u) {
+      const int i = i0 + u;
+      if (i < ib) {
+        cp_wait<kStages - 4>();
+        __syncthreads();
+        issue(kStages - 1 + (i - ia), (u + kStages - 1) % kStages);  // slot of plane i-2
+        body(i, us[u % kStages], us[(u + 1) % kStages], us[(u + 2) % kStages],
+             CELLS ? cs[u % kStages] : nullptr, CELLS ? cs[(u + 1) % kStages] : nullptr);
+      }
+    }
+  }
+  cp_wait<0>();
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kSB, 4) k3_top_s(const __grid_constant__ Top3 a) {
+  __shared__ double us[kStages][kColU * kRowU];
+  __shared__ double cs[KIND == OP_ELEMENT ? kStages : 1][kColC * kRowC];
+  const Column col(a.N, a.ilo, a.ihi, a.chunk);
+  const int N = a.N;
+  const size_t NN = (size_t)N * N;
+  const int k = col.k0 + threadIdx.x, j = col.j0 + threadIdx.y;
+  const bool own = k <= N - 2 && j <= N - 2;
+  const size_t col_off = (size_t)j * N + k;
+  const int xo = (threadIdx.y + 1) * kRowU + threadIdx.x + 1;
+  const int co = (threadIdx.y + 1) * kRowC + threadIdx.x + 1;
+  double s = 0.0, mx = 0.0;
+  stream25s<KIND == OP_ELEMENT>(col, a.u, a.op.e, us, cs,
+      [&](int i, const double* pm, const double* p0, const double* pp, const double* cm,
+          const double* c0) {
+        if (!own) return;
+        const size_t v = (size_t)i * NN + col_off;
+        const double rhs = a.rhs ? __ldg(a.rhs + v) : 0.0;
+        double x[27];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+          const int o = xo + (t / 3 - 1) * kRowU + (t % 3 - 1);
+          x[t] = pm[o];
+          x[9 + t] = p0[o];
+          x[18 + t] = pp[o];
+        }
+        double au, dg;
+        if (KIND == OP_CONST) {
+          au = const_from(x, a.op.m, a.op.se, a.op.sc);
+          dg = a.op.cdiag;
+        } else {
+          double ec[8], E, T;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {  // cell (i-c0, j-c1, k-c2)
+            const int c0b = c & 1, c1 = (c >> 1) & 1, c2 = c >> 2;
+            ec[c] = (c0b ? cm : c0)[co - c1 * kRowC - c2];
+          }
+          element_ET(x, ec, E, T);
+          dg = K_D * E;
+          au = (dg * x[13]) - (K_E * T);
+        }
+        const double rho = rhs - au;
+        const double t = a.hw * rho;
+        s = s + t * t;
+        mx = fmax(mx, fabs(rho));
+        a.g[v] = (a.w * rho) / dg;
+        if (a.rho) a.rho[v] = rho;
+      });
+  __shared__ double rs[kSB / 32], rm[kSB / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_down_sync(0xffffffffu, s, o);
+    mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+  }
+  if ((col.lt & 31) == 0) { rs[col.lt >> 5] = s; rm[col.lt >> 5] = mx; }
+  __syncthreads();
+  if (col.lt == 0) {
+    double A = 0.0, B = 0.0;
+    for (int q = 0; q < kSB / 32; ++q) { A += rs[q]; B = fmax(B, rm[q]); }
+    a.part_sum[blockIdx.x] = A;
+    a.part_max[blockIdx.x] = B;
+  }
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(kSB, 2) k3_top(const __grid_constant__ Top3 a) {
   __shared__ double us[kStages][kColU * kRowU];
@@ -234,6 +329,32 @@ struct SmoothS {
   double* sm;
   double scale;
 };
+
+__global__ void __launch_bounds__(kSB, 5) k3_smooth_ss(const __grid_constant__ SmoothS a) {
+  __shared__ double xs[kStages][kColU * kRowU];
+  const Column col(a.N, a.ilo, a.ihi, a.chunk);
+  const int N = a.N;
+  const size_t NN = (size_t)N * N;
+  const int k = col.k0 + threadIdx.x, j = col.j0 + threadIdx.y;
+  const bool own = k <= N - 2 && j <= N - 2;
+  const size_t col_off = (size_t)j * N + k;
+  const int xo = (threadIdx.y + 1) * kRowU + threadIdx.x + 1;
+  stream25s<false>(col, a.x, nullptr, xs, nullptr,
+      [&](int i, const double* pm, const double* p0, const double* pp, const double*, const double*) {
+        if (!own) return;
+        double x[27];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+          const int o = xo + (t / 3 - 1) * kRowU + (t % 3 - 1);
+          x[t] = pm[o];
+          x[9 + t] = p0[o];
+          x[18 + t] = pp[o];
+        }
+        double v = const_from(x, C_D8, C_E6, C_C12);
+        v = v * a.scale;
+        a.sm[(size_t)i * NN + col_off] = v;
+      });
+}
 
 __global__ void __launch_bounds__(kSB, 3) k3_smooth_s(const __grid_constant__ SmoothS a) {
   __shared__ double xs[kStages][kColU * kRowU];
