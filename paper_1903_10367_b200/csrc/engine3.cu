@@ -28,6 +28,7 @@ struct Lvl3 {
   double w = 0.0;
   int grid = 0, part_off = 0;
   int s_chunk = 0, s_blocks = 0;  // 2.5D tiling (k3_top / k3_smooth_s)
+  int s2_chunk = 0, s2_blocks = 0;  // two-row 2.5D tiling (k3_top2 / k3_smooth2)
   int c_grid = 0;                 // k3_down_c grid
   int u_grid = 0;                 // k3_up_cell grid (this level as the coarse one)
 };
@@ -306,13 +307,17 @@ SmoothS make_smooth_s(Engine3* e, int l) {
 
 // 2.5D kernels reading their neighbourhoods from shared memory (k3_top_s,
 // k3_smooth_ss) instead of register windows; TMG_TOPV=r selects the latter.
-const bool kTopSmem = [] {
+// variants of the 2.5D kernels: 's' shared-memory window (1 row / thread),
+// 'r' register window, '2' two rows per thread (shared-memory window), 'R' two
+// rows per thread with a register window along i.  Defaults are the measured
+// fastest at config 5 (k3_top2 4.4 ms, k3_smooth2r 1.6 ms at L6).
+const char kTopV = [] {
   const char* v = std::getenv("TMG_TOPV");
-  return !(v && v[0] == 'r');
+  return v ? v[0] : '2';
 }();
-const bool kSmoothSmem = [] {
+const char kSmoothV = [] {
   const char* v = std::getenv("TMG_SMOOTHV");
-  return v && v[0] == 's';
+  return v ? v[0] : 'R';  // measured at config 5 L6: R 1.59 ms, 2 2.39, r 2.3, s 2.85
 }();
 
 int enqueue_down(Engine3* e, bool write) {
@@ -323,7 +328,33 @@ int enqueue_down(Engine3* e, bool write) {
     Lvl3& c = e->L[l];
     if (l == e->ltop) {
       Top3 a = make_top(e, l);
-      if (kTopSmem) {
+      if (kTopV == 'R') {
+        a.chunk = c.s2_chunk;
+        const dim3 b2(kSX, k2Y / 2);
+        const size_t sm = k2RSmemV + k2RSmemC;
+        cudaEvent_t e0_ = nullptr;
+        TRY3(begin_k(e, &e0_));
+        if (c.op.kind == OP_CONST) k3_top2r<OP_CONST><<<c.s2_blocks, b2, sm, e->s>>>(a);
+        else k3_top2r<OP_ELEMENT><<<c.s2_blocks, b2, sm, e->s>>>(a);
+        CKL3();
+        TRY3(end_k(e, kname("k3_down", l), e0_));
+      } else if (kTopV == '2') {
+        a.chunk = c.s2_chunk;
+        const dim3 b2(kSX, k2Y / 2);
+        if (c.op.kind == OP_CONST) {
+          cudaEvent_t e0_ = nullptr;
+          TRY3(begin_k(e, &e0_));
+          k3_top2<OP_CONST><<<c.s2_blocks, b2, k2TopSmem, e->s>>>(a);
+          CKL3();
+          TRY3(end_k(e, kname("k3_down", l), e0_));
+        } else {
+          cudaEvent_t e0_ = nullptr;
+          TRY3(begin_k(e, &e0_));
+          k3_top2<OP_ELEMENT><<<c.s2_blocks, b2, k2TopSmem, e->s>>>(a);
+          CKL3();
+          TRY3(end_k(e, kname("k3_down", l), e0_));
+        }
+      } else if (kTopV == 's') {
         if (c.op.kind == OP_CONST) LAUNCH3(kname("k3_down", l), k3_top_s<OP_CONST>, c.s_blocks, sblk, a);
         else LAUNCH3(kname("k3_down", l), k3_top_s<OP_ELEMENT>, c.s_blocks, sblk, a);
       } else {
@@ -340,8 +371,25 @@ int enqueue_down(Engine3* e, bool write) {
     if (jac && write && l > e->lmin) {
       SmoothS sa = make_smooth_s(e, l);
       // the smoothing kernel is faster with the register window (measured: 2.18 vs 2.85 ms at L6)
-      if (kSmoothSmem) LAUNCH3(kname("k3_smooth", l), k3_smooth_ss, c.s_blocks, sblk, sa);
-      else LAUNCH3(kname("k3_smooth", l), k3_smooth_s, c.s_blocks, sblk, sa);
+      if (kSmoothV == 'R') {
+        sa.chunk = c.s2_chunk;
+        cudaEvent_t e0_ = nullptr;
+        TRY3(begin_k(e, &e0_));
+        k3_smooth2r<<<c.s2_blocks, dim3(kSX, k2Y / 2), k2RSmemV, e->s>>>(sa);
+        CKL3();
+        TRY3(end_k(e, kname("k3_smooth", l), e0_));
+      } else if (kSmoothV == '2') {
+        sa.chunk = c.s2_chunk;
+        cudaEvent_t e0_ = nullptr;
+        TRY3(begin_k(e, &e0_));
+        k3_smooth2<<<c.s2_blocks, dim3(kSX, k2Y / 2), k2SmoothSmem, e->s>>>(sa);
+        CKL3();
+        TRY3(end_k(e, kname("k3_smooth", l), e0_));
+      } else if (kSmoothV == 's') {
+        LAUNCH3(kname("k3_smooth", l), k3_smooth_ss, c.s_blocks, sblk, sa);
+      } else {
+        LAUNCH3(kname("k3_smooth", l), k3_smooth_s, c.s_blocks, sblk, sa);
+      }
     }
   }
   Chain3 ch{};
@@ -602,6 +650,14 @@ int build(Engine3* e, const tmg_tree3* t) {
     Lvl3& c = e->L[l];
     c.w = (cfg.variant == VAR_EXP) ? std::pow(cfg.omega_hat, (double)(l1 - l)) : cfg.omega;
   }
+  CK3(cudaFuncSetAttribute(k3_top2<OP_CONST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2TopSmem));
+  CK3(cudaFuncSetAttribute(k3_top2<OP_ELEMENT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2TopSmem));
+  CK3(cudaFuncSetAttribute(k3_smooth2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2SmoothSmem));
+  CK3(cudaFuncSetAttribute(k3_smooth2r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2RSmemV));
+  CK3(cudaFuncSetAttribute(k3_top2r<OP_CONST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(k2RSmemV + k2RSmemC)));
+  CK3(cudaFuncSetAttribute(k3_top2r<OP_ELEMENT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(k2RSmemV + k2RSmemC)));
   int* deg;
   TRY3(alloc3(e, &deg, 1));
   if (cfg.flavor == TMG_GEOMETRIC) {
@@ -688,6 +744,13 @@ int build(Engine3* e, const tmg_tree3* t) {
       c.s_chunk = (c.N - 2 + nch - 1) / nch;
       const int chunks = (c.N - 2 + c.s_chunk - 1) / c.s_chunk;
       c.s_blocks = tiles * chunks;
+      {
+        const int t2 = ((c.N - 2 + kSX - 1) / kSX) * ((c.N - 2 + k2Y - 1) / k2Y);
+        int n2 = (148 * 12 + t2 - 1) / t2;
+        n2 = std::max(1, std::min(n2, std::max(1, (c.N - 2) / 4)));
+        c.s2_chunk = (c.N - 2 + n2 - 1) / n2;
+        c.s2_blocks = t2 * ((c.N - 2 + c.s2_chunk - 1) / c.s2_chunk);
+      }
       const size_t ni = (size_t)(c.N - 2) * (c.N - 2) * (c.N - 2);
       const size_t ncell = (size_t)(c.N - 1) * (c.N - 1) * (c.N - 1);
       c.c_grid = (int)std::max<size_t>(1, std::min<size_t>((ni + 127) / 128, 148 * 32));
@@ -695,7 +758,7 @@ int build(Engine3* e, const tmg_tree3* t) {
     }
     if (l == l1 && l > e->lc) {
       c.part_off = 0;
-      parts = c.s_blocks;
+      parts = std::max(c.s_blocks, c.s2_blocks);
     }
   }
   // fused fine pass: BoxMG, every variant but adafac-pi, a grid level below the top

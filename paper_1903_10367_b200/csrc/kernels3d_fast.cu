@@ -34,6 +34,14 @@ struct Top3 {
   double* part_max;
 };
 
+struct SmoothS {
+  int N, ilo, ihi, chunk;
+  const double* x;
+  double* sm;
+  double scale;
+};
+
+
 // 2.5D streaming.  A CTA owns a kSX x kSY column of (k, j) and marches the
 // planes i in [ia, ib).  Halo planes of u (and of the cell coefficients) are
 // staged into a kStages-deep shared-memory ring with cp.async (8-byte
@@ -262,6 +270,389 @@ __global__ void __launch_bounds__(kSB, 4) k3_top_s(const __grid_constant__ Top3 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Two rows per thread: CTA = 32 (k) x 16 (j) column, 256 threads, thread
+// (tx, ty) owns rows j0 + 2 ty and j0 + 2 ty + 1.  The 4 x 3 neighbourhood
+// of the two rows is read once per plane (18 shared loads per vertex instead
+// of 27) and every per-plane overhead (staging, barrier, loop) is shared by
+// two vertices.
+constexpr int k2Y = 16;
+constexpr int k2Stages = 5;  // 5 x (612 + 561) doubles fit the 48 KB static limit
+constexpr int k2RowU = kSX + 2, k2ColU = k2Y + 2;
+constexpr int k2RowC = kSX + 1, k2ColC = k2Y + 1;
+
+struct Column2 {
+  static constexpr int kPU = (k2ColU * k2RowU + kSB - 1) / kSB;
+  static constexpr int kPC = (k2ColC * k2RowC + kSB - 1) / kSB;
+  int N, k0, j0, ia, ib, lt;
+  long long ou[kPU], oc[kPC];
+  __device__ Column2(int N_, int ilo, int ihi, int chunk) : N(N_) {
+    const int tilesx = (N - 2 + kSX - 1) / kSX, tilesy = (N - 2 + k2Y - 1) / k2Y;
+    int b = blockIdx.x;
+    const int tx = b % tilesx;
+    b /= tilesx;
+    const int ty = b % tilesy;
+    const int tz = b / tilesy;
+    k0 = 1 + tx * kSX;
+    j0 = 1 + ty * k2Y;
+    ia = ilo + tz * chunk;
+    ib = min(ihi, ia + chunk);
+    lt = threadIdx.y * kSX + threadIdx.x;
+    const int n = N - 1;
+#pragma unroll
+    for (int p = 0; p < kPU; ++p) {
+      const int q = lt + p * kSB;
+      const int jj = q / k2RowU, kk = q - jj * k2RowU;
+      const int j = j0 - 1 + jj, k = k0 - 1 + kk;
+      ou[p] = (q < k2ColU * k2RowU) ? ((j < N && k < N) ? (long long)j * N + k : -1) : -2;
+    }
+#pragma unroll
+    for (int p = 0; p < kPC; ++p) {
+      const int q = lt + p * kSB;
+      const int jj = q / k2RowC, kk = q - jj * k2RowC;
+      const int cj = j0 - 1 + jj, ck = k0 - 1 + kk;
+      oc[p] = (q < k2ColC * k2RowC) ? ((cj < n && ck < n) ? (long long)cj * n + ck : -1) : -2;
+    }
+  }
+  __device__ __forceinline__ void stage_v(double* buf, const double* x, int p) const {
+    const bool okp = p >= 0 && p < N;
+    const double* base = x + (size_t)(okp ? p : 0) * N * N;
+#pragma unroll
+    for (int q = 0; q < kPU; ++q) {
+      if (ou[q] == -2) continue;
+      const bool ok = okp && ou[q] >= 0;
+      cp_async8(buf + lt + q * kSB, ok ? base + ou[q] : x, ok);
+    }
+  }
+  __device__ __forceinline__ void stage_c(double* buf, const double* e, int c) const {
+    const int n = N - 1;
+    const bool okp = c >= 0 && c < n;
+    const double* base = e + (size_t)(okp ? c : 0) * n * n;
+#pragma unroll
+    for (int q = 0; q < kPC; ++q) {
+      if (oc[q] == -2) continue;
+      const bool ok = okp && oc[q] >= 0;
+      cp_async8(buf + lt + q * kSB, ok ? base + oc[q] : e, ok);
+    }
+  }
+};
+
+template <int S, bool CELLS, class Body>
+__device__ __forceinline__ void stream25x2(const Column2& col, const double* x, const double* e,
+                                           double (*us)[k2ColU * k2RowU], double (*cs)[k2ColC * k2RowC],
+                                           Body&& body) {
+  const int ia = col.ia, ib = col.ib;
+  auto issue = [&](int g, int slot) {
+    col.stage_v(us[slot], x, ia - 1 + g);
+    if (CELLS) col.stage_c(cs[slot], e, ia - 1 + g);
+    cp_commit();
+  };
+#pragma unroll
+  for (int g = 0; g < S - 1; ++g) issue(g, g);
+  for (int i0 = ia; i0 < ib; i0 += S) {
+#pragma unroll
+    for (int u = 0; u < S; ++u) {
+      const int i = i0 + u;
+      if (i < ib) {
+        cp_wait<S - 4>();
+        __syncthreads();
+        issue(S - 1 + (i - ia), (u + S - 1) % S);
+        body(i, us[u % S], us[(u + 1) % S], us[(u + 2) % S],
+             CELLS ? cs[u % S] : nullptr, CELLS ? cs[(u + 1) % S] : nullptr);
+      }
+    }
+  }
+  cp_wait<0>();
+}
+
+// 4 x 3 x 3 neighbourhood (rows j-1 .. j+2) of the thread's two vertices
+__device__ __forceinline__ void load_two(const double* pm, const double* p0, const double* pp, int xo,
+                                         double x0[27], double x1[27]) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int o = xo + (r - 1) * k2RowU + (c - 1);
+      const double a = pm[o], b = p0[o], d = pp[o];
+      if (r <= 2) { x0[r * 3 + c] = a; x0[9 + r * 3 + c] = b; x0[18 + r * 3 + c] = d; }
+      if (r >= 1) { x1[(r - 1) * 3 + c] = a; x1[9 + (r - 1) * 3 + c] = b; x1[18 + (r - 1) * 3 + c] = d; }
+    }
+}
+
+constexpr int k2TopStages = 5, k2SmoothStages = 10;  // measured: top 5 > 8 stages (occupancy)
+constexpr size_t k2TopSmem = sizeof(double) * k2TopStages * (k2ColU * k2RowU + k2ColC * k2RowC);
+constexpr size_t k2SmoothSmem = sizeof(double) * k2SmoothStages * k2ColU * k2RowU;
+
+// Two rows per thread with a register window along i: each plane's 4 x 3
+// neighbourhood of the thread's two vertices is read from shared memory once
+// (6 loads per vertex instead of 18) and kept in registers for the three
+// output planes it feeds.  Unrolled by S (a multiple of 3): ring slots and
+// register rotation are compile-time constants.
+template <int S, bool CELLS, class Body>
+__device__ __forceinline__ void stream25x2r(const Column2& col, const double* x, const double* e,
+                                            double (*us)[k2ColU * k2RowU],
+                                            double (*cs)[k2ColC * k2RowC], int xo, int co,
+                                            Body&& body) {
+  static_assert(S % 3 == 0, "register rotation needs S % 3 == 0");
+  const int ia = col.ia, ib = col.ib;
+  auto issue = [&](int g, int slot) {
+    col.stage_v(us[slot], x, ia - 1 + g);
+    if (CELLS) col.stage_c(cs[slot], e, ia - 1 + g);
+    cp_commit();
+  };
+  auto ld12 = [&](const double* p, double w[12]) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) w[r * 3 + c] = p[xo + (r - 1) * k2RowU + (c - 1)];
+  };
+  auto ld6 = [&](const double* p, double w[6]) {  // cells rows j-1..j+1, cols k-1..k
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) w[r * 2 + c] = p[co + (r - 1) * k2RowC - c];
+  };
+#pragma unroll
+  for (int g = 0; g < S; ++g) issue(g, g);
+  double X[3][12], E[3][6];
+  cp_wait<S - 2>();
+  __syncthreads();
+  ld12(us[0], X[0]);
+  ld12(us[1], X[1]);
+  if (CELLS) ld6(cs[0], E[0]);
+  for (int i0 = ia; i0 < ib; i0 += S) {
+#pragma unroll
+    for (int u = 0; u < S; ++u) {
+      const int i = i0 + u;
+      if (i < ib) {
+        cp_wait<S - 3>();
+        __syncthreads();
+        ld12(us[(u + 2) % S], X[(u + 2) % 3]);
+        if (CELLS) ld6(cs[(u + 1) % S], E[(u + 1) % 3]);
+        issue(S + (i - ia), u);  // the slot of plane i-1, read two steps ago
+        body(i, X[u % 3], X[(u + 1) % 3], X[(u + 2) % 3], E[u % 3], E[(u + 1) % 3]);
+      }
+    }
+  }
+  cp_wait<0>();
+}
+
+// x27 of the lower (h = 0) or upper (h = 1) vertex from three 4x3 planes
+__device__ __forceinline__ void pick27(const double* wm, const double* w0, const double* wp, int h,
+                                       double x[27]) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      x[r * 3 + c] = wm[(r + h) * 3 + c];
+      x[9 + r * 3 + c] = w0[(r + h) * 3 + c];
+      x[18 + r * 3 + c] = wp[(r + h) * 3 + c];
+    }
+}
+
+constexpr int k2RStages = 6;
+constexpr size_t k2RSmemV = sizeof(double) * k2RStages * k2ColU * k2RowU;
+constexpr size_t k2RSmemC = sizeof(double) * k2RStages * k2ColC * k2RowC;
+
+__global__ void __launch_bounds__(kSB, 2) k3_smooth2r(const __grid_constant__ SmoothS a) {
+  extern __shared__ double dyn2[];  // k2RSmemV
+  auto xs = reinterpret_cast<double(*)[k2ColU * k2RowU]>(dyn2);
+  const Column2 col(a.N, a.ilo, a.ihi, a.chunk);
+  const int N = a.N;
+  const size_t NN = (size_t)N * N;
+  const int k = col.k0 + threadIdx.x, j = col.j0 + 2 * threadIdx.y;
+  const bool ok0 = k <= N - 2 && j <= N - 2, ok1 = k <= N - 2 && j + 1 <= N - 2;
+  const size_t col_off = (size_t)j * N + k;
+  const int xo = (2 * threadIdx.y + 1) * k2RowU + threadIdx.x + 1;
+  stream25x2r<k2RStages, false>(col, a.x, nullptr, xs, nullptr, xo, 0,
+      [&](int i, const double* wm, const double* w0, const double* wp, const double*, const double*) {
+        if (!ok0) return;
+        const size_t v = (size_t)i * NN + col_off;
+        double x[27];
+        pick27(wm, w0, wp, 0, x);
+        double v0 = const_from(x, C_D8, C_E6, C_C12);
+        a.sm[v] = v0 * a.scale;
+        if (ok1) {
+          pick27(wm, w0, wp, 1, x);
+          double v1 = const_from(x, C_D8, C_E6, C_C12);
+          a.sm[v + N] = v1 * a.scale;
+        }
+      });
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kSB, 2) k3_top2r(const __grid_constant__ Top3 a) {
+  extern __shared__ double dyn2[];  // k2RSmemV + k2RSmemC
+  auto us = reinterpret_cast<double(*)[k2ColU * k2RowU]>(dyn2);
+  auto cs = reinterpret_cast<double(*)[k2ColC * k2RowC]>(dyn2 + k2RStages * k2ColU * k2RowU);
+  const Column2 col(a.N, a.ilo, a.ihi, a.chunk);
+  const int N = a.N;
+  const size_t NN = (size_t)N * N;
+  const int k = col.k0 + threadIdx.x, j = col.j0 + 2 * threadIdx.y;
+  const bool ok0 = k <= N - 2 && j <= N - 2, ok1 = k <= N - 2 && j + 1 <= N - 2;
+  const size_t col_off = (size_t)j * N + k;
+  const int xo = (2 * threadIdx.y + 1) * k2RowU + threadIdx.x + 1;
+  const int co = (2 * threadIdx.y + 1) * k2RowC + threadIdx.x + 1;
+  double s = 0.0, mx = 0.0;
+  stream25x2r<k2RStages, KIND == OP_ELEMENT>(col, a.u, a.op.e, us, cs, xo, co,
+      [&](int i, const double* wm, const double* w0, const double* wp, const double* em,
+          const double* e0) {
+        if (!ok0) return;
+        const size_t v = (size_t)i * NN + col_off;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1 && !ok1) break;
+          const size_t vh = v + (size_t)h * N;
+          const double rhs = a.rhs ? __ldg(a.rhs + vh) : 0.0;
+          double x[27];
+          pick27(wm, w0, wp, h, x);
+          double au, dg;
+          if (KIND == OP_CONST) {
+            au = const_from(x, a.op.m, a.op.se, a.op.sc);
+            dg = a.op.cdiag;
+          } else {
+            double ec[8], E, T;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {  // cell (i-c0, j+h-c1, k-c2): rows j-1..j+1 -> index h+1-c1
+              const int c0b = c & 1, c1 = (c >> 1) & 1, c2 = c >> 2;
+              ec[c] = (c0b ? em : e0)[(h + 1 - c1) * 2 + c2];
+            }
+            element_ET(x, ec, E, T);
+            dg = K_D * E;
+            au = (dg * x[13]) - (K_E * T);
+          }
+          const double rho = rhs - au;
+          const double t = a.hw * rho;
+          s = s + t * t;
+          mx = fmax(mx, fabs(rho));
+          a.g[vh] = (a.w * rho) / dg;
+          if (a.rho) a.rho[vh] = rho;
+        }
+      });
+  __shared__ double rs[kSB / 32], rm[kSB / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_down_sync(0xffffffffu, s, o);
+    mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+  }
+  if ((col.lt & 31) == 0) { rs[col.lt >> 5] = s; rm[col.lt >> 5] = mx; }
+  __syncthreads();
+  if (col.lt == 0) {
+    double A = 0.0, B = 0.0;
+    for (int q = 0; q < kSB / 32; ++q) { A += rs[q]; B = fmax(B, rm[q]); }
+    a.part_sum[blockIdx.x] = A;
+    a.part_max[blockIdx.x] = B;
+  }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kSB, 3) k3_top2(const __grid_constant__ Top3 a) {
+  extern __shared__ double dyn2[];  // k2TopSmem
+  auto us = reinterpret_cast<double(*)[k2ColU * k2RowU]>(dyn2);
+  auto cs = reinterpret_cast<double(*)[k2ColC * k2RowC]>(dyn2 + k2TopStages * k2ColU * k2RowU);
+  const Column2 col(a.N, a.ilo, a.ihi, a.chunk);
+  const int N = a.N;
+  const size_t NN = (size_t)N * N;
+  const int k = col.k0 + threadIdx.x, j = col.j0 + 2 * threadIdx.y;
+  const bool ok0 = k <= N - 2 && j <= N - 2, ok1 = k <= N - 2 && j + 1 <= N - 2;
+  const size_t col_off = (size_t)j * N + k;
+  const int xo = (2 * threadIdx.y + 1) * k2RowU + threadIdx.x + 1;
+  const int co = (2 * threadIdx.y + 1) * k2RowC + threadIdx.x + 1;
+  double s = 0.0, mx = 0.0;
+  stream25x2<k2TopStages, KIND == OP_ELEMENT>(col, a.u, a.op.e, us, cs,
+      [&](int i, const double* pm, const double* p0, const double* pp, const double* cm,
+          const double* c0) {
+        if (!ok0) return;
+        const size_t v = (size_t)i * NN + col_off;
+        const double rhs0 = a.rhs ? __ldg(a.rhs + v) : 0.0;
+        const double rhs1 = (ok1 && a.rhs) ? __ldg(a.rhs + v + N) : 0.0;
+        double x0[27], x1[27];
+        load_two(pm, p0, pp, xo, x0, x1);
+        double au0, dg0, au1 = 0.0, dg1 = 1.0;
+        if (KIND == OP_CONST) {
+          au0 = const_from(x0, a.op.m, a.op.se, a.op.sc);
+          au1 = const_from(x1, a.op.m, a.op.se, a.op.sc);
+          dg0 = dg1 = a.op.cdiag;
+        } else {
+          // cells (i-c0, j-c1 (+1), k-c2): rows j-1, j, j+1 of cell planes i-1 and i
+          double cr[2][3][2];
+#pragma unroll
+          for (int c0b = 0; c0b < 2; ++c0b)
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+              for (int c2 = 0; c2 < 2; ++c2)
+                cr[c0b][r][c2] = (c0b ? cm : c0)[co + (r - 1) * k2RowC - c2];
+          double e0[8], e1[8], E, T;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int c0b = c & 1, c1 = (c >> 1) & 1, c2 = c >> 2;
+            e0[c] = cr[c0b][1 - c1][c2];
+            e1[c] = cr[c0b][2 - c1][c2];
+          }
+          element_ET(x0, e0, E, T);
+          dg0 = K_D * E;
+          au0 = (dg0 * x0[13]) - (K_E * T);
+          element_ET(x1, e1, E, T);
+          dg1 = K_D * E;
+          au1 = (dg1 * x1[13]) - (K_E * T);
+        }
+        const double rho0 = rhs0 - au0;
+        const double t0 = a.hw * rho0;
+        s = s + t0 * t0;
+        mx = fmax(mx, fabs(rho0));
+        a.g[v] = (a.w * rho0) / dg0;
+        if (a.rho) a.rho[v] = rho0;
+        if (ok1) {
+          const double rho1 = rhs1 - au1;
+          const double t1 = a.hw * rho1;
+          s = s + t1 * t1;
+          mx = fmax(mx, fabs(rho1));
+          a.g[v + N] = (a.w * rho1) / dg1;
+          if (a.rho) a.rho[v + N] = rho1;
+        }
+      });
+  __shared__ double rs[kSB / 32], rm[kSB / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_down_sync(0xffffffffu, s, o);
+    mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+  }
+  if ((col.lt & 31) == 0) { rs[col.lt >> 5] = s; rm[col.lt >> 5] = mx; }
+  __syncthreads();
+  if (col.lt == 0) {
+    double A = 0.0, B = 0.0;
+    for (int q = 0; q < kSB / 32; ++q) { A += rs[q]; B = fmax(B, rm[q]); }
+    a.part_sum[blockIdx.x] = A;
+    a.part_max[blockIdx.x] = B;
+  }
+}
+
+__global__ void __launch_bounds__(kSB, 4) k3_smooth2(const __grid_constant__ SmoothS a) {
+  extern __shared__ double dyn2[];  // k2SmoothSmem
+  auto xs = reinterpret_cast<double(*)[k2ColU * k2RowU]>(dyn2);
+  const Column2 col(a.N, a.ilo, a.ihi, a.chunk);
+  const int N = a.N;
+  const size_t NN = (size_t)N * N;
+  const int k = col.k0 + threadIdx.x, j = col.j0 + 2 * threadIdx.y;
+  const bool ok0 = k <= N - 2 && j <= N - 2, ok1 = k <= N - 2 && j + 1 <= N - 2;
+  const size_t col_off = (size_t)j * N + k;
+  const int xo = (2 * threadIdx.y + 1) * k2RowU + threadIdx.x + 1;
+  stream25x2<k2SmoothStages, false>(col, a.x, nullptr, xs, nullptr,
+      [&](int i, const double* pm, const double* p0, const double* pp, const double*, const double*) {
+        if (!ok0) return;
+        double x0[27], x1[27];
+        load_two(pm, p0, pp, xo, x0, x1);
+        double v0 = const_from(x0, C_D8, C_E6, C_C12);
+        v0 = v0 * a.scale;
+        const size_t v = (size_t)i * NN + col_off;
+        a.sm[v] = v0;
+        if (ok1) {
+          double v1 = const_from(x1, C_D8, C_E6, C_C12);
+          v1 = v1 * a.scale;
+          a.sm[v + N] = v1;
+        }
+      });
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(kSB, 2) k3_top(const __grid_constant__ Top3 a) {
   __shared__ double us[kStages][kColU * kRowU];
@@ -322,13 +713,6 @@ __global__ void __launch_bounds__(kSB, 2) k3_top(const __grid_constant__ Top3 a)
     a.part_max[blockIdx.x] = B;
   }
 }
-
-struct SmoothS {
-  int N, ilo, ihi, chunk;
-  const double* x;
-  double* sm;
-  double scale;
-};
 
 __global__ void __launch_bounds__(kSB, 5) k3_smooth_ss(const __grid_constant__ SmoothS a) {
   __shared__ double xs[kStages][kColU * kRowU];

@@ -177,3 +177,34 @@ def test_degenerate_collapse_raises_arithmetic_error():
     tree.eps[2][:, :] = 0.0  # zero material everywhere on the fine level -> det == 0
     with pytest.raises(ArithmeticError):
         GpuEngine(tree, SolverConfig(variant="adafac-jac", flavor="boxmg"))
+
+
+def test_config4_full_size_against_reference():
+    """BASELINE config 4 at full size (annulus 4 -> 8, eps = 100 disc, adaFACx BoxMG, 3.07 M
+    fine DoFs, 34,992 hanging vertices): the same seeded inputs as the reference run
+    (input SHA), bit-exact vertex classification on every level (SHA + counts) and the
+    reference's residual history up to its divergence exit (bench.py:203-205)."""
+    import hashlib
+    import json
+    case = load("cfg4_4to8")
+    meta = case.meta
+    wl = workloads.config4()
+    tree = wl.tree
+    got_sha = hashlib.sha256(np.ascontiguousarray(np.concatenate(
+        [tree.eps[l].ravel() for l in range(len(tree.u))]
+        + [wl.rhs[l].ravel() for l in sorted(wl.rhs)] + [np.zeros(0)])).tobytes()).hexdigest()
+    assert got_sha == meta["inputs_sha"], "seeded inputs differ from the reference run"
+    eng = GpuEngine(tree, SolverConfig(variant=wl.variant, flavor=wl.flavor), sync="lazy")
+    eng.rhs.update(wl.rhs)
+    for l in range(eng.lmin, eng.ltop + 1):
+        k = eng.kinds(l)
+        assert hashlib.sha256(np.ascontiguousarray(k).tobytes()).hexdigest() == meta[f"kinds_sha_{l}"], l
+        assert np.bincount(k.ravel(), minlength=5).tolist() == meta[f"kinds_count_{l}"], l
+    n = len(case["l2h"])
+    hist = eng.advance_many(n)
+    np.testing.assert_allclose([s.l2h for s in hist], case["l2h"], rtol=1e-9)
+    np.testing.assert_allclose([s.linf for s in hist], case["linf"], rtol=1e-9)
+    assert [s.dofs for s in hist] == case["dofs"].tolist()
+    assert [s.updates for s in hist] == case["updates"].tolist()
+    # the reference stopped with EXIT_DIVERGED: normalized l2h above 1e4
+    assert hist[-1].l2h / hist[0].l2h > 1e4 and meta["status"] == "diverged"
