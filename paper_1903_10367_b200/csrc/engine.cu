@@ -200,13 +200,22 @@ const char* lvl_name(const char* base, int l) {
 
 // 32 x 8 vertex tiles of the grid kernels (k_down, k_up)
 inline unsigned tiles_x(int N) { return (unsigned)((N + tmg::kTileX - 1) / tmg::kTileX); }
-inline unsigned tiles_y(int N) { return (unsigned)((N + tmg::kTileY - 1) / tmg::kTileY); }
+inline unsigned tiles_y(int N, int ty = tmg::kTileY) { return (unsigned)((N + ty - 1) / ty); }
 
-#define LAUNCH_TILES(h, name, kernel, N, ...)                                          \
+// Coarse grid levels run 32 x kCoarseTileY tiles: their per-vertex work is
+// heavy (BoxMG restriction + R~ from P, ~200 registers) and they have few
+// vertices, so small CTAs spread them over more SMs (TMG_CTY overrides).
+const int kCoarseTileY = [] {
+  const char* v = std::getenv("TMG_CTY");
+  const int t = v ? std::atoi(v) : 2;
+  return (t == 1 || t == 2 || t == 4 || t == 8) ? t : 2;
+}();
+
+#define LAUNCH_TILES(h, name, kernel, N, TY, ...)                                      \
   do {                                                                                 \
     cudaEvent_t e0_ = nullptr;                                                         \
     TRY(begin_k(h, name, &e0_));                                                       \
-    kernel<<<dim3(tiles_x(N), tiles_y(N)), dim3(tmg::kTileX, tmg::kTileY), 0, (h)->s>>>( \
+    kernel<<<dim3(tiles_x(N), tiles_y(N, TY)), dim3(tmg::kTileX, (TY)), 0, (h)->s>>>(  \
         __VA_ARGS__);                                                                  \
     CKL();                                                                             \
     TRY(end_k(h, name, e0_));                                                          \
@@ -326,9 +335,9 @@ int enqueue_down(tmg_handle* h, bool write) {
   for (int l = h->ltop; l > h->lc; --l) {
     tmg::DownArgs a = make_down(h, l, write);
     if (l == h->ltop)
-      LAUNCH_TILES(h, lvl_name("k_down", l), tmg::k_down<1>, h->L[l].N, a);
+      LAUNCH_TILES(h, lvl_name("k_down", l), tmg::k_down<1>, h->L[l].N, tmg::kTileY, a);
     else
-      LAUNCH_TILES(h, lvl_name("k_down", l), tmg::k_down<0>, h->L[l].N, a);
+      LAUNCH_TILES(h, lvl_name("k_down", l), tmg::k_down<0>, h->L[l].N, kCoarseTileY, a);
   }
   TRY(launch_coarse(h, write));
   return TMG_OK;
@@ -361,7 +370,8 @@ int enqueue_cycle(tmg_handle* h) {
   TRY(enqueue_down(h, true));  // includes the coarse chain (down, stats, up)
   for (int l = h->lc + 1; l <= h->ltop; ++l) {
     tmg::UpArgs a = make_up(h, l);
-    LAUNCH_TILES(h, lvl_name("k_up", l), tmg::k_up, h->L[l].N, a);
+    LAUNCH_TILES(h, lvl_name("k_up", l), tmg::k_up, h->L[l].N,
+                 l == h->ltop ? tmg::kTileY : kCoarseTileY, a);
   }
   TRY(enqueue_hang(h));  // injection rides in k_up / k_coarse
   return TMG_OK;
@@ -644,7 +654,7 @@ int build(tmg_handle* h, const tmg_tree* t) {
       TRY(dalloc(h, &c.rdof, c.nv));
     }
     if (l < l1) TRY(dalloc(h, &c.carry, c.nv));
-    c.nblocks = (int)(tiles_x(c.N) * tiles_y(c.N));
+    c.nblocks = (int)(tiles_x(c.N) * tiles_y(c.N, l == l1 ? tmg::kTileY : kCoarseTileY));
     if (l > h->lc) {
       c.part_off = parts;
       parts += c.nblocks;

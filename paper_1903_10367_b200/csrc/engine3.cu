@@ -86,6 +86,7 @@ struct Engine3 {
   std::vector<int> own_lo, own_hi;  // by level
   std::vector<int> own_blocks;      // k3_top / k3_smooth_s blocks for the owned range
   std::vector<int> own_chunk;
+  std::vector<int> own_blocks2, own_chunk2;  // two-row kernels (k3_top2 / k3_smooth2r)
   double* red = nullptr;            // {sum, max} of this cycle's stats
   int top_parts = 0;
   // fused fine pass (pipelined schedule): the finest level's u and g are double
@@ -828,9 +829,9 @@ struct ErrScope {
 
 // --- sharded mode ---------------------------------------------------------------
 
-// 2.5D tiling of the interior planes [ilo, ihi) of an N^3 level
-void tiling(int N, int ilo, int ihi, int* chunk, int* blocks) {
-  const int tiles = ((N - 2 + kSX - 1) / kSX) * ((N - 2 + kSY - 1) / kSY);
+// 2.5D tiling of the interior planes [ilo, ihi) of an N^3 level (ty = rows per CTA)
+void tiling(int N, int ilo, int ihi, int* chunk, int* blocks, int ty = kSY) {
+  const int tiles = ((N - 2 + kSX - 1) / kSX) * ((N - 2 + ty - 1) / ty);
   const int np = std::max(1, ihi - ilo);
   int nch = (148 * 16 + tiles - 1) / tiles;
   nch = std::max(1, std::min(nch, std::max(1, np / 4)));
@@ -856,10 +857,16 @@ int phase3(Engine3* e, int phase, int l) {
         Top3 a = make_top(e, l);
         a.ilo = lo;
         a.ihi = hi;
-        a.chunk = e->own_chunk[l];
-        e->top_parts = e->own_blocks[l];
-        if (c.op.kind == OP_CONST) LAUNCH3(kname("k3_down", l), k3_top<OP_CONST>, e->own_blocks[l], sblk, a);
-        else LAUNCH3(kname("k3_down", l), k3_top<OP_ELEMENT>, e->own_blocks[l], sblk, a);
+        a.chunk = e->own_chunk2[l];
+        e->top_parts = e->own_blocks2[l];
+        cudaEvent_t e0_ = nullptr;
+        TRY3(begin_k(e, &e0_));
+        if (c.op.kind == OP_CONST)
+          k3_top2<OP_CONST><<<e->own_blocks2[l], dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
+        else
+          k3_top2<OP_ELEMENT><<<e->own_blocks2[l], dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
+        CKL3();
+        TRY3(end_k(e, kname("k3_down", l), e0_));
       } else {
         Down3 a = make_down(e, l, true);
         a.ilo = lo;
@@ -878,8 +885,12 @@ int phase3(Engine3* e, int phase, int l) {
       SmoothS a = make_smooth_s(e, l);
       a.ilo = lo;
       a.ihi = hi;
-      a.chunk = e->own_chunk[l];
-      LAUNCH3(kname("k3_smooth", l), k3_smooth_s, e->own_blocks[l], sblk, a);
+      a.chunk = e->own_chunk2[l];
+      cudaEvent_t e0_ = nullptr;
+      TRY3(begin_k(e, &e0_));
+      k3_smooth2r<<<e->own_blocks2[l], dim3(kSX, k2Y / 2), k2RSmemV, e->s>>>(a);
+      CKL3();
+      TRY3(end_k(e, kname("k3_smooth", l), e0_));
       return TMG_OK;
     }
     case TMG_PH_REDUCE: {
@@ -973,6 +984,8 @@ int e3_shard(Engine3* e, int ls, const int32_t* lo, const int32_t* hi, std::stri
   e->own_hi.assign(e->ltop + 1, 0);
   e->own_blocks.assign(e->ltop + 1, 0);
   e->own_chunk.assign(e->ltop + 1, 1);
+  e->own_blocks2.assign(e->ltop + 1, 0);
+  e->own_chunk2.assign(e->ltop + 1, 1);
   int maxb = 0;
   for (int l = ls; l <= e->ltop; ++l) {
     if (lo[l] < 0 || hi[l] > e->L[l].N || lo[l] > hi[l]) return fail3(e, TMG_EINVAL, "bad owned plane range");
@@ -980,7 +993,8 @@ int e3_shard(Engine3* e, int ls, const int32_t* lo, const int32_t* hi, std::stri
     e->own_hi[l] = hi[l];
     const int a = std::max(1, lo[l]), b = std::min(e->L[l].N - 1, hi[l]);
     tiling(e->L[l].N, a, std::max(a + 1, b), &e->own_chunk[l], &e->own_blocks[l]);
-    maxb = std::max(maxb, e->own_blocks[l]);
+    tiling(e->L[l].N, a, std::max(a + 1, b), &e->own_chunk2[l], &e->own_blocks2[l], k2Y);
+    maxb = std::max(maxb, std::max(e->own_blocks[l], e->own_blocks2[l]));
   }
   e->ls = ls;
   e->sharded = true;

@@ -780,11 +780,12 @@ __device__ __forceinline__ void block_reduce(double& s, double& m) {
   }
   const int t = threadIdx.y * blockDim.x + threadIdx.x;
   const int w = t >> 5, lane = t & 31;
+  const int nw = (int)(blockDim.x * blockDim.y) >> 5;  // <= BS / 32
   if (lane == 0) { ss[w] = s; sm[w] = m; }
   __syncthreads();
   if (t == 0) {
     double a = 0.0, b = 0.0;
-    for (int k = 0; k < BS / 32; ++k) { a += ss[k]; b = fmax(b, sm[k]); }
+    for (int k = 0; k < nw; ++k) { a += ss[k]; b = fmax(b, sm[k]); }
     s = a;
     m = b;
   }
@@ -796,7 +797,7 @@ __device__ __forceinline__ void block_reduce(double& s, double& m) {
 template <int TOP>
 __global__ void __launch_bounds__(kBlock) k_down(const __grid_constant__ DownArgs a) {
   const int j = blockIdx.x * kTileX + threadIdx.x;
-  const int i = blockIdx.y * kTileY + threadIdx.y;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;  // tile height: 8 (finest) or 2 (coarse)
   double s = 0.0, m = 0.0;
   if (i < a.N && j < a.N) down_vertex<LdNC, TOP>(a, i, j, s, m);
   block_reduce<kBlock>(s, m);
@@ -809,7 +810,7 @@ __global__ void __launch_bounds__(kBlock) k_down(const __grid_constant__ DownArg
 
 __global__ void __launch_bounds__(kBlock) k_up(const __grid_constant__ UpArgs a) {
   const int j = blockIdx.x * kTileX + threadIdx.x;
-  const int i = blockIdx.y * kTileY + threadIdx.y;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
   if (i < a.N && j < a.N) up_vertex<LdNC>(a, i, j);
 }
 
