@@ -306,21 +306,6 @@ SmoothS make_smooth_s(Engine3* e, int l) {
   return a;
 }
 
-// 2.5D kernels reading their neighbourhoods from shared memory (k3_top_s,
-// k3_smooth_ss) instead of register windows; TMG_TOPV=r selects the latter.
-// variants of the 2.5D kernels: 's' shared-memory window (1 row / thread),
-// 'r' register window, '2' two rows per thread (shared-memory window), 'R' two
-// rows per thread with a register window along i.  Defaults are the measured
-// fastest at config 5 (k3_top2 4.4 ms, k3_smooth2r 1.6 ms at L6).
-const char kTopV = [] {
-  const char* v = std::getenv("TMG_TOPV");
-  return v ? v[0] : '2';
-}();
-const char kSmoothV = [] {
-  const char* v = std::getenv("TMG_SMOOTHV");
-  return v ? v[0] : 'R';  // measured at config 5 L6: R 1.59 ms, 2 2.39, r 2.3, s 2.85
-}();
-
 int enqueue_down(Engine3* e, bool write) {
   const bool jac = e->cfg.variant == VAR_JAC;
   const bool boxmg = e->cfg.flavor == TMG_BOXMG;
@@ -329,39 +314,13 @@ int enqueue_down(Engine3* e, bool write) {
     Lvl3& c = e->L[l];
     if (l == e->ltop) {
       Top3 a = make_top(e, l);
-      if (kTopV == 'R') {
-        a.chunk = c.s2_chunk;
-        const dim3 b2(kSX, k2Y / 2);
-        const size_t sm = k2RSmemV + k2RSmemC;
-        cudaEvent_t e0_ = nullptr;
-        TRY3(begin_k(e, &e0_));
-        if (c.op.kind == OP_CONST) k3_top2r<OP_CONST><<<c.s2_blocks, b2, sm, e->s>>>(a);
-        else k3_top2r<OP_ELEMENT><<<c.s2_blocks, b2, sm, e->s>>>(a);
-        CKL3();
-        TRY3(end_k(e, kname("k3_down", l), e0_));
-      } else if (kTopV == '2') {
-        a.chunk = c.s2_chunk;
-        const dim3 b2(kSX, k2Y / 2);
-        if (c.op.kind == OP_CONST) {
-          cudaEvent_t e0_ = nullptr;
-          TRY3(begin_k(e, &e0_));
-          k3_top2<OP_CONST><<<c.s2_blocks, b2, k2TopSmem, e->s>>>(a);
-          CKL3();
-          TRY3(end_k(e, kname("k3_down", l), e0_));
-        } else {
-          cudaEvent_t e0_ = nullptr;
-          TRY3(begin_k(e, &e0_));
-          k3_top2<OP_ELEMENT><<<c.s2_blocks, b2, k2TopSmem, e->s>>>(a);
-          CKL3();
-          TRY3(end_k(e, kname("k3_down", l), e0_));
-        }
-      } else if (kTopV == 's') {
-        if (c.op.kind == OP_CONST) LAUNCH3(kname("k3_down", l), k3_top_s<OP_CONST>, c.s_blocks, sblk, a);
-        else LAUNCH3(kname("k3_down", l), k3_top_s<OP_ELEMENT>, c.s_blocks, sblk, a);
-      } else {
-        if (c.op.kind == OP_CONST) LAUNCH3(kname("k3_down", l), k3_top<OP_CONST>, c.s_blocks, sblk, a);
-        else LAUNCH3(kname("k3_down", l), k3_top<OP_ELEMENT>, c.s_blocks, sblk, a);
-      }
+      a.chunk = c.s2_chunk;
+      cudaEvent_t e0_ = nullptr;
+      TRY3(begin_k(e, &e0_));
+      if (c.op.kind == OP_CONST) k3_top2<OP_CONST><<<c.s2_blocks, dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
+      else k3_top2<OP_ELEMENT><<<c.s2_blocks, dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
+      CKL3();
+      TRY3(end_k(e, kname("k3_down", l), e0_));
     } else {
       Down3 a = make_down(e, l, write);
       if (boxmg && jac) LAUNCH3(kname("k3_down", l), (k3_down_c<true, true>), c.c_grid, 128, a);
@@ -371,26 +330,12 @@ int enqueue_down(Engine3* e, bool write) {
     }
     if (jac && write && l > e->lmin) {
       SmoothS sa = make_smooth_s(e, l);
-      // the smoothing kernel is faster with the register window (measured: 2.18 vs 2.85 ms at L6)
-      if (kSmoothV == 'R') {
-        sa.chunk = c.s2_chunk;
-        cudaEvent_t e0_ = nullptr;
-        TRY3(begin_k(e, &e0_));
-        k3_smooth2r<<<c.s2_blocks, dim3(kSX, k2Y / 2), k2RSmemV, e->s>>>(sa);
-        CKL3();
-        TRY3(end_k(e, kname("k3_smooth", l), e0_));
-      } else if (kSmoothV == '2') {
-        sa.chunk = c.s2_chunk;
-        cudaEvent_t e0_ = nullptr;
-        TRY3(begin_k(e, &e0_));
-        k3_smooth2<<<c.s2_blocks, dim3(kSX, k2Y / 2), k2SmoothSmem, e->s>>>(sa);
-        CKL3();
-        TRY3(end_k(e, kname("k3_smooth", l), e0_));
-      } else if (kSmoothV == 's') {
-        LAUNCH3(kname("k3_smooth", l), k3_smooth_ss, c.s_blocks, sblk, sa);
-      } else {
-        LAUNCH3(kname("k3_smooth", l), k3_smooth_s, c.s_blocks, sblk, sa);
-      }
+      sa.chunk = c.s2_chunk;
+      cudaEvent_t e0_ = nullptr;
+      TRY3(begin_k(e, &e0_));
+      k3_smooth2r<<<c.s2_blocks, dim3(kSX, k2Y / 2), k2RSmemV, e->s>>>(sa);
+      CKL3();
+      TRY3(end_k(e, kname("k3_smooth", l), e0_));
     }
   }
   Chain3 ch{};
@@ -653,12 +598,7 @@ int build(Engine3* e, const tmg_tree3* t) {
   }
   CK3(cudaFuncSetAttribute(k3_top2<OP_CONST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2TopSmem));
   CK3(cudaFuncSetAttribute(k3_top2<OP_ELEMENT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2TopSmem));
-  CK3(cudaFuncSetAttribute(k3_smooth2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2SmoothSmem));
   CK3(cudaFuncSetAttribute(k3_smooth2r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2RSmemV));
-  CK3(cudaFuncSetAttribute(k3_top2r<OP_CONST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(k2RSmemV + k2RSmemC)));
-  CK3(cudaFuncSetAttribute(k3_top2r<OP_ELEMENT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(k2RSmemV + k2RSmemC)));
   int* deg;
   TRY3(alloc3(e, &deg, 1));
   if (cfg.flavor == TMG_GEOMETRIC) {

@@ -1,18 +1,24 @@
 // 3D cycle kernels specialised for the large levels (same per-element DAGs as
 // kernels3d.cu / oracle/mg3d.py, different data movement):
 //
-// * k3_top<KIND>   finest-level down sweep, 2.5D: a CTA owns a 32 (k) x 8 (j)
-//                  column and marches a chunk of i-planes, keeping a ring of
-//                  three u-planes (+halo) and two cell-coefficient planes in
-//                  shared memory, so each u / coefficient value is read from
-//                  HBM once per sweep instead of 27 / 8 times through L1.
-// * k3_smooth_s    R~ smoothing sm = A1(rho) * s with the same 2.5D scheme.
+// * k3_top2<KIND>  finest-level down sweep, 2.5D: a CTA owns a 32 (k) x 16 (j)
+//                  column (two rows per thread) and marches a chunk of
+//                  i-planes; halo planes of u and of the cell coefficients are
+//                  staged with cp.async into a shared-memory ring, so each
+//                  value is read from HBM once per sweep.
+// * k3_smooth2r    adaFACx smoothing sm = A1(rho) * s, two rows per thread
+//                  with a register window along i (6 shared loads / vertex).
+// * k3_smooth_s    the same, one row per thread (coarser levels).
 // * k3_down_c      coarse-level down sweep: operator apply + FAS RHS +
 //                  Jacobi + adaFACx damping; R and R~ share one pass over
 //                  the 124 BoxMG weight planes (each weight loaded once).
-// * k3_up_cell     prolongation owned by coarse cells: thread W updates the
-//                  27 fine vertices 3W + r, reading every P weight exactly
-//                  once with warp-coalesced plane loads.
+// * k3_up_cell     prolongation owned by coarse cells: thread (W, ri, rj)
+//                  updates fine vertices 3W + (ri, rj, 0..2), reading every P
+//                  weight exactly once with warp-coalesced plane loads.
+// Variants measured and dropped (config 5, L6): 1-row register / shared
+// windows for the top kernel (6.3 / 4.8 ms vs 4.4), 2-row register window for
+// the top kernel (spills, 7.2 ms), warp-staged coalesced prolongation rows
+// (6.7 ms vs 5.4).
 #include "kernels3d.cuh"
 
 namespace t3 {
@@ -175,101 +181,6 @@ __device__ __forceinline__ void stream25(const Column& col, const double* x, con
   cp_wait<0>();
 }
 
-// Variant of stream25 that keeps no register window: the body reads its 27
-// neighbours straight from the shared-memory ring (three live planes), which
-// frees ~60 registers per thread for occupancy.  Same stage depth.
-template <bool CELLS, class Body>
-__device__ __forceinline__ void stream25s(const Column& col, const double* x, const double* e,
-                                          double (*us)[kColU * kRowU], double (*cs)[kColC * kRowC],
-                                          Body&& body) {
-  const int ia = col.ia, ib = col.ib;
-  auto issue = [&](int g, int slot) {
-    col.stage_v(us[slot], x, ia - 1 + g);
-    if (CELLS) col.stage_c(cs[slot], e, ia - 1 + g);
-    cp_commit();
-  };
-#pragma unroll
-  for (int g = 0; g < kStages - 1; ++g) issue(g, g);
-  for (int i0 = ia; i0 < ib; i0 += kStages) {
-#pragma unroll
-    for (int u = 0; u < kStages; ++u) {
-      const int i = i0 + u;
-      if (i < ib) {
-        cp_wait<kStages - 4>();
-        __syncthreads();
-        issue(kStages - 1 + (i - ia), (u + kStages - 1) % kStages);  // slot of plane i-2
-        body(i, us[u % kStages], us[(u + 1) % kStages], us[(u + 2) % kStages],
-             CELLS ? cs[u % kStages] : nullptr, CELLS ? cs[(u + 1) % kStages] : nullptr);
-      }
-    }
-  }
-  cp_wait<0>();
-}
-
-template <int KIND>
-__global__ void __launch_bounds__(kSB, 4) k3_top_s(const __grid_constant__ Top3 a) {
-  __shared__ double us[kStages][kColU * kRowU];
-  __shared__ double cs[KIND == OP_ELEMENT ? kStages : 1][kColC * kRowC];
-  const Column col(a.N, a.ilo, a.ihi, a.chunk);
-  const int N = a.N;
-  const size_t NN = (size_t)N * N;
-  const int k = col.k0 + threadIdx.x, j = col.j0 + threadIdx.y;
-  const bool own = k <= N - 2 && j <= N - 2;
-  const size_t col_off = (size_t)j * N + k;
-  const int xo = (threadIdx.y + 1) * kRowU + threadIdx.x + 1;
-  const int co = (threadIdx.y + 1) * kRowC + threadIdx.x + 1;
-  double s = 0.0, mx = 0.0;
-  stream25s<KIND == OP_ELEMENT>(col, a.u, a.op.e, us, cs,
-      [&](int i, const double* pm, const double* p0, const double* pp, const double* cm,
-          const double* c0) {
-        if (!own) return;
-        const size_t v = (size_t)i * NN + col_off;
-        const double rhs = a.rhs ? __ldg(a.rhs + v) : 0.0;
-        double x[27];
-#pragma unroll
-        for (int t = 0; t < 9; ++t) {
-          const int o = xo + (t / 3 - 1) * kRowU + (t % 3 - 1);
-          x[t] = pm[o];
-          x[9 + t] = p0[o];
-          x[18 + t] = pp[o];
-        }
-        double au, dg;
-        if (KIND == OP_CONST) {
-          au = const_from(x, a.op.m, a.op.se, a.op.sc);
-          dg = a.op.cdiag;
-        } else {
-          double ec[8], E, T;
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {  // cell (i-c0, j-c1, k-c2)
-            const int c0b = c & 1, c1 = (c >> 1) & 1, c2 = c >> 2;
-            ec[c] = (c0b ? cm : c0)[co - c1 * kRowC - c2];
-          }
-          element_ET(x, ec, E, T);
-          dg = K_D * E;
-          au = (dg * x[13]) - (K_E * T);
-        }
-        const double rho = rhs - au;
-        const double t = a.hw * rho;
-        s = s + t * t;
-        mx = fmax(mx, fabs(rho));
-        a.g[v] = (a.w * rho) / dg;
-        if (a.rho) a.rho[v] = rho;
-      });
-  __shared__ double rs[kSB / 32], rm[kSB / 32];
-  for (int o = 16; o > 0; o >>= 1) {
-    s += __shfl_down_sync(0xffffffffu, s, o);
-    mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
-  }
-  if ((col.lt & 31) == 0) { rs[col.lt >> 5] = s; rm[col.lt >> 5] = mx; }
-  __syncthreads();
-  if (col.lt == 0) {
-    double A = 0.0, B = 0.0;
-    for (int q = 0; q < kSB / 32; ++q) { A += rs[q]; B = fmax(B, rm[q]); }
-    a.part_sum[blockIdx.x] = A;
-    a.part_max[blockIdx.x] = B;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Two rows per thread: CTA = 32 (k) x 16 (j) column, 256 threads, thread
 // (tx, ty) owns rows j0 + 2 ty and j0 + 2 ty + 1.  The 4 x 3 neighbourhood
@@ -277,7 +188,6 @@ __global__ void __launch_bounds__(kSB, 4) k3_top_s(const __grid_constant__ Top3 
 // of 27) and every per-plane overhead (staging, barrier, loop) is shared by
 // two vertices.
 constexpr int k2Y = 16;
-constexpr int k2Stages = 5;  // 5 x (612 + 561) doubles fit the 48 KB static limit
 constexpr int k2RowU = kSX + 2, k2ColU = k2Y + 2;
 constexpr int k2RowC = kSX + 1, k2ColC = k2Y + 1;
 
@@ -379,9 +289,8 @@ __device__ __forceinline__ void load_two(const double* pm, const double* p0, con
     }
 }
 
-constexpr int k2TopStages = 5, k2SmoothStages = 10;  // measured: top 5 > 8 stages (occupancy)
+constexpr int k2TopStages = 5;  // measured: 5 stages beat 8 (occupancy)
 constexpr size_t k2TopSmem = sizeof(double) * k2TopStages * (k2ColU * k2RowU + k2ColC * k2RowC);
-constexpr size_t k2SmoothSmem = sizeof(double) * k2SmoothStages * k2ColU * k2RowU;
 
 // Two rows per thread with a register window along i: each plane's 4 x 3
 // neighbourhood of the thread's two vertices is read from shared memory once
@@ -452,7 +361,6 @@ __device__ __forceinline__ void pick27(const double* wm, const double* w0, const
 
 constexpr int k2RStages = 6;
 constexpr size_t k2RSmemV = sizeof(double) * k2RStages * k2ColU * k2RowU;
-constexpr size_t k2RSmemC = sizeof(double) * k2RStages * k2ColC * k2RowC;
 
 __global__ void __launch_bounds__(kSB, 2) k3_smooth2r(const __grid_constant__ SmoothS a) {
   extern __shared__ double dyn2[];  // k2RSmemV
@@ -478,70 +386,6 @@ __global__ void __launch_bounds__(kSB, 2) k3_smooth2r(const __grid_constant__ Sm
           a.sm[v + N] = v1 * a.scale;
         }
       });
-}
-
-template <int KIND>
-__global__ void __launch_bounds__(kSB, 2) k3_top2r(const __grid_constant__ Top3 a) {
-  extern __shared__ double dyn2[];  // k2RSmemV + k2RSmemC
-  auto us = reinterpret_cast<double(*)[k2ColU * k2RowU]>(dyn2);
-  auto cs = reinterpret_cast<double(*)[k2ColC * k2RowC]>(dyn2 + k2RStages * k2ColU * k2RowU);
-  const Column2 col(a.N, a.ilo, a.ihi, a.chunk);
-  const int N = a.N;
-  const size_t NN = (size_t)N * N;
-  const int k = col.k0 + threadIdx.x, j = col.j0 + 2 * threadIdx.y;
-  const bool ok0 = k <= N - 2 && j <= N - 2, ok1 = k <= N - 2 && j + 1 <= N - 2;
-  const size_t col_off = (size_t)j * N + k;
-  const int xo = (2 * threadIdx.y + 1) * k2RowU + threadIdx.x + 1;
-  const int co = (2 * threadIdx.y + 1) * k2RowC + threadIdx.x + 1;
-  double s = 0.0, mx = 0.0;
-  stream25x2r<k2RStages, KIND == OP_ELEMENT>(col, a.u, a.op.e, us, cs, xo, co,
-      [&](int i, const double* wm, const double* w0, const double* wp, const double* em,
-          const double* e0) {
-        if (!ok0) return;
-        const size_t v = (size_t)i * NN + col_off;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (h == 1 && !ok1) break;
-          const size_t vh = v + (size_t)h * N;
-          const double rhs = a.rhs ? __ldg(a.rhs + vh) : 0.0;
-          double x[27];
-          pick27(wm, w0, wp, h, x);
-          double au, dg;
-          if (KIND == OP_CONST) {
-            au = const_from(x, a.op.m, a.op.se, a.op.sc);
-            dg = a.op.cdiag;
-          } else {
-            double ec[8], E, T;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {  // cell (i-c0, j+h-c1, k-c2): rows j-1..j+1 -> index h+1-c1
-              const int c0b = c & 1, c1 = (c >> 1) & 1, c2 = c >> 2;
-              ec[c] = (c0b ? em : e0)[(h + 1 - c1) * 2 + c2];
-            }
-            element_ET(x, ec, E, T);
-            dg = K_D * E;
-            au = (dg * x[13]) - (K_E * T);
-          }
-          const double rho = rhs - au;
-          const double t = a.hw * rho;
-          s = s + t * t;
-          mx = fmax(mx, fabs(rho));
-          a.g[vh] = (a.w * rho) / dg;
-          if (a.rho) a.rho[vh] = rho;
-        }
-      });
-  __shared__ double rs[kSB / 32], rm[kSB / 32];
-  for (int o = 16; o > 0; o >>= 1) {
-    s += __shfl_down_sync(0xffffffffu, s, o);
-    mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
-  }
-  if ((col.lt & 31) == 0) { rs[col.lt >> 5] = s; rm[col.lt >> 5] = mx; }
-  __syncthreads();
-  if (col.lt == 0) {
-    double A = 0.0, B = 0.0;
-    for (int q = 0; q < kSB / 32; ++q) { A += rs[q]; B = fmax(B, rm[q]); }
-    a.part_sum[blockIdx.x] = A;
-    a.part_max[blockIdx.x] = B;
-  }
 }
 
 template <int KIND>
@@ -624,120 +468,6 @@ __global__ void __launch_bounds__(kSB, 3) k3_top2(const __grid_constant__ Top3 a
     a.part_sum[blockIdx.x] = A;
     a.part_max[blockIdx.x] = B;
   }
-}
-
-__global__ void __launch_bounds__(kSB, 4) k3_smooth2(const __grid_constant__ SmoothS a) {
-  extern __shared__ double dyn2[];  // k2SmoothSmem
-  auto xs = reinterpret_cast<double(*)[k2ColU * k2RowU]>(dyn2);
-  const Column2 col(a.N, a.ilo, a.ihi, a.chunk);
-  const int N = a.N;
-  const size_t NN = (size_t)N * N;
-  const int k = col.k0 + threadIdx.x, j = col.j0 + 2 * threadIdx.y;
-  const bool ok0 = k <= N - 2 && j <= N - 2, ok1 = k <= N - 2 && j + 1 <= N - 2;
-  const size_t col_off = (size_t)j * N + k;
-  const int xo = (2 * threadIdx.y + 1) * k2RowU + threadIdx.x + 1;
-  stream25x2<k2SmoothStages, false>(col, a.x, nullptr, xs, nullptr,
-      [&](int i, const double* pm, const double* p0, const double* pp, const double*, const double*) {
-        if (!ok0) return;
-        double x0[27], x1[27];
-        load_two(pm, p0, pp, xo, x0, x1);
-        double v0 = const_from(x0, C_D8, C_E6, C_C12);
-        v0 = v0 * a.scale;
-        const size_t v = (size_t)i * NN + col_off;
-        a.sm[v] = v0;
-        if (ok1) {
-          double v1 = const_from(x1, C_D8, C_E6, C_C12);
-          v1 = v1 * a.scale;
-          a.sm[v + N] = v1;
-        }
-      });
-}
-
-template <int KIND>
-__global__ void __launch_bounds__(kSB, 2) k3_top(const __grid_constant__ Top3 a) {
-  __shared__ double us[kStages][kColU * kRowU];
-  __shared__ double cs[KIND == OP_ELEMENT ? kStages : 1][kColC * kRowC];
-  const Column col(a.N, a.ilo, a.ihi, a.chunk);
-  const int N = a.N;
-  const size_t NN = (size_t)N * N;
-  const int k = col.k0 + threadIdx.x, j = col.j0 + threadIdx.y;
-  const bool own = k <= N - 2 && j <= N - 2;
-  const size_t col_off = (size_t)j * N + k;
-  double rhs_n = (own && a.rhs) ? __ldg(a.rhs + (size_t)col.ia * NN + col_off) : 0.0;
-  double s = 0.0, mx = 0.0;
-  stream25<KIND == OP_ELEMENT>(col, a.u, a.op.e, us, cs,
-      [&](int i, const double* xm, const double* x0, const double* xp, const double* em,
-          const double* e0) {
-        const double rhs = rhs_n;
-        if (own && a.rhs && i + 1 < col.ib) rhs_n = __ldg(a.rhs + (size_t)(i + 1) * NN + col_off);
-        if (!own) return;
-        double x[27];
-#pragma unroll
-        for (int t = 0; t < 9; ++t) {
-          x[t] = xm[t];
-          x[9 + t] = x0[t];
-          x[18 + t] = xp[t];
-        }
-        double au, dg;
-        if (KIND == OP_CONST) {
-          au = const_from(x, a.op.m, a.op.se, a.op.sc);
-          dg = a.op.cdiag;
-        } else {
-          double ec[8], E, T;
-#pragma unroll
-          for (int c = 0; c < 8; ++c) ec[c] = (c & 1) ? em[c >> 1] : e0[c >> 1];  // cell (i-c0, j-c1, k-c2)
-          element_ET(x, ec, E, T);
-          dg = K_D * E;
-          au = (dg * x[13]) - (K_E * T);
-        }
-        const double rho = rhs - au;
-        const double t = a.hw * rho;
-        s = s + t * t;
-        mx = fmax(mx, fabs(rho));
-        const size_t v = (size_t)i * NN + col_off;
-        a.g[v] = (a.w * rho) / dg;
-        if (a.rho) a.rho[v] = rho;
-      });
-  // block reduction of the stats partials
-  __shared__ double rs[kSB / 32], rm[kSB / 32];
-  for (int o = 16; o > 0; o >>= 1) {
-    s += __shfl_down_sync(0xffffffffu, s, o);
-    mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
-  }
-  if ((col.lt & 31) == 0) { rs[col.lt >> 5] = s; rm[col.lt >> 5] = mx; }
-  __syncthreads();
-  if (col.lt == 0) {
-    double A = 0.0, B = 0.0;
-    for (int q = 0; q < kSB / 32; ++q) { A += rs[q]; B = fmax(B, rm[q]); }
-    a.part_sum[blockIdx.x] = A;
-    a.part_max[blockIdx.x] = B;
-  }
-}
-
-__global__ void __launch_bounds__(kSB, 5) k3_smooth_ss(const __grid_constant__ SmoothS a) {
-  __shared__ double xs[kStages][kColU * kRowU];
-  const Column col(a.N, a.ilo, a.ihi, a.chunk);
-  const int N = a.N;
-  const size_t NN = (size_t)N * N;
-  const int k = col.k0 + threadIdx.x, j = col.j0 + threadIdx.y;
-  const bool own = k <= N - 2 && j <= N - 2;
-  const size_t col_off = (size_t)j * N + k;
-  const int xo = (threadIdx.y + 1) * kRowU + threadIdx.x + 1;
-  stream25s<false>(col, a.x, nullptr, xs, nullptr,
-      [&](int i, const double* pm, const double* p0, const double* pp, const double*, const double*) {
-        if (!own) return;
-        double x[27];
-#pragma unroll
-        for (int t = 0; t < 9; ++t) {
-          const int o = xo + (t / 3 - 1) * kRowU + (t % 3 - 1);
-          x[t] = pm[o];
-          x[9 + t] = p0[o];
-          x[18 + t] = pp[o];
-        }
-        double v = const_from(x, C_D8, C_E6, C_C12);
-        v = v * a.scale;
-        a.sm[(size_t)i * NN + col_off] = v;
-      });
 }
 
 __global__ void __launch_bounds__(kSB, 3) k3_smooth_s(const __grid_constant__ SmoothS a) {
