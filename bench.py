@@ -408,6 +408,40 @@ def run_ours(args, dist: Dist):
                 "cycle_frac": bm["cycle"] / (ms_step * 1e-3) / 1e9 / peak}
     eng.close()
 
+    # ---- time to a 1e-8 residual reduction (north star; bench.py:200 stop rule) ----
+    ttt = None
+    if not args.no_ttt:
+        wl3 = wl if wl.dim == 3 else workloads.by_name(args.workload)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e3 = GpuEngine(wl3.tree, SolverConfig(variant=wl3.variant, flavor=wl3.flavor), device=dev,
+                       sync="lazy")
+        e3.rhs.update(wl3.rhs)
+        e3._flush_rhs()
+        torch.cuda.synchronize()
+        t_setup = time.perf_counter() - t0
+        cap, chunk, done, r0, reached = args.ttt_cap, 5, 0, None, None
+        t0 = time.perf_counter()
+        while done < cap and reached is None:
+            hs = e3.advance_many(min(chunk, cap - done))
+            for k, h in enumerate(hs):
+                if r0 is None:
+                    r0 = h.l2h
+                if reached is None and h.l2h <= 1e-8 * r0:
+                    reached = done + k
+            done += len(hs)
+        torch.cuda.synchronize()
+        t_solve = time.perf_counter() - t0
+        ttt = {"target": 1e-8, "reached": reached is not None,
+               "cycles": reached if reached is not None else done,
+               "final_reduction": hs[-1].l2h / r0 if r0 else None,
+               "setup_s": t_setup, "solve_s": t_solve,
+               "note": "stats of cycle n are the residual of the iterate it starts from "
+                       "(solvers.py:129-135); solve_s includes the cycles run past the target "
+                       f"inside the last chunk of {chunk}" if reached is not None else
+                       f"not reached within {cap} cycles"}
+        e3.close()
+
     # ---- end to end through the drop-in API -------------------------------------
     wl2 = wl if wl.dim == 3 else workloads.by_name(args.workload)
     tree = wl2.tree
@@ -460,6 +494,7 @@ def run_ours(args, dist: Dist):
                        "ms_per_step_l2_warm": ms_warm / args.steps,
                        "total_updates_per_s": dist.ws * updates / (ms_step * 1e-3)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "time_to_1e-8": ttt,
             "gpu_launches": launches * args.steps,
             "kernel_ms": {k: round(v[0] / v[1], 6) for k, v in prof.items()},
         }
@@ -577,6 +612,8 @@ def main():
     ap.add_argument("--workload", default="config5")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-1e-8 run")
+    ap.add_argument("--ttt-cap", type=int, default=200, help="cycle cap of the time-to-1e-8 run")
     ap.add_argument("--force-shard", action="store_true",
                     help="3D: run the sharded (NCCL) path even on one rank (testing)")
     args = ap.parse_args()
