@@ -113,6 +113,7 @@ struct tmg_handle {
   // coarse chain (cluster kernel) and its argument blocks
   int lc = 0, part_base = 0;
   unsigned long long* stamps = nullptr;  // k_coarse phase timestamps (diagnostics)
+  double* scratch = nullptr;             // per-CTA residual partials of the cluster chain
 };
 
 namespace {
@@ -307,6 +308,12 @@ tmg::UpArgs make_up(tmg_handle* h, int l) {
   return a;
 }
 
+// the coarse chain on a thread-block cluster (TMG_CHAIN=block: one CTA)
+const bool kChainCluster = [] {
+  const char* v = std::getenv("TMG_CHAIN");
+  return !(v && v[0] == 'b');
+}();
+
 int launch_coarse(tmg_handle* h, bool write) {
   tmg::CoarseArgs a{};
   a.l0 = h->lmin;
@@ -325,7 +332,23 @@ int launch_coarse(tmg_handle* h, bool write) {
   }
   cudaEvent_t e0 = nullptr;
   TRY(begin_k(h, "k_coarse", &e0));
-  tmg::k_coarse<<<1, tmg::kCoarseBlock, 0, h->s>>>(a);
+  if (kChainCluster) {
+    // the chain on one thread-block cluster of kClusterCTAs CTAs
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(tmg::kClusterCTAs);
+    lc.blockDim = dim3(tmg::kCoarseBlock);
+    lc.stream = h->s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = tmg::kClusterCTAs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, tmg::k_coarse_cl, a, h->scratch));
+  } else {
+    tmg::k_coarse<<<1, tmg::kCoarseBlock, 0, h->s>>>(a);
+  }
   CKL();
   TRY(end_k(h, "k_coarse", e0));
   return TMG_OK;
@@ -666,6 +689,7 @@ int build(tmg_handle* h, const tmg_tree* t) {
                      cudaMemcpyHostToDevice, h->s));
   h->part_base = parts;
   TRY(dalloc(h, &h->stamps, 64));
+  TRY(dalloc(h, &h->scratch, 2 * tmg::kClusterCTAs));
   h->nparts = parts;
   TRY(dalloc(h, &h->part_sum, parts));
   TRY(dalloc(h, &h->part_max, parts));

@@ -893,6 +893,81 @@ __global__ void __launch_bounds__(kCoarseBlock) k_coarse(const __grid_constant__
   }
 }
 
+// The coarse chain on a thread-block cluster: the same phases as k_coarse,
+// with each level's vertices spread over the kClusterCTAs CTAs of the cluster
+// and cluster barriers (release / acquire at cluster scope) between levels.
+// Data produced inside the launch is read through L2 (LdCG).  The residual
+// partials are combined in a fixed order by CTA rank 0.
+constexpr int kClusterCTAs = 8;
+
+__global__ void __launch_bounds__(kCoarseBlock) k_coarse_cl(const __grid_constant__ CoarseArgs a,
+                                                             double* scratch) {
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ double rs[kCoarseBlock / 32], rm[kCoarseBlock / 32];
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int rank = (int)cl.block_rank(), csz = (int)cl.num_blocks();
+  const int gt = rank * nthr + tid, gn = csz * nthr;
+  double s = 0.0, m = 0.0;
+  for (int l = a.lc; l >= a.l0; --l) {
+    const DownArgs& d = a.down[l - a.l0];
+    const int N = d.N, nv = N * N;
+    if (d.is_top) {
+      for (int v = gt; v < nv; v += gn) {
+        const int i = v / N;
+        down_vertex<LdCG, 1>(d, i, v - i * N, s, m);
+      }
+    } else {
+      for (int v = gt; v < nv; v += gn) {
+        const int i = v / N;
+        down_vertex<LdCG, 0>(d, i, v - i * N, s, m);
+      }
+    }
+    cl.sync();
+  }
+  // per-CTA partial -> scratch[rank]; rank 0 reduces grid partials + scratch in order
+  block_reduce<kCoarseBlock>(s, m);
+  if (tid == 0) {
+    scratch[2 * rank] = s;
+    scratch[2 * rank + 1] = m;
+  }
+  cl.sync();
+  if (rank == 0) {
+    double x = 0.0, y = 0.0;
+    for (int k = tid; k < a.part_base; k += nthr) {
+      x += a.part_sum[k];
+      y = fmax(y, a.part_max[k]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      x += __shfl_down_sync(0xffffffffu, x, o);
+      y = fmax(y, __shfl_down_sync(0xffffffffu, y, o));
+    }
+    if ((tid & 31) == 0) { rs[tid >> 5] = x; rm[tid >> 5] = y; }
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0, u = 0.0;
+      for (int k = 0; k < kCoarseBlock / 32; ++k) { t += rs[k]; u = fmax(u, rm[k]); }
+      for (int k = 0; k < csz; ++k) {
+        t += __ldcg(scratch + 2 * k);
+        u = fmax(u, __ldcg(scratch + 2 * k + 1));
+      }
+      const int slot = *a.counter;
+      a.hist[2 * (slot % a.cap)] = sqrt(t);
+      a.hist[2 * (slot % a.cap) + 1] = u;
+      *a.counter = slot + 1;
+    }
+  }
+  if (!a.do_up) return;
+  for (int l = a.l0; l <= a.lc; ++l) {
+    const UpArgs& u = a.up[l - a.l0];
+    const int N = u.N, nv = N * N;
+    for (int v = gt; v < nv; v += gn) {
+      const int i = v / N;
+      up_vertex<LdCG>(u, i, v - i * N);
+    }
+    cl.sync();
+  }
+}
+
 // FAS injection (solvers.py:283-288), standalone update_fas_state()
 __global__ void k_inject_u(double* __restrict__ uc, const uint8_t* __restrict__ flags_c, int Nc,
                            const double* __restrict__ uf, int Nf) {

@@ -113,6 +113,7 @@ template <int TOP>
 __global__ void k_down(const __grid_constant__ DownArgs a);
 __global__ void k_up(const __grid_constant__ UpArgs a);
 __global__ void k_coarse(const __grid_constant__ CoarseArgs a);
+__global__ void k_coarse_cl(const __grid_constant__ CoarseArgs a, double* scratch);
 __global__ void k_inject_u(double* uc, const uint8_t* flags_c, int Nc, const double* uf, int Nf);
 __global__ void k_hang(double* u, const uint8_t* flags, int N, const double* uc, int Nc);
 
