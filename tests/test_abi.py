@@ -46,3 +46,23 @@ def test_config_validation_mirrors_reference():
         SolverConfig(omega=0.0)
     with pytest.raises(ValueError):
         SolverConfig(omega_hat=1.0)
+
+
+def test_product_package_never_imports_the_oracle():
+    """The oracle is test infrastructure: nothing under the product package may use it."""
+    pkg = os.path.join(ROOT, "paper_1903_10367_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_3d_entry_points_declared_and_bound():
+    decl = declared_symbols()
+    for name in ("tmg3_create", "tmg3_rebuild", "tmg3_shard", "tmg3_phase", "tmg3_field",
+                 "tmg3_stream", "tmg3_history", "tmg_dim"):
+        assert name in decl, name
+    L = _abi.lib()
+    for name in decl:
+        assert getattr(L, name).argtypes is not None or name in ("tmg_last_error", "tmg_device_count"), name

@@ -141,3 +141,27 @@ def test_3d_fused_fine_pass_equals_unfused(variant, monkeypatch):
     e1.pull()
     e2.pull()
     assert np.array_equal(wl1.tree.u[4], wl2.tree.u[4])
+
+
+def test_3d_error_paths_raise_like_the_reference():
+    import ctypes as C
+
+    from paper_1903_10367_b200 import _abi, sharding
+    wl = workloads.config5(levels=2, block=3)
+    with pytest.raises(ValueError):
+        GpuEngine(wl.tree, SolverConfig(variant="multiplicative-v10", flavor="boxmg"))
+    with pytest.raises(ValueError, match="rtilde_true_operator"):
+        GpuEngine(wl.tree, SolverConfig(variant="adafac-jac", flavor="boxmg", rtilde_true_operator=True))
+    wl = workloads.config5(levels=3)
+    eng = GpuEngine(wl.tree, SolverConfig(variant=wl.variant, flavor=wl.flavor), sync="lazy")
+    L = _abi.lib()
+    with pytest.raises(ValueError, match="not sharded"):
+        _abi.check(L.tmg3_phase(eng._h, _abi.PH_DOWN, 3))
+    lo = (C.c_int32 * 4)(0, 0, 0, 0)
+    hi = (C.c_int32 * 4)(0, 0, 0, 99)  # beyond the level
+    with pytest.raises(ValueError, match="plane range"):
+        _abi.check(L.tmg3_shard(eng._h, 2, lo, hi))
+    with pytest.raises(ValueError):
+        _abi.check(L.tmg_get_u(eng._h, 9, None))
+    with pytest.raises(ValueError):
+        sharding.plan(2, 8)  # too shallow for 8 ranks
