@@ -9,6 +9,8 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "engine3.h"
 #include "kernels3d.cu"
 #include "kernels3d_fast.cu"
@@ -23,6 +25,7 @@ struct Lvl3 {
   size_t nv = 0, ncell = 0;
   double *u = nullptr, *rhs = nullptr, *g = nullptr, *rho = nullptr, *sm = nullptr, *carry = nullptr;
   double *eff = nullptr, *coef = nullptr, *tbl = nullptr, *P = nullptr;
+  double* coefp = nullptr;  // finest level: coef with rows padded to even length (TMA)
   double *bR = nullptr, *bT = nullptr;  // level ltop-1: restrictions from the fused fine pass
   Op3 op{};
   double w = 0.0;
@@ -274,6 +277,57 @@ Up3 make_up(Engine3* e, int l) {
   return a;
 }
 
+// 3D tensor map of an N^3 fp64 vertex field for the TMA-staged 2.5D kernels:
+// box = one halo plane of a 32 x 16 column (34 x 18 doubles), zero fill
+// outside the grid (the stencils' zero extension).  false if the driver
+// entry point is unavailable (the kernels then stage with cp.async).
+bool vertex_tmap(CUtensorMap* map, const double* base, int N) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }();
+  if (!encode || !base) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)N};
+  const cuuint64_t strides[2] = {(cuuint64_t)N * 8, (cuuint64_t)N * N * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)k2RowU, (cuuint32_t)k2ColU, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// The same for the finest level's cell coefficients, stored with rows padded
+// to an even length (coefp) so that TMA can stride them.
+bool cell_tmap(CUtensorMap* map, const double* base, int n) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }();
+  if (!encode || !base) return false;
+  const cuuint64_t np = (cuuint64_t)(n + (n & 1));  // padded row length
+  const cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)n};
+  const cuuint64_t strides[2] = {np * 8, np * n * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)k2RowC, (cuuint32_t)k2ColC, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// TMA staging of the streaming kernels' vertex planes (TMG_TMA=0: cp.async)
+const bool kUseTma = [] {
+  const char* v = std::getenv("TMG_TMA");
+  return !(v && v[0] == '0');
+}();
+
 Top3 make_top(Engine3* e, int l) {
   Lvl3& c = e->L[l];
   Top3 a{};
@@ -290,6 +344,8 @@ Top3 make_top(Engine3* e, int l) {
   a.rho = (l > e->lmin) ? c.rho : nullptr;
   a.part_sum = e->part_sum;
   a.part_max = e->part_max;
+  a.use_tma = kUseTma && vertex_tmap(&a.tm, c.u, c.N);
+  if (a.use_tma && c.op.kind == OP_ELEMENT && c.coefp && cell_tmap(&a.tmc, c.coefp, c.N - 1)) a.use_tma = 2;
   return a;
 }
 
@@ -303,6 +359,7 @@ SmoothS make_smooth_s(Engine3* e, int l) {
   a.x = c.rho;
   a.sm = c.sm;
   a.scale = e->cfg.omega * 3.0 / 8.0;
+  a.use_tma = kUseTma && vertex_tmap(&a.tm, c.rho, c.N);
   return a;
 }
 
@@ -644,6 +701,15 @@ int build(Engine3* e, const tmg_tree3* t) {
       c.op.kind = OP_TABLE;
       c.op.tbl = c.tbl;
       raw = Rows{c.N, c.tbl, nullptr};
+    }
+  }
+  {  // row-padded copy of the finest level's cell coefficients for the TMA-staged top kernel
+    Lvl3& top = e->L[l1];
+    if (top.op.kind == OP_ELEMENT) {
+      const int n = top.N - 1, np = n + (n & 1);
+      TRY3(alloc3(e, &top.coefp, (size_t)n * n * np));
+      CK3(cudaMemcpy2DAsync(top.coefp, sizeof(double) * np, top.coef, sizeof(double) * n,
+                            sizeof(double) * n, (size_t)n * n, cudaMemcpyDeviceToDevice, e->s));
     }
   }
   int hdeg = 0;

@@ -19,6 +19,8 @@
 // windows for the top kernel (6.3 / 4.8 ms vs 4.4), 2-row register window for
 // the top kernel (spills, 7.2 ms), warp-staged coalesced prolongation rows
 // (6.7 ms vs 5.4).
+#include <cuda.h>  // CUtensorMap (kernel parameter of the TMA-staged kernels)
+
 #include "kernels3d.cuh"
 
 namespace t3 {
@@ -29,6 +31,9 @@ constexpr int kRowU = kSX + 2, kColU = kSY + 2;  // u plane with halo
 constexpr int kRowC = kSX + 1, kColC = kSY + 1;  // cell plane with halo (cells k-1.., j-1..)
 
 struct Top3 {
+  CUtensorMap tm;          // 3D map of u (box 34 x 18 x 1 doubles), used when use_tma
+  CUtensorMap tmc;         // 3D map of the row-padded cell coefficients (box 34 x 17 x 1), use_tma == 2
+  int use_tma;
   int N, ilo, ihi, chunk;  // planes [ilo, ihi) split in chunks
   const double* u;
   const double* rhs;
@@ -41,6 +46,8 @@ struct Top3 {
 };
 
 struct SmoothS {
+  CUtensorMap tm;  // 3D map of x (box 34 x 18 x 1 doubles), used when use_tma
+  int use_tma;
   int N, ilo, ihi, chunk;
   const double* x;
   double* sm;
@@ -64,6 +71,41 @@ __device__ __forceinline__ void cp_async8(void* smem, const double* gmem, bool p
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int Np>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(Np) : "memory"); }
+
+// TMA (cp.async.bulk.tensor) + mbarrier helpers: one elected thread arms the
+// slot's barrier with the byte count and issues the bulk tensor copy; the
+// consumers wait on the barrier's phase parity.
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned ready = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ready)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  } while (!ready);
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_addr(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(smem_addr(bar))
+      : "memory");
+}
 
 struct Column {
   static constexpr int kPU = (kColU * kRowU + kSB - 1) / kSB;
@@ -189,7 +231,12 @@ __device__ __forceinline__ void stream25(const Column& col, const double* x, con
 // two vertices.
 constexpr int k2Y = 16;
 constexpr int k2RowU = kSX + 2, k2ColU = k2Y + 2;
-constexpr int k2RowC = kSX + 1, k2ColC = k2Y + 1;
+constexpr int k2RowC = kSX + 2, k2ColC = k2Y + 1;  // 33 cells used; rows padded to 34 (TMA: 16-byte rows)
+// vertex-plane slot: 18 x 34 doubles padded to a multiple of 128 bytes (TMA destination)
+constexpr int k2SlotU = ((k2ColU * k2RowU * 8 + 127) / 128) * 128 / 8;
+constexpr unsigned k2BoxBytes = k2ColU * k2RowU * 8;
+constexpr int k2SlotC = ((k2ColC * k2RowC * 8 + 127) / 128) * 128 / 8;
+constexpr unsigned k2BoxBytesC = k2ColC * k2RowC * 8;
 
 struct Column2 {
   static constexpr int kPU = (k2ColU * k2RowU + kSB - 1) / kSB;
@@ -247,24 +294,50 @@ struct Column2 {
   }
 };
 
+// tm != nullptr: the vertex planes arrive by TMA (one bulk tensor copy per
+// plane, completion on bars[slot]); the cell planes keep 8-byte cp.async (their
+// rows are an odd number of doubles, which TMA strides cannot express).
 template <int S, bool CELLS, class Body>
 __device__ __forceinline__ void stream25x2(const Column2& col, const double* x, const double* e,
-                                           double (*us)[k2ColU * k2RowU], double (*cs)[k2ColC * k2RowC],
-                                           Body&& body) {
+                                           double (*us)[k2SlotU], double (*cs)[k2SlotC],
+                                           const CUtensorMap* tm, uint64_t* bars, Body&& body,
+                                           const CUtensorMap* tmc = nullptr) {
   const int ia = col.ia, ib = col.ib;
+  if (tm && col.lt == 0) {
+    for (int q = 0; q < S; ++q) mbar_init(&bars[q], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
   auto issue = [&](int g, int slot) {
-    col.stage_v(us[slot], x, ia - 1 + g);
-    if (CELLS) col.stage_c(cs[slot], e, ia - 1 + g);
+    const bool ctma = CELLS && tmc;
+    if (tm) {
+      if (col.lt == 0) {
+        mbar_expect_tx(&bars[slot], k2BoxBytes + (ctma ? k2BoxBytesC : 0u));
+        tma_load_3d(us[slot], tm, &bars[slot], col.k0 - 1, col.j0 - 1, ia - 1 + g);
+        if (ctma) tma_load_3d(cs[slot], tmc, &bars[slot], col.k0 - 1, col.j0 - 1, ia - 1 + g);
+      }
+    } else {
+      col.stage_v(us[slot], x, ia - 1 + g);
+    }
+    if (CELLS && !ctma) col.stage_c(cs[slot], e, ia - 1 + g);
     cp_commit();
+  };
+  auto wait_v = [&](int g) {
+    if (tm) mbar_wait(&bars[g % S], (unsigned)(g / S) & 1u);
   };
 #pragma unroll
   for (int g = 0; g < S - 1; ++g) issue(g, g);
+  if (tm) {
+    wait_v(0);
+    wait_v(1);
+  }
   for (int i0 = ia; i0 < ib; i0 += S) {
 #pragma unroll
     for (int u = 0; u < S; ++u) {
       const int i = i0 + u;
       if (i < ib) {
         cp_wait<S - 4>();
+        wait_v(i - ia + 2);
         __syncthreads();
         issue(S - 1 + (i - ia), (u + S - 1) % S);
         body(i, us[u % S], us[(u + 1) % S], us[(u + 2) % S],
@@ -290,7 +363,7 @@ __device__ __forceinline__ void load_two(const double* pm, const double* p0, con
 }
 
 constexpr int k2TopStages = 5;  // measured: 5 stages beat 8 (occupancy)
-constexpr size_t k2TopSmem = sizeof(double) * k2TopStages * (k2ColU * k2RowU + k2ColC * k2RowC);
+constexpr size_t k2TopSmem = sizeof(double) * k2TopStages * (k2SlotU + k2SlotC);
 
 // Two rows per thread with a register window along i: each plane's 4 x 3
 // neighbourhood of the thread's two vertices is read from shared memory once
@@ -299,15 +372,30 @@ constexpr size_t k2TopSmem = sizeof(double) * k2TopStages * (k2ColU * k2RowU + k
 // register rotation are compile-time constants.
 template <int S, bool CELLS, class Body>
 __device__ __forceinline__ void stream25x2r(const Column2& col, const double* x, const double* e,
-                                            double (*us)[k2ColU * k2RowU],
-                                            double (*cs)[k2ColC * k2RowC], int xo, int co,
-                                            Body&& body) {
+                                            double (*us)[k2SlotU],
+                                            double (*cs)[k2SlotC], int xo, int co,
+                                            const CUtensorMap* tm, uint64_t* bars, Body&& body) {
   static_assert(S % 3 == 0, "register rotation needs S % 3 == 0");
   const int ia = col.ia, ib = col.ib;
+  if (tm && col.lt == 0) {
+    for (int q = 0; q < S; ++q) mbar_init(&bars[q], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
   auto issue = [&](int g, int slot) {
-    col.stage_v(us[slot], x, ia - 1 + g);
+    if (tm) {
+      if (col.lt == 0) {
+        mbar_expect_tx(&bars[slot], k2BoxBytes);
+        tma_load_3d(us[slot], tm, &bars[slot], col.k0 - 1, col.j0 - 1, ia - 1 + g);
+      }
+    } else {
+      col.stage_v(us[slot], x, ia - 1 + g);
+    }
     if (CELLS) col.stage_c(cs[slot], e, ia - 1 + g);
     cp_commit();
+  };
+  auto wait_v = [&](int g) {
+    if (tm) mbar_wait(&bars[g % S], (unsigned)(g / S) & 1u);
   };
   auto ld12 = [&](const double* p, double w[12]) {
 #pragma unroll
@@ -325,6 +413,8 @@ __device__ __forceinline__ void stream25x2r(const Column2& col, const double* x,
   for (int g = 0; g < S; ++g) issue(g, g);
   double X[3][12], E[3][6];
   cp_wait<S - 2>();
+  wait_v(0);
+  wait_v(1);
   __syncthreads();
   ld12(us[0], X[0]);
   ld12(us[1], X[1]);
@@ -335,6 +425,7 @@ __device__ __forceinline__ void stream25x2r(const Column2& col, const double* x,
       const int i = i0 + u;
       if (i < ib) {
         cp_wait<S - 3>();
+        wait_v(i - ia + 2);
         __syncthreads();
         ld12(us[(u + 2) % S], X[(u + 2) % 3]);
         if (CELLS) ld6(cs[(u + 1) % S], E[(u + 1) % 3]);
@@ -360,11 +451,12 @@ __device__ __forceinline__ void pick27(const double* wm, const double* w0, const
 }
 
 constexpr int k2RStages = 6;
-constexpr size_t k2RSmemV = sizeof(double) * k2RStages * k2ColU * k2RowU;
+constexpr size_t k2RSmemV = sizeof(double) * k2RStages * k2SlotU;
 
 __global__ void __launch_bounds__(kSB, 2) k3_smooth2r(const __grid_constant__ SmoothS a) {
-  extern __shared__ double dyn2[];  // k2RSmemV
-  auto xs = reinterpret_cast<double(*)[k2ColU * k2RowU]>(dyn2);
+  extern __shared__ __align__(128) double dyn2[];  // k2RSmemV
+  __shared__ uint64_t bars[k2RStages];
+  auto xs = reinterpret_cast<double(*)[k2SlotU]>(dyn2);
   const Column2 col(a.N, a.ilo, a.ihi, a.chunk);
   const int N = a.N;
   const size_t NN = (size_t)N * N;
@@ -372,7 +464,7 @@ __global__ void __launch_bounds__(kSB, 2) k3_smooth2r(const __grid_constant__ Sm
   const bool ok0 = k <= N - 2 && j <= N - 2, ok1 = k <= N - 2 && j + 1 <= N - 2;
   const size_t col_off = (size_t)j * N + k;
   const int xo = (2 * threadIdx.y + 1) * k2RowU + threadIdx.x + 1;
-  stream25x2r<k2RStages, false>(col, a.x, nullptr, xs, nullptr, xo, 0,
+  stream25x2r<k2RStages, false>(col, a.x, nullptr, xs, nullptr, xo, 0, a.use_tma ? &a.tm : nullptr, bars,
       [&](int i, const double* wm, const double* w0, const double* wp, const double*, const double*) {
         if (!ok0) return;
         const size_t v = (size_t)i * NN + col_off;
@@ -390,9 +482,10 @@ __global__ void __launch_bounds__(kSB, 2) k3_smooth2r(const __grid_constant__ Sm
 
 template <int KIND>
 __global__ void __launch_bounds__(kSB, 3) k3_top2(const __grid_constant__ Top3 a) {
-  extern __shared__ double dyn2[];  // k2TopSmem
-  auto us = reinterpret_cast<double(*)[k2ColU * k2RowU]>(dyn2);
-  auto cs = reinterpret_cast<double(*)[k2ColC * k2RowC]>(dyn2 + k2TopStages * k2ColU * k2RowU);
+  extern __shared__ __align__(128) double dyn2[];  // k2TopSmem
+  __shared__ uint64_t bars[k2TopStages];
+  auto us = reinterpret_cast<double(*)[k2SlotU]>(dyn2);
+  auto cs = reinterpret_cast<double(*)[k2SlotC]>(dyn2 + k2TopStages * k2SlotU);
   const Column2 col(a.N, a.ilo, a.ihi, a.chunk);
   const int N = a.N;
   const size_t NN = (size_t)N * N;
@@ -402,7 +495,8 @@ __global__ void __launch_bounds__(kSB, 3) k3_top2(const __grid_constant__ Top3 a
   const int xo = (2 * threadIdx.y + 1) * k2RowU + threadIdx.x + 1;
   const int co = (2 * threadIdx.y + 1) * k2RowC + threadIdx.x + 1;
   double s = 0.0, mx = 0.0;
-  stream25x2<k2TopStages, KIND == OP_ELEMENT>(col, a.u, a.op.e, us, cs,
+  const CUtensorMap* tmc = (KIND == OP_ELEMENT && a.use_tma == 2) ? &a.tmc : nullptr;
+  stream25x2<k2TopStages, KIND == OP_ELEMENT>(col, a.u, a.op.e, us, cs, a.use_tma ? &a.tm : nullptr, bars,
       [&](int i, const double* pm, const double* p0, const double* pp, const double* cm,
           const double* c0) {
         if (!ok0) return;
@@ -454,7 +548,8 @@ __global__ void __launch_bounds__(kSB, 3) k3_top2(const __grid_constant__ Top3 a
           a.g[v + N] = (a.w * rho1) / dg1;
           if (a.rho) a.rho[v + N] = rho1;
         }
-      });
+      },
+      tmc);
   __shared__ double rs[kSB / 32], rm[kSB / 32];
   for (int o = 16; o > 0; o >>= 1) {
     s += __shfl_down_sync(0xffffffffu, s, o);
