@@ -67,6 +67,10 @@ typedef struct {
   double damping_scale;
   int32_t rtilde_true_operator;
   int32_t device;
+  /* BoxMG, 3D: start from d-linear P and rediscretised coarse rows and build
+   * BoxMG P + Galerkin rows one level per cycle, finest first (the paper's
+   * throttled setup; the reference builds all levels in rebuild()) */
+  int32_t throttled;
 } tmg_config;
 
 /* The spacetree data model, spacetree.py:86-120.  refined[l] for l < lmax

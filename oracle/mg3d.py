@@ -261,9 +261,11 @@ def restrict_dlinear(f: np.ndarray) -> np.ndarray:
 
 
 def dlinear_p_table(nc: int) -> np.ndarray:
-    """The d-linear weights in the BoxMG P layout (for tests)."""
+    """The d-linear weights in the BoxMG P layout: ((w_a * w_b) * w_c), w_o = max(0, 1 - |o|/3),
+    zero where the fine offset leaves the grid (the throttled start, and tests)."""
     w = np.maximum(0.0, 1.0 - np.abs(np.arange(-2, 3)) / 3.0)
-    p = np.broadcast_to(np.einsum("a,b,c->abc", w, w, w), (nc + 1,) * 3 + (5, 5, 5)).copy()
+    w3 = (w[:, None, None] * w[None, :, None]) * w[None, None, :]
+    p = np.broadcast_to(w3, (nc + 1,) * 3 + (5, 5, 5)).copy()
     idx = 3 * np.arange(nc + 1)
     for o in range(-2, 3):
         out = (idx + o < 0) | (idx + o > 3 * nc)
@@ -571,6 +573,11 @@ class Config:
     omega_tilde: float | None = None
     omega_hat: float = 0.7
     damping_scale: float = 1.0
+    # BoxMG only: start from d-linear P and rediscretised coarse operators and
+    # replace them by BoxMG P / Galerkin rows one level per cycle, finest first
+    # (the paper's throttled operator propagation; the
+    # reference builds every level eagerly, solvers.py:227-250)
+    throttled: bool = False
 
     @property
     def wt(self) -> float:
@@ -619,17 +626,27 @@ class Engine:
                 self.tr[l] = Transfer(3**l, None, cfg.omega)
         else:
             self.ops[top] = Op(self.coef[top])
-            raw = self.ops[top].table()
-            for l in range(top - 1, l0 - 1, -1):
-                P = boxmg_p(raw, 3**l)
-                masked = raw * self.masks[l + 1]["dof"][..., None]
-                rap = galerkin(masked, P)
-                tbl = assemble_table(self.coef[l])
-                ov = self.masks[l]["overlapped"]
-                tbl[ov] = rap[ov]
-                self.ops[l] = Op(table=tbl)
-                self.tr[l] = Transfer(3**l, P, cfg.omega)
-                raw = tbl
+            self.thr_next = l0 - 1
+            if cfg.throttled:
+                for l in range(top - 1, l0 - 1, -1):
+                    self.ops[l] = Op(table=assemble_table(self.coef[l]))
+                    self.tr[l] = Transfer(3**l, dlinear_p_table(3**l), cfg.omega)
+                self.thr_next = top - 1
+            else:
+                for l in range(top - 1, l0 - 1, -1):
+                    self._build_boxmg_level(l)
+
+    def _build_boxmg_level(self, l: int) -> None:
+        """BoxMG P and Galerkin rows of level l from level l+1's operator (solvers.py:227-250)."""
+        raw = self.ops[l + 1].table()
+        P = boxmg_p(raw, 3**l)
+        masked = raw * self.masks[l + 1]["dof"][..., None]
+        rap = galerkin(masked, P)
+        tbl = assemble_table(self.coef[l])
+        ov = self.masks[l]["overlapped"]
+        tbl[ov] = rap[ov]
+        self.ops[l] = Op(table=tbl)
+        self.tr[l] = Transfer(3**l, P, self.cfg.omega)
 
     def update_fas_state(self) -> None:
         t = self.tree
@@ -672,6 +689,9 @@ class Engine:
 
     def advance(self) -> Stats:
         """One additive cycle; stats of the starting iterate (solvers.py:334-399)."""
+        if self.cfg.flavor == "boxmg" and self.thr_next >= self.tree.lmin:
+            self._build_boxmg_level(self.thr_next)  # throttled: one more level per cycle
+            self.thr_next -= 1
         t, cfg = self.tree, self.cfg
         l0, l1 = t.lmin, self.ltop
         b = {l1: self._rhs(l1)}

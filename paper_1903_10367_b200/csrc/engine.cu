@@ -752,6 +752,7 @@ int tmg_create(const tmg_tree* tree, const tmg_config* cfg, tmg_handle** out) {
   if (!(cfg->omega > 0.0 && cfg->omega <= 1.0)) return fail(TMG_EINVAL, "omega must lie in (0, 1]");
   if (!(cfg->omega_hat > 0.0 && cfg->omega_hat < 1.0))
     return fail(TMG_EINVAL, "omega_hat must lie in (0, 1)");
+  if (cfg->throttled) return fail(TMG_EINVAL, "throttled setup is offered for 3D trees (tmg3_create)");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return fail(TMG_ECUDA, "no CUDA device: the engine has no CPU fallback");
@@ -784,6 +785,8 @@ int tmg3_create(const tmg_tree3* tree, const tmg_config* cfg, tmg_handle** out) 
     return fail(TMG_EINVAL, "multiplicative-v10 (dense two-grid reference) is not offered on the device");
   if (cfg->flavor != TMG_GEOMETRIC && cfg->flavor != TMG_BOXMG)
     return fail(TMG_EINVAL, "unknown operator flavor");
+  if (cfg->throttled && cfg->flavor != TMG_BOXMG)
+    return fail(TMG_EINVAL, "throttled setup applies to flavor boxmg");
   if (!(cfg->omega > 0.0 && cfg->omega <= 1.0)) return fail(TMG_EINVAL, "omega must lie in (0, 1]");
   if (!(cfg->omega_hat > 0.0 && cfg->omega_hat < 1.0))
     return fail(TMG_EINVAL, "omega_hat must lie in (0, 1)");

@@ -101,6 +101,9 @@ struct Engine3 {
   double* gbuf[2] = {nullptr, nullptr};
   int ffp_tiles = 0, ffp_chunk = 0, ffp_blocks = 0;
   std::map<int, cudaGraphExec_t> gcache;
+  // throttled BoxMG setup: next level to receive BoxMG P + Galerkin rows (< lmin: done)
+  int thr_next = -1;
+  int* deg = nullptr;
 };
 
 namespace {
@@ -615,6 +618,43 @@ Op3 element_op(double c, bool is_const, const double* coef) {
   return o;
 }
 
+// BoxMG P and Galerkin rows of level l from level l+1's operator (solvers.py:227-250):
+// P[l] and tbl[l] are rewritten in place, so captured graphs stay valid
+int boxmg_level(Engine3* e, int l) {
+  Lvl3& c = e->L[l];
+  Lvl3& f = e->L[l + 1];
+  const Rows raw = (l + 1 == e->ltop) ? Rows{f.N, nullptr, f.coef} : Rows{f.N, f.tbl, nullptr};
+  const int nc = c.N - 1;
+  k3_p_init<<<nblk(c.nv), 256, 0, e->s>>>(c.P, c.nv);
+  CKL3();
+  for (int ax = 0; ax < 3; ++ax) {
+    k3_edges<<<nblk((size_t)nc * c.N * c.N, 128), 128, 0, e->s>>>(c.P, nc, ax, raw, e->deg);
+    CKL3();
+  }
+  for (int nx = 0; nx < 3; ++nx) {
+    k3_faces<<<nblk((size_t)c.N * nc * nc, 128), 128, 0, e->s>>>(c.P, nc, nx, raw);
+    CKL3();
+  }
+  k3_cells<<<nblk((size_t)nc * nc * nc, 128), 128, 0, e->s>>>(c.P, nc, raw);
+  CKL3();
+  k3_assemble<<<nblk(c.nv), 256, 0, e->s>>>(c.tbl, Rows{c.N, nullptr, c.coef});
+  CKL3();
+  if (c.N > 2) {
+    const size_t ni = (size_t)(c.N - 2) * (c.N - 2) * (c.N - 2);
+    k3_rap<<<nblk(ni, 128), 128, 0, e->s>>>(c.tbl, nc, c.P, raw);
+    CKL3();
+  }
+  return TMG_OK;
+}
+
+int check_degenerate(Engine3* e) {
+  int hdeg = 0;
+  CK3(cudaMemcpyAsync(&hdeg, e->deg, sizeof(int), cudaMemcpyDeviceToHost, e->s));
+  CK3(cudaStreamSynchronize(e->s));
+  if (hdeg) return fail3(e, TMG_EDEGENERATE, "degenerate collapsed stencil in face-point solve");
+  return TMG_OK;
+}
+
 int build(Engine3* e, const tmg_tree3* t) {
   const tmg_config& cfg = e->cfg;
   if (t->lmin < 1) return fail3(e, TMG_EINVAL, "lmin must be at least 1");
@@ -656,8 +696,8 @@ int build(Engine3* e, const tmg_tree3* t) {
   CK3(cudaFuncSetAttribute(k3_top2<OP_CONST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2TopSmem));
   CK3(cudaFuncSetAttribute(k3_top2<OP_ELEMENT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2TopSmem));
   CK3(cudaFuncSetAttribute(k3_smooth2r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2RSmemV));
-  int* deg;
-  TRY3(alloc3(e, &deg, 1));
+  TRY3(alloc3(e, &e->deg, 1));
+  e->thr_next = l0 - 1;
   if (cfg.flavor == TMG_GEOMETRIC) {
     for (int l = l0; l <= l1; ++l) {
       Lvl3& c = e->L[l];
@@ -672,36 +712,23 @@ int build(Engine3* e, const tmg_tree3* t) {
     double v;
     TRY3(const_of(e, top.coef, top.ncell, &kc, &v));
     top.op = element_op(v, kc, top.coef);
-    Rows raw{top.N, nullptr, top.coef};
     for (int l = l1 - 1; l >= l0; --l) {
       Lvl3& c = e->L[l];
-      const int nc = c.N - 1;
       TRY3(alloc3(e, &c.P, 125 * c.nv, false));
-      k3_p_init<<<nblk(c.nv), 256, 0, e->s>>>(c.P, c.nv);
-      CKL3();
-      for (int ax = 0; ax < 3; ++ax) {
-        k3_edges<<<nblk((size_t)nc * c.N * c.N, 128), 128, 0, e->s>>>(c.P, nc, ax, raw, deg);
-        CKL3();
-      }
-      for (int nx = 0; nx < 3; ++nx) {
-        k3_faces<<<nblk((size_t)c.N * nc * nc, 128), 128, 0, e->s>>>(c.P, nc, nx, raw);
-        CKL3();
-      }
-      k3_cells<<<nblk((size_t)nc * nc * nc, 128), 128, 0, e->s>>>(c.P, nc, raw);
-      CKL3();
       TRY3(alloc3(e, &c.tbl, 27 * c.nv, false));
-      k3_assemble<<<nblk(c.nv), 256, 0, e->s>>>(c.tbl, Rows{c.N, nullptr, c.coef});
-      CKL3();
-      if (c.N > 2) {
-        const size_t ni = (size_t)(c.N - 2) * (c.N - 2) * (c.N - 2);
-        k3_rap<<<nblk(ni, 128), 128, 0, e->s>>>(c.tbl, nc, c.P, raw);
+      if (cfg.throttled) {  // d-linear P, rediscretised rows; upgraded one level per cycle
+        k3_p_dlinear<<<nblk(c.nv), 256, 0, e->s>>>(c.P, c.N);
         CKL3();
+        k3_assemble<<<nblk(c.nv), 256, 0, e->s>>>(c.tbl, Rows{c.N, nullptr, c.coef});
+        CKL3();
+      } else {
+        TRY3(boxmg_level(e, l));
       }
       c.op = Op3{};
       c.op.kind = OP_TABLE;
       c.op.tbl = c.tbl;
-      raw = Rows{c.N, c.tbl, nullptr};
     }
+    if (cfg.throttled) e->thr_next = l1 - 1;
   }
   {  // row-padded copy of the finest level's cell coefficients for the TMA-staged top kernel
     Lvl3& top = e->L[l1];
@@ -712,10 +739,7 @@ int build(Engine3* e, const tmg_tree3* t) {
                             sizeof(double) * n, (size_t)n * n, cudaMemcpyDeviceToDevice, e->s));
     }
   }
-  int hdeg = 0;
-  CK3(cudaMemcpyAsync(&hdeg, deg, sizeof(int), cudaMemcpyDeviceToHost, e->s));
-  CK3(cudaStreamSynchronize(e->s));
-  if (hdeg) return fail3(e, TMG_EDEGENERATE, "degenerate collapsed stencil in face-point solve");
+  TRY3(check_degenerate(e));
 
   // counts (solvers.py:449-459)
   long long sum = 0, lt = 0, gt = 0;
@@ -1017,6 +1041,12 @@ int e3_shard(Engine3* e, int ls, const int32_t* lo, const int32_t* hi, std::stri
 int e3_phase(Engine3* e, int phase, int level, std::string& err) {
   ErrScope es(e, err);
   if (!e->sharded) return fail3(e, TMG_EINVAL, "handle is not sharded (tmg3_shard)");
+  if (phase == TMG_PH_DOWN && level == e->ltop && e->thr_next >= e->lmin) {
+    // throttled setup at the start of a sharded cycle; every rank holds the full operators
+    TRY3(boxmg_level(e, e->thr_next));
+    TRY3(check_degenerate(e));
+    --e->thr_next;
+  }
   return phase3(e, phase, level);
 }
 
@@ -1059,6 +1089,11 @@ int e3_history(Engine3* e, int count, tmg_stats* out, std::string& err) {
 // one cycle from the graph of the current state (+ the fused-pass state machine)
 int launch_cycle(Engine3* e) {
   TRY3(ensure_graph(e));
+  if (e->thr_next >= e->lmin) {  // throttled setup: one more BoxMG level before this cycle
+    TRY3(boxmg_level(e, e->thr_next));
+    TRY3(check_degenerate(e));
+    --e->thr_next;
+  }
   const bool applied = e->fpend;
   CK3(cudaGraphLaunch(e->gexec, e->s));
   if (e->ffp) ffp_advance(e, applied);

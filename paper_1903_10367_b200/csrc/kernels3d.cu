@@ -519,6 +519,27 @@ __global__ void k3_p_init(double* P, size_t nvc) {
   for (int s = 0; s < 125; ++s) P[(size_t)s * nvc + v] = (s == 62) ? 1.0 : 0.0;
 }
 
+// d-linear weights in the BoxMG P layout (mg3d.dlinear_p_table): ((w_a w_b) w_c),
+// w_o = max(0, 1 - |o|/3), zero where the fine offset leaves the grid -- the
+// starting P of the throttled setup
+__global__ void k3_p_dlinear(double* P, int Nc) {
+  const size_t nvc = (size_t)Nc * Nc * Nc;
+  const size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nvc) return;
+  const int K = (int)(v % Nc), J = (int)((v / Nc) % Nc), I = (int)(v / ((size_t)Nc * Nc));
+  const int nf = 3 * (Nc - 1);
+  for (int a = -2; a <= 2; ++a)
+    for (int b = -2; b <= 2; ++b)
+      for (int c = -2; c <= 2; ++c) {
+        const int fi = 3 * I + a, fj = 3 * J + b, fk = 3 * K + c;
+        const bool in = fi >= 0 && fi <= nf && fj >= 0 && fj <= nf && fk >= 0 && fk <= nf;
+        const double wa = fmax(0.0, 1.0 - (double)abs(a) / 3.0);
+        const double wb = fmax(0.0, 1.0 - (double)abs(b) / 3.0);
+        const double wc = fmax(0.0, 1.0 - (double)abs(c) / 3.0);
+        P[(size_t)pslot(a, b, c) * nvc + v] = in ? (wa * wb) * wc : 0.0;
+      }
+}
+
 __device__ __forceinline__ double pget(const double* P, int Nc, int I, int J, int K, int a, int b, int c) {
   if (a < -2 || a > 2 || b < -2 || b > 2 || c < -2 || c > 2) return 0.0;
   const size_t nvc = (size_t)Nc * Nc * Nc;

@@ -48,6 +48,9 @@ class SolverConfig:
     omega_hat: float = 0.7
     rtilde_true_operator: bool = False
     damping_scale: float = 1.0
+    # BoxMG, 3D: d-linear start, BoxMG P + Galerkin rows one level per cycle
+    # (the paper's throttled setup; not in the reference, which builds eagerly)
+    throttled: bool = False
 
     def __post_init__(self):
         if self.variant not in VARIANTS:
@@ -181,7 +184,8 @@ class GpuEngine:
         return _abi.Config(_abi.VARIANT_IDS[c.variant], _abi.FLAVOR_IDS[c.flavor], float(c.omega),
                            math.nan if c.omega_tilde is None else float(c.omega_tilde),
                            float(c.omega_hat), float(c.damping_scale),
-                           1 if c.rtilde_true_operator else 0, int(self.device))
+                           1 if c.rtilde_true_operator else 0, int(self.device),
+                           1 if getattr(c, "throttled", False) else 0)
 
     def _create(self) -> None:
         L = _abi.lib()

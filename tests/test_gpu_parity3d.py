@@ -143,6 +143,36 @@ def test_3d_fused_fine_pass_equals_unfused(variant, monkeypatch):
     assert np.array_equal(wl1.tree.u[4], wl2.tree.u[4])
 
 
+@pytest.mark.parametrize("name,variant", [("config5-small", "adafac-jac"), ("config5-L4", "adafac-jac"),
+                                          ("config5-L4", "additive"), ("config5-L4", "bpx")])
+def test_3d_throttled_setup_bitwise(name, variant):
+    """Throttled BoxMG setup (one level per cycle, finest first) equals the oracle bitwise;
+    once every level is upgraded the P and Galerkin tables equal the eager build's."""
+    wl = workloads.by_name(name)
+    top, lmin = wl.tree.depth, wl.tree.lmin
+    n = top - lmin + 2
+    t, e, oh = oracle_run(wl, n, variant, throttled=True)
+    eng, h = gpu_run(wl, n, variant, throttled=True)
+    check(wl, eng, h, t, e, oh)
+    _, e_eager, _ = oracle_run(workloads.by_name(name), 0, variant)
+    for l in range(lmin, top):
+        assert np.array_equal(eng.transfers[l].p_table, e_eager.tr[l].p), f"P level {l}"
+        got = eng.ops[l].table().reshape(e_eager.ops[l].tbl.shape)
+        assert np.array_equal(got, e_eager.ops[l].tbl), f"A level {l}"
+
+
+def test_3d_throttled_rebuild_restarts():
+    wl = workloads.by_name("config5-small")
+    eng, h1 = gpu_run(wl, 3, throttled=True)
+    wl2 = workloads.by_name("config5-small")
+    eng2, _ = gpu_run(wl2, 0, throttled=True)
+    for l in range(len(wl2.tree.u)):
+        eng.tree.u[l][...] = wl2.tree.u[l]
+    eng.rebuild()
+    h2 = eng.advance_many(3)
+    np.testing.assert_allclose([s.l2h for s in h2], [s.l2h for s in h1], rtol=1e-13)
+
+
 def test_3d_error_paths_raise_like_the_reference():
     import ctypes as C
 
@@ -150,6 +180,8 @@ def test_3d_error_paths_raise_like_the_reference():
     wl = workloads.config5(levels=2, block=3)
     with pytest.raises(ValueError):
         GpuEngine(wl.tree, SolverConfig(variant="multiplicative-v10", flavor="boxmg"))
+    with pytest.raises(ValueError, match="throttled"):
+        GpuEngine(wl.tree, SolverConfig(variant="adafac-jac", flavor="geometric", throttled=True))
     with pytest.raises(ValueError, match="rtilde_true_operator"):
         GpuEngine(wl.tree, SolverConfig(variant="adafac-jac", flavor="boxmg", rtilde_true_operator=True))
     wl = workloads.config5(levels=3)

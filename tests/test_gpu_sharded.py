@@ -21,21 +21,21 @@ from paper_1903_10367_b200 import GpuEngine, SolverConfig, sharding, workloads
 pytestmark = pytest.mark.gpu
 
 
-def serial(wl, n, variant):
-    eng = GpuEngine(wl.tree, SolverConfig(variant=variant, flavor=wl.flavor), sync="lazy")
+def serial(wl, n, variant, **kw):
+    eng = GpuEngine(wl.tree, SolverConfig(variant=variant, flavor=wl.flavor, **kw), sync="lazy")
     eng.rhs.update(wl.rhs)
     h = eng.advance_many(n)
     eng.pull()
     return h
 
 
-def sharded_local(mk, world, n, variant):
+def sharded_local(mk, world, n, variant, **kw):
     wl0 = mk()
     pl = sharding.plan(wl0.tree.depth, world)
     shards, wls = [], []
     for r in range(world):
         wl = mk()
-        eng = GpuEngine(wl.tree, SolverConfig(variant=variant, flavor=wl.flavor), sync="lazy")
+        eng = GpuEngine(wl.tree, SolverConfig(variant=variant, flavor=wl.flavor, **kw), sync="lazy")
         eng.rhs.update(wl.rhs)
         eng._flush_rhs()
         shards.append(sharding.GpuShard(eng, pl, r))
@@ -65,6 +65,19 @@ def test_gpu_sharded_equals_serial(world, name, variant):
             assert np.array_equal(wls[r].tree.u[l][lo:hi], wl.tree.u[l][lo:hi]), f"rank {r} level {l}"
         for l in range(wl.tree.lmin, pl.ls):
             assert np.array_equal(wls[r].tree.u[l], wl.tree.u[l]), f"rank {r} replicated level {l}"
+
+
+def test_gpu_sharded_throttled_equals_serial():
+    """Throttled setup in the sharded schedule: the level upgrade runs at the top DOWN phase."""
+    mk = lambda: workloads.by_name("config5-L4")  # noqa: E731
+    wl = mk()
+    n = 5
+    hs = serial(wl, n, "adafac-jac", throttled=True)
+    pl, wls, shards, h = sharded_local(mk, 2, n, "adafac-jac", throttled=True)
+    np.testing.assert_allclose([s.l2h for s in h], [s.l2h for s in hs], rtol=1e-13)
+    for r in range(2):
+        lo, hi = pl.rng(wl.tree.depth, r)
+        assert np.array_equal(wls[r].tree.u[wl.tree.depth][lo:hi], wl.tree.u[wl.tree.depth][lo:hi])
 
 
 def test_gpu_dist_transport_world1_nccl():

@@ -163,7 +163,7 @@ def test_galerkin_equals_ptap():
     np.testing.assert_allclose(r1[1:-1, 1:-1, 1:-1], t3[1:-1, 1:-1, 1:-1], atol=1e-13)
 
 
-def make(L, flavor, variant="adafac-jac", blocks=False, seed=0, ds=1.0):
+def make(L, flavor, variant="adafac-jac", blocks=False, seed=0, ds=1.0, throttled=False):
     t = m.Tree(L)
     rng = np.random.default_rng(seed)
     n = 3**L
@@ -171,7 +171,7 @@ def make(L, flavor, variant="adafac-jac", blocks=False, seed=0, ds=1.0):
         blk = 3 ** max(L - 3, 0)
         b = 10.0 ** rng.uniform(-2, 2, (n // blk,) * 3)
         t.eps[L] = np.kron(b, np.ones((blk,) * 3))
-    eng = m.Engine(t, m.Config(variant=variant, flavor=flavor, damping_scale=ds))
+    eng = m.Engine(t, m.Config(variant=variant, flavor=flavor, damping_scale=ds, throttled=throttled))
     f = rng.uniform(-1, 1, (n - 1,) * 3)
     rhs = np.zeros((n + 1,) * 3)
     rhs[1:-1, 1:-1, 1:-1] = (3.0 ** -L) ** 3 * f
@@ -225,3 +225,35 @@ def test_cycle_converges_and_counts(flavor):
     dofs = {l: (3**l - 1) ** 3 for l in range(1, 4)}
     assert h[0].dofs == dofs[3]
     assert h[0].updates == sum(dofs.values()) + dofs[1] + dofs[2]
+
+
+def test_throttled_setup_reaches_the_eager_operators():
+    """Throttled BoxMG: cycle 1 already uses BoxMG on the level
+    below the top; after top - lmin cycles every P and Galerkin table equals the
+    eager build bitwise and the two runs converge alike."""
+    t1, e1 = make(3, "boxmg", "adafac-jac", blocks=True)
+    t2, e2 = make(3, "boxmg", "adafac-jac", blocks=True, throttled=True)
+    # before any cycle: d-linear P and rediscretised rows on every coarse level
+    for l in (1, 2):
+        assert np.array_equal(e2.tr[l].p, m.dlinear_p_table(3**l))
+        assert np.array_equal(e2.ops[l].tbl, m.assemble_table(e2.coef[l]))
+    h1 = [e1.advance().l2h for _ in range(12)]
+    h2 = [e2.advance().l2h for _ in range(12)]
+    assert h2[0] == h1[0]  # stats of the starting iterate
+    assert h2[1] != h1[1]  # level 1 is still d-linear in cycle 1
+    for l in (1, 2):
+        assert np.array_equal(e1.tr[l].p, e2.tr[l].p)
+        assert np.array_equal(e1.ops[l].tbl, e2.ops[l].tbl)
+    assert h2[-1] < 0.1 * h2[0]
+    np.testing.assert_allclose(h2[-1], h1[-1], rtol=0.5)
+
+
+def test_dlinear_p_table_equals_dlinear_prolongation():
+    """The d-linear weights in the P layout prolong like the separable transfer."""
+    nc = 3
+    rng = np.random.default_rng(3)
+    xc = np.zeros((nc + 1,) * 3)
+    xc[1:-1, 1:-1, 1:-1] = rng.standard_normal((nc - 1,) * 3)
+    a = m.Transfer(nc, None, 0.6).prolong(xc)
+    b = m.Transfer(nc, m.dlinear_p_table(nc), 0.6).prolong(xc)
+    np.testing.assert_allclose(a, b, rtol=0, atol=1e-14)
