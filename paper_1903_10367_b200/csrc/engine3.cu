@@ -331,6 +331,28 @@ const bool kUseTma = [] {
   return !(v && v[0] == '0');
 }();
 
+// BoxMG prolongation: tiled cube kernel (TMG_UPT=0: the cell-owned k3_up_cell)
+const bool kUseUpTile = [] {
+  const char* v = std::getenv("TMG_UPT");
+  return !(v && v[0] == '0');
+}();
+
+int launch_up_boxmg(Engine3* e, int l, const Up3& a) {
+  if (!kUseUpTile) {
+    LAUNCH3(kname("k3_up", l), k3_up_cell<true>, e->L[l - 1].u_grid, 128, a);
+    return TMG_OK;
+  }
+  const int nc = a.Nc - 1;
+  const int tiles = ((nc + kUX - 1) / kUX) * ((nc + kUY - 1) / kUY);
+  const int Ilo = a.ilo / 3, Ihi = std::min(nc, (a.ihi + 2) / 3);
+  const int planes = std::max(1, Ihi - Ilo);
+  const int nch = std::max(1, std::min((148 * 16 + tiles - 1) / tiles, std::max(1, planes / 2)));
+  const int chunk = (planes + nch - 1) / nch;
+  const dim3 grid(tiles, (planes + chunk - 1) / chunk);
+  LAUNCH3(kname("k3_up", l), k3_up_tile, grid, dim3(kUX, kUY), a, chunk);
+  return TMG_OK;
+}
+
 Top3 make_top(Engine3* e, int l) {
   Lvl3& c = e->L[l];
   Top3 a{};
@@ -503,7 +525,7 @@ int enqueue_cycle_ffp(Engine3* e, bool apply) {
   LAUNCH3("k3_chain", k3_chain, 1, kChainBlock, ch);
   for (int l = e->lc + 1; l <= e->ltop - 1; ++l) {
     Up3 a = make_up(e, l);
-    LAUNCH3(kname("k3_up", l), k3_up_cell<true>, e->L[l - 1].u_grid, 128, a);
+    TRY3(launch_up_boxmg(e, l, a));
   }
   return TMG_OK;
 }
@@ -521,7 +543,7 @@ void ffp_advance(Engine3* e, bool applied) {
 int ffp_flush(Engine3* e) {
   if (!e->ffp || !e->fpend) return TMG_OK;
   Up3 a = make_up(e, e->ltop);  // u = current buffer, g = latest d
-  LAUNCH3(kname("k3_up", e->ltop), k3_up_cell<true>, e->L[e->ltop - 1].u_grid, 128, a);
+  TRY3(launch_up_boxmg(e, e->ltop, a));
   e->fpend = false;
   return TMG_OK;
 }
@@ -536,7 +558,7 @@ int enqueue_cycle(Engine3* e) {
     Up3 a = make_up(e, l);
     const int g = e->L[l - 1].u_grid;
     if (pi) LAUNCH3(kname("k3_up", l), k3_up, e->L[l].grid, blk, a);
-    else if (boxmg) LAUNCH3(kname("k3_up", l), k3_up_cell<true>, g, 128, a);
+    else if (boxmg) TRY3(launch_up_boxmg(e, l, a));
     else LAUNCH3(kname("k3_up", l), k3_up_cell<false>, g, 128, a);
   }
   return TMG_OK;
@@ -963,7 +985,7 @@ int phase3(Engine3* e, int phase, int l) {
         Up3 a = make_up(e, q);
         const int g = e->L[q - 1].u_grid;
         if (pi) LAUNCH3(kname("k3_up", q), k3_up, e->L[q].grid, blk, a);
-        else if (boxmg) LAUNCH3(kname("k3_up", q), k3_up_cell<true>, g, 128, a);
+        else if (boxmg) TRY3(launch_up_boxmg(e, q, a));
         else LAUNCH3(kname("k3_up", q), k3_up_cell<false>, g, 128, a);
       }
       e->host_counter++;
@@ -981,7 +1003,7 @@ int phase3(Engine3* e, int phase, int l) {
       if (pi) {
         const dim3 blk(kTX, kTY, kTZ);
         LAUNCH3(kname("k3_up", l), k3_up, e->L[l].grid, blk, a);
-      } else if (boxmg) LAUNCH3(kname("k3_up", l), k3_up_cell<true>, g, 128, a);
+      } else if (boxmg) TRY3(launch_up_boxmg(e, l, a));
       else LAUNCH3(kname("k3_up", l), k3_up_cell<false>, g, 128, a);
       return TMG_OK;
     }

@@ -12,9 +12,11 @@
 // * k3_down_c      coarse-level down sweep: operator apply + FAS RHS +
 //                  Jacobi + adaFACx damping; R and R~ share one pass over
 //                  the 124 BoxMG weight planes (each weight loaded once).
-// * k3_up_cell     prolongation owned by coarse cells: thread (W, ri, rj)
-//                  updates fine vertices 3W + (ri, rj, 0..2), reading every P
-//                  weight exactly once with warp-coalesced plane loads.
+// * k3_up_tile     BoxMG prolongation: thread (J, K) marches coarse cells I
+//                  and updates the 27 fine vertices of each cube, every P
+//                  weight read once with warp-coalesced plane loads, slots
+//                  compile-time (k3_up_cell, the grid-stride cell-owned
+//                  version, serves the d-linear flavour and TMG_UPT=0).
 // Variants measured and dropped (config 5, L6): 1-row register / shared
 // windows for the top kernel (6.3 / 4.8 ms vs 4.4), 2-row register window for
 // the top kernel (spills, 7.2 ms), warp-staged coalesced prolongation rows
@@ -707,6 +709,91 @@ __global__ void __launch_bounds__(128) k3_up_cell(const __grid_constant__ Up3 a)
         a.ul[lc][vid(a.Nl[lc], ii, jj, kk)] = un;
       }
     }
+  }
+}
+
+// BoxMG prolongation, tiled: thread (J, K) owns the coarse cell column (., J, K)
+// and marches the cells I of a chunk; per step it updates the 27 fine vertices
+// 3(I, J, K) + (ri, rj, rk), each of the cube's 124 P weights read once (warp
+// along K: coalesced plane loads), the eight coarse carry corners held in
+// registers (plane I+1 becomes plane I of the next step).  The (ri, rj, rk)
+// loops are unrolled, so slots and skips are compile-time: no divisions and no
+// per-vertex branching.  Same DAG as k3_up_cell (corner order d = 7..0).
+constexpr int kUX = 32, kUY = 4;
+
+// (6 CTAs / SM: 80 registers; measured on config 5 L6 against 1, 4, 8, 12 and a
+// three-threads-per-cube split: 5.0 ms vs 9.3 / 7.0 / 5.3 / 6.2 / 5.3+)
+__global__ void __launch_bounds__(kUX * kUY, 6) k3_up_tile(const __grid_constant__ Up3 a, int chunk) {
+  const int Nc = a.Nc, nc = Nc - 1, N = a.N;
+  const int tilesK = (nc + kUX - 1) / kUX;
+  const int K = (blockIdx.x % tilesK) * kUX + threadIdx.x;
+  const int J = (blockIdx.x / tilesK) * kUY + threadIdx.y;
+  if (K >= nc || J >= nc) return;
+  const int Ilo = a.ilo / 3, Ihi = min(nc, (a.ihi + 2) / 3);
+  const int Ia = Ilo + blockIdx.y * chunk, Ib = min(Ihi, Ia + chunk);
+  if (Ia >= Ib) return;
+  const size_t NcNc = (size_t)Nc * Nc, nvc = NcNc * Nc, NN = (size_t)N * N;
+  const double* __restrict__ P = a.P;
+  const double* __restrict__ cc = a.carry_c;
+  const double* __restrict__ g = a.g;
+  double* __restrict__ u = a.u;
+  double* __restrict__ carry = a.carry;
+  double c0[2][2], c1[2][2];
+  {
+    const size_t w = ((size_t)Ia * Nc + J) * Nc + K;
+#pragma unroll
+    for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+      for (int dk = 0; dk < 2; ++dk) c0[dj][dk] = __ldg(cc + w + dj * Nc + dk);
+  }
+  for (int I = Ia; I < Ib; ++I) {
+    const size_t wb = ((size_t)I * Nc + J) * Nc + K;
+#pragma unroll
+    for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+      for (int dk = 0; dk < 2; ++dk) c1[dj][dk] = __ldg(cc + wb + NcNc + dj * Nc + dk);
+    const size_t vb = ((size_t)(3 * I) * N + 3 * J) * N + 3 * K;
+#pragma unroll
+    for (int ri = 0; ri < 3; ++ri) {
+      const int i = 3 * I + ri;
+      if (i < a.ilo || i >= a.ihi) continue;
+#pragma unroll
+      for (int rj = 0; rj < 3; ++rj) {
+        if (rj == 0 && J == 0) continue;
+#pragma unroll
+        for (int rk = 0; rk < 3; ++rk) {
+          if (rk == 0 && K == 0) continue;
+          double acc = 0.0;
+#pragma unroll
+          for (int d = 7; d >= 0; --d) {
+            const int di = (d >> 2) & 1, dj = (d >> 1) & 1, dk = d & 1;
+            if ((di && !ri) || (dj && !rj) || (dk && !rk)) continue;
+            const int sl = pslot(ri - 3 * di, rj - 3 * dj, rk - 3 * dk);
+            const double wt = (sl == 62) ? 1.0 : __ldg(P + (size_t)sl * nvc + wb + di * NcNc + dj * Nc + dk);
+            acc = acc + wt * (di ? c1[dj][dk] : c0[dj][dk]);
+          }
+          const size_t v = vb + ri * NN + rj * N + rk;
+          const double c = acc + __ldg(g + v);
+          if (carry) carry[v] = c;
+          const double un = u[v] + c;
+          u[v] = un;
+          if (ri == 0 && rj == 0 && rk == 0) {  // FAS walk-down injection
+            int ii = I, jj = J, kk = K;
+            for (int lc = a.l - 1; lc >= a.l0; --lc) {
+              a.ul[lc][vid(a.Nl[lc], ii, jj, kk)] = un;
+              if (ii % 3 || jj % 3 || kk % 3) break;
+              ii /= 3;
+              jj /= 3;
+              kk /= 3;
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+      for (int dk = 0; dk < 2; ++dk) c0[dj][dk] = c1[dj][dk];
   }
 }
 
