@@ -15,6 +15,7 @@
 #include "kernels3d.cu"
 #include "kernels3d_fast.cu"
 #include "kernels3d_ffp.cu"
+#include "kernels3d_ffp4.cu"
 
 namespace {
 
@@ -102,6 +103,7 @@ struct Engine3 {
   int ffp_tiles = 0, ffp_chunk = 0, ffp_blocks = 0;
   std::map<int, cudaGraphExec_t> gcache;
   // throttled BoxMG setup: next level to receive BoxMG P + Galerkin rows (< lmin: done)
+  bool ffp4 = false;  // version-4 fused pass (TMA plane sets, partial-sum smoothing)
   int thr_next = -1;
   int* deg = nullptr;
 };
@@ -325,6 +327,27 @@ bool cell_tmap(CUtensorMap* map, const double* base, int n) {
                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Generic 3D tensor map over fp64 data (dims innermost first, byte strides of dims 1, 2).
+bool tmap3(CUtensorMap* map, const double* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
+           uint64_t s2, uint32_t b0, uint32_t b1, uint32_t b2) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }();
+  if (!encode || !base) return false;
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {s1, s2};
+  const cuuint32_t box[3] = {b0, b1, b2};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // TMA staging of the streaming kernels' vertex planes (TMG_TMA=0: cp.async)
 const bool kUseTma = [] {
   const char* v = std::getenv("TMG_TMA");
@@ -476,12 +499,40 @@ Ffp3 make_ffp(Engine3* e, bool apply) {
   return a;
 }
 
+int make_ffp4(Engine3* e, bool apply, Ffp4* A) {
+  *A = Ffp4{};
+  A->f = make_ffp(e, apply);
+  const Ffp3& f = A->f;
+  const uint64_t N = (uint64_t)f.N, Nc = (uint64_t)f.Nc, n = N - 1, np = n + (n & 1);
+  bool ok = tmap3(&A->tu, f.u_in, N, N, N, N * 8, N * N * 8, k4U, k4U, 1);
+  if (apply) {
+    ok = ok && tmap3(&A->tg, f.g_in, N, N, N, N * 8, N * N * 8, k4U, k4U, 1);
+    ok = ok && tmap3(&A->tk, f.carry_c, Nc, Nc, Nc, Nc * 8, Nc * Nc * 8, k4K, k4K, 2);
+  }
+  if (f.op.kind == OP_ELEMENT)
+    ok = ok && tmap3(&A->tc, e->L[e->ltop].coefp, n, n, n, np * 8, np * n * 8, k4U, k4U, 1);
+  if (f.rhs) ok = ok && tmap3(&A->th, f.rhs, N, N, N, N * 8, N * N * 8, k4U, k4U, 1);
+  if (!ok) return fail3(e, TMG_ECUDA, "tensor map encoding failed (fused fine pass)");
+  const char* dbg = std::getenv("TMG_FFP4_DBG");
+  A->dbg = dbg ? std::atoi(dbg) : 0;
+  return TMG_OK;
+}
+
 // One cycle with the fused fine pass: FFP (finest level), then the coarse levels.
 int enqueue_cycle_ffp(Engine3* e, bool apply) {
   const bool jac = e->cfg.variant == VAR_JAC;
   const dim3 sblk(kSX, kSY);
-  Ffp3 f = make_ffp(e, apply);
-  {
+  if (e->ffp4) {
+    Ffp4 A;
+    TRY3(make_ffp4(e, apply, &A));
+    cudaEvent_t e0_ = nullptr;
+    TRY3(begin_k(e, &e0_));
+    if (A.f.op.kind == OP_CONST) k3_ffp4<OP_CONST><<<e->ffp_blocks, k4Threads, kFfp4Smem, e->s>>>(A);
+    else k3_ffp4<OP_ELEMENT><<<e->ffp_blocks, k4Threads, kFfp4Smem, e->s>>>(A);
+    CKL3();
+    TRY3(end_k(e, kname("k3_down", e->ltop), e0_));
+  } else {
+    Ffp3 f = make_ffp(e, apply);
     cudaEvent_t e0_ = nullptr;
     TRY3(begin_k(e, &e0_));
     k3_ffp<<<e->ffp_blocks, kFThreads, kFfpSmem, e->s>>>(f);
@@ -818,8 +869,9 @@ int build(Engine3* e, const tmg_tree3* t) {
   {
     // opt-in (TMG_FFP=1) until it beats the phase-by-phase cycle (profiles/r01_ffp_*)
     const char* env = std::getenv("TMG_FFP");
-    const bool want = env && std::strcmp(env, "1") == 0;
+    const bool want = env && (std::strcmp(env, "1") == 0 || std::strcmp(env, "4") == 0);
     e->ffp = want && cfg.flavor == TMG_BOXMG && cfg.variant != VAR_PI && l1 - 1 > e->lc;
+    e->ffp4 = e->ffp && std::strcmp(env, "4") == 0;
     e->fpend = false;
     e->pu = e->pg = 0;
     if (e->ffp) {
@@ -833,9 +885,15 @@ int build(Engine3* e, const tmg_tree3* t) {
       TRY3(alloc3(e, &e->gbuf[1], c.nv));
       TRY3(alloc3(e, &cc.bR, cc.nv));
       TRY3(alloc3(e, &cc.bT, cc.nv));
-      e->ffp_tiles = (c.N - 1 + 3 * kFT - 1) / (3 * kFT);
+      if (e->ffp4) {
+        CK3(cudaFuncSetAttribute(k3_ffp4<OP_CONST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFfp4Smem));
+        CK3(cudaFuncSetAttribute(k3_ffp4<OP_ELEMENT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kFfp4Smem));
+      }
+      const int ft = e->ffp4 ? k4T : kFT;
+      e->ffp_tiles = (c.N - 1 + 3 * ft - 1) / (3 * ft);
       const int t2 = e->ffp_tiles * e->ffp_tiles;
-      int nch = (8 * 148 + t2 - 1) / t2;
+      int nch = ((e->ffp4 ? 148 : 8 * 148) + t2 - 1) / t2;
       nch = std::max(1, std::min(nch, std::max(1, cc.N / 8)));
       e->ffp_chunk = (cc.N + nch - 1) / nch;
       e->ffp_blocks = t2 * ((cc.N + e->ffp_chunk - 1) / e->ffp_chunk);

@@ -119,11 +119,12 @@ def test_3d_fixture_history_and_sha(name):
         assert _sha(wl.tree.u[int(l)]) == sha, f"u level {l}"
 
 
+@pytest.mark.parametrize("ffp", ["1", "4"])
 @pytest.mark.parametrize("variant", ["adafac-jac", "additive", "additive-exp", "bpx", "afacc"])
-def test_3d_fused_fine_pass_equals_unfused(variant, monkeypatch):
+def test_3d_fused_fine_pass_equals_unfused(variant, ffp, monkeypatch):
     """The fused fine pass (pipelined schedule, BoxMG) is bit-identical to the phase-by-phase cycle."""
     n = 5
-    monkeypatch.setenv("TMG_FFP", "1")
+    monkeypatch.setenv("TMG_FFP", ffp)
     wl1 = workloads.by_name("config5-L4")
     e1, h1 = gpu_run(wl1, n, variant)
     monkeypatch.setenv("TMG_FFP", "0")
