@@ -23,6 +23,13 @@ CASES = {
     "skew_boxmg_jac_L4": dict(setup="skew", k=3, variant="adafac-jac", flavor="boxmg", lmax=4,
                               max_cycles=40, target=1e-8),
     "needle_bpx_L3": dict(setup="needle", k=1, variant="bpx", lmax=3, max_cycles=30),
+    # the reference's single-touch engine (pipeline.py), SURVEY.md §8(f) item 4
+    "pipe_poisson_jac_L3": dict(setup="poisson", variant="adafac-jac", lmax=3, max_cycles=15,
+                                target=1e-30, engine="pipelined"),
+    "pipe_halfjump_pi_L3": dict(setup="half-jump", k=2, variant="adafac-pi", lmax=3, max_cycles=10,
+                                target=1e-30, engine="pipelined"),
+    "pipe_skew_boxmg_additive_L3": dict(setup="skew", k=3, variant="additive", flavor="boxmg", lmax=3,
+                                        max_cycles=10, target=1e-30, engine="pipelined"),
 }
 
 

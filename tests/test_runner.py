@@ -3,7 +3,8 @@
 CPU: the configuration checks and the CSV schema of ``treemg.bench``
 (tests/test_bench.py:44-57, 80-89).  GPU: whole runs through GpuEngine
 reproduce the reference's CSV (tests/golden/runs/reference_runs.json, made by
-tests/golden/make_runs.py from ``treemg.bench.run``): same number of reports,
+tests/golden/make_runs.py from ``treemg.bench.run``, including ``pipe_*`` runs of
+the reference's single-touch ``PipelineEngine``): same number of reports,
 same exit status, identical integer columns, normalised residuals within
 1e-12 (d-linear) / 1e-9 (BoxMG) relative.
 """
@@ -30,6 +31,9 @@ def test_config_validation_messages():
         runner.ExperimentConfig(variant="gauss-seidel").validate()
     with pytest.raises(runner.ConfigError, match="engine"):
         runner.ExperimentConfig(engine="gpu").validate()
+    with pytest.raises(runner.ConfigError, match="pipelined"):
+        runner.ExperimentConfig(engine="pipelined", variant="bpx").validate()
+    runner.ExperimentConfig(engine="pipelined", variant="adafac-pi").validate()
     with pytest.raises(runner.ConfigError, match="omega"):
         runner.ExperimentConfig(omega=1.5).validate()
     with pytest.raises(runner.ConfigError, match="amr"):
