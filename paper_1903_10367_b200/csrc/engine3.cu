@@ -16,6 +16,7 @@
 #include "kernels3d_fast.cu"
 #include "kernels3d_ffp.cu"
 #include "kernels3d_ffp4.cu"
+#include "kernels3d_upq.cu"
 
 namespace {
 
@@ -26,6 +27,7 @@ struct Lvl3 {
   size_t nv = 0, ncell = 0;
   double *u = nullptr, *rhs = nullptr, *g = nullptr, *rho = nullptr, *sm = nullptr, *carry = nullptr;
   double *eff = nullptr, *coef = nullptr, *tbl = nullptr, *P = nullptr;
+  double* Pc = nullptr;  // level ltop-1: cube-owned copy of P for the TMA-fed prolongation (k3_up_tma)
   double* coefp = nullptr;  // finest level: coef with rows padded to even length (TMA)
   double *bR = nullptr, *bT = nullptr;  // level ltop-1: restrictions from the fused fine pass
   Op3 op{};
@@ -329,7 +331,8 @@ bool cell_tmap(CUtensorMap* map, const double* base, int n) {
 
 // Generic 3D tensor map over fp64 data (dims innermost first, byte strides of dims 1, 2).
 bool tmap3(CUtensorMap* map, const double* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
-           uint64_t s2, uint32_t b0, uint32_t b1, uint32_t b2) {
+           uint64_t s2, uint32_t b0, uint32_t b1, uint32_t b2,
+           CUtensorMapL2promotion prom = CU_TENSOR_MAP_L2_PROMOTION_L2_128B) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -345,7 +348,7 @@ bool tmap3(CUtensorMap* map, const double* base, uint64_t d0, uint64_t d1, uint6
   const cuuint32_t estr[3] = {1, 1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+                prom, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // TMA staging of the streaming kernels' vertex planes (TMG_TMA=0: cp.async)
@@ -360,7 +363,64 @@ const bool kUseUpTile = [] {
   return !(v && v[0] == '0');
 }();
 
+bool tmap4(CUtensorMap* map, const double* base, const uint64_t d[4], const uint64_t s[3], const uint32_t b[4]) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }();
+  if (!encode || !base) return false;
+  const cuuint64_t dims[4] = {d[0], d[1], d[2], d[3]};
+  const cuuint64_t strides[3] = {s[0], s[1], s[2]};
+  const cuuint32_t box[4] = {b[0], b[1], b[2], b[3]};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+int launch_up_tma(Engine3* e, int l, const Up3& a) {
+  const Lvl3& cc = e->L[l - 1];
+  UpQ A{};
+  A.a = a;
+  const uint64_t N = (uint64_t)a.N, Nc = (uint64_t)a.Nc;
+  const uint64_t nc_ = Nc - 1, Kp = (nc_ + kQK - 1) / kQK * kQK;
+  const uint64_t dp[4] = {nc_, nc_, nc_, (uint64_t)kQS}, sp[3] = {Kp * 8, Kp * nc_ * 8, Kp * nc_ * nc_ * 8};
+  const uint32_t bp[4] = {kQK, kQJ, 1, kQS};
+  bool ok = tmap4(&A.tp, cc.Pc, dp, sp, bp);
+  ok = ok && tmap3(&A.tu, a.u, N, N, N, N * 8, N * N * 8, kQFK, kQFJ, 3, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+  ok = ok && tmap3(&A.tg, a.g, N, N, N, N * 8, N * N * 8, kQFK, kQFJ, 3, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+  ok = ok && tmap3(&A.tc, a.carry_c, Nc, Nc, Nc, Nc * 8, Nc * Nc * 8, kQCK, kQCJ, 2);
+  if (!ok) return fail3(e, TMG_ECUDA, "tensor map encoding failed (k3_up_tma)");
+  const int nc = a.Nc - 1;
+  A.tilesK = (nc + kQK - 1) / kQK;
+  A.nI = nc;
+  A.steps = (long long)A.tilesK * ((nc + kQJ - 1) / kQJ) * nc;
+  const int grid = (int)std::min<long long>(num_sms(), A.steps);
+  A.per = (A.steps + grid - 1) / grid;
+  cudaEvent_t e0_ = nullptr;
+  TRY3(begin_k(e, &e0_));
+  if (a.carry) k3_up_tma<true><<<grid, kQT, kUpTmaSmem, e->s>>>(A);
+  else k3_up_tma<false><<<grid, kQT, kUpTmaSmem, e->s>>>(A);
+  CKL3();
+  TRY3(end_k(e, kname("k3_up", l), e0_));
+  return TMG_OK;
+}
+
 int launch_up_boxmg(Engine3* e, int l, const Up3& a) {
+  if (e->L[l - 1].Pc && !e->sharded && a.ilo == 1 && a.ihi == a.N - 1 && !a.pi) return launch_up_tma(e, l, a);
   if (!kUseUpTile) {
     LAUNCH3(kname("k3_up", l), k3_up_cell<true>, e->L[l - 1].u_grid, 128, a);
     return TMG_OK;
@@ -691,6 +751,16 @@ Op3 element_op(double c, bool is_const, const double* coef) {
   return o;
 }
 
+// the cube-owned copy of level l's P (k3_up_tma), after every change of P
+int refresh_pc(Engine3* e, int l) {
+  Lvl3& c = e->L[l];
+  if (!c.Pc) return TMG_OK;
+  const size_t nc = (size_t)c.N - 1;
+  k3_p_cube<<<nblk(nc * nc * nc, 128), 128, 0, e->s>>>(c.P, c.Pc, c.N, (int)((nc + kQK - 1) / kQK * kQK));
+  CKL3();
+  return TMG_OK;
+}
+
 // BoxMG P and Galerkin rows of level l from level l+1's operator (solvers.py:227-250):
 // P[l] and tbl[l] are rewritten in place, so captured graphs stay valid
 int boxmg_level(Engine3* e, int l) {
@@ -717,7 +787,7 @@ int boxmg_level(Engine3* e, int l) {
     k3_rap<<<nblk(ni, 128), 128, 0, e->s>>>(c.tbl, nc, c.P, raw);
     CKL3();
   }
-  return TMG_OK;
+  return refresh_pc(e, l);
 }
 
 int check_degenerate(Engine3* e) {
@@ -769,6 +839,8 @@ int build(Engine3* e, const tmg_tree3* t) {
   CK3(cudaFuncSetAttribute(k3_top2<OP_CONST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2TopSmem));
   CK3(cudaFuncSetAttribute(k3_top2<OP_ELEMENT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2TopSmem));
   CK3(cudaFuncSetAttribute(k3_smooth2r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2RSmemV));
+  CK3(cudaFuncSetAttribute(k3_up_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpTmaSmem));
+  CK3(cudaFuncSetAttribute(k3_up_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpTmaSmem));
   TRY3(alloc3(e, &e->deg, 1));
   e->thr_next = l0 - 1;
   if (cfg.flavor == TMG_GEOMETRIC) {
@@ -789,9 +861,16 @@ int build(Engine3* e, const tmg_tree3* t) {
       Lvl3& c = e->L[l];
       TRY3(alloc3(e, &c.P, 125 * c.nv, false));
       TRY3(alloc3(e, &c.tbl, 27 * c.nv, false));
+      // BoxMG prolongation of the finest level as a TMA stream (k3_up_tma; TMG_UPQ=0: k3_up_tile)
+      const char* upq = std::getenv("TMG_UPQ");
+      if (l == l1 - 1 && !(upq && upq[0] == '0') && c.N - 1 >= kQK) {
+        const size_t nc = (size_t)c.N - 1, Kp = (nc + kQK - 1) / kQK * kQK;
+        TRY3(alloc3(e, &c.Pc, (size_t)kQS * nc * nc * Kp));
+      }
       if (cfg.throttled) {  // d-linear P, rediscretised rows; upgraded one level per cycle
         k3_p_dlinear<<<nblk(c.nv), 256, 0, e->s>>>(c.P, c.N);
         CKL3();
+        TRY3(refresh_pc(e, l));
         k3_assemble<<<nblk(c.nv), 256, 0, e->s>>>(c.tbl, Rows{c.N, nullptr, c.coef});
         CKL3();
       } else {

@@ -198,3 +198,21 @@ def test_3d_error_paths_raise_like_the_reference():
         _abi.check(L.tmg_get_u(eng._h, 9, None))
     with pytest.raises(ValueError):
         sharding.plan(2, 8)  # too shallow for 8 ranks
+
+
+@pytest.mark.parametrize("variant,throttled", [("adafac-jac", False), ("additive", False), ("adafac-jac", True)])
+def test_3d_prolongation_stream_equals_tile(variant, throttled, monkeypatch):
+    """The TMA-fed finest-level prolongation (k3_up_tma over the cube-owned copy of P;
+    used from depth 5 up) is bit-identical to the per-thread tiled kernel (TMG_UPQ=0),
+    which the depth <= 4 tests pin to the oracle."""
+    n = 4
+    monkeypatch.setenv("TMG_UPQ", "1")
+    wl1 = workloads.by_name("config5-L5")
+    e1, h1 = gpu_run(wl1, n, variant, throttled=throttled)
+    monkeypatch.setenv("TMG_UPQ", "0")
+    wl2 = workloads.by_name("config5-L5")
+    e2, h2 = gpu_run(wl2, n, variant, throttled=throttled)
+    assert [s.l2h for s in h1] == [s.l2h for s in h2]
+    assert [s.linf for s in h1] == [s.linf for s in h2]
+    for l in range(1, 6):
+        assert np.array_equal(wl1.tree.u[l], wl2.tree.u[l]), f"level {l}"
