@@ -454,6 +454,10 @@ Top3 make_top(Engine3* e, int l) {
   a.part_max = e->part_max;
   a.use_tma = kUseTma && vertex_tmap(&a.tm, c.u, c.N);
   if (a.use_tma && c.op.kind == OP_ELEMENT && c.coefp && cell_tmap(&a.tmc, c.coefp, c.N - 1)) a.use_tma = 2;
+  // rhs through TMA as well (TMG_TMA_RHS=0: per-thread loads); needs the vertex-plane TMA path
+  const char* tr = std::getenv("TMG_TMA_RHS");
+  a.rhs_tma = a.use_tma && c.rhs && !(tr && tr[0] == '0') &&
+              tmap3(&a.tmr, c.rhs, c.N, c.N, c.N, (uint64_t)c.N * 8, (uint64_t)c.N * c.N * 8, k2RowR, k2Y, 1);
   return a;
 }
 

@@ -35,6 +35,8 @@ constexpr int kRowC = kSX + 1, kColC = kSY + 1;  // cell plane with halo (cells 
 struct Top3 {
   CUtensorMap tm;          // 3D map of u (box 34 x 18 x 1 doubles), used when use_tma
   CUtensorMap tmc;         // 3D map of the row-padded cell coefficients (box 34 x 17 x 1), use_tma == 2
+  CUtensorMap tmr;         // 3D map of rhs (box 34 x 16 x 1 from k0 - 1: the column's rows), used when rhs_tma
+  int rhs_tma;
   int use_tma;
   int N, ilo, ihi, chunk;  // planes [ilo, ihi) split in chunks
   const double* u;
@@ -299,11 +301,15 @@ struct Column2 {
 // tm != nullptr: the vertex planes arrive by TMA (one bulk tensor copy per
 // plane, completion on bars[slot]); the cell planes keep 8-byte cp.async (their
 // rows are an odd number of doubles, which TMA strides cannot express).
+// rhs slot: the column's 16 rows of one plane, from k0 - 1 (TMA boxes start at 16-byte aligned
+// inner coordinates), 34 wide
+constexpr int k2RowR = kSX + 2, k2SlotR = k2RowR * k2Y;
 template <int S, bool CELLS, class Body>
 __device__ __forceinline__ void stream25x2(const Column2& col, const double* x, const double* e,
                                            double (*us)[k2SlotU], double (*cs)[k2SlotC],
                                            const CUtensorMap* tm, uint64_t* bars, Body&& body,
-                                           const CUtensorMap* tmc = nullptr) {
+                                           const CUtensorMap* tmc = nullptr, const CUtensorMap* tmr = nullptr,
+                                           double (*rs)[k2SlotR] = nullptr) {
   const int ia = col.ia, ib = col.ib;
   if (tm && col.lt == 0) {
     for (int q = 0; q < S; ++q) mbar_init(&bars[q], 1);
@@ -314,9 +320,10 @@ __device__ __forceinline__ void stream25x2(const Column2& col, const double* x, 
     const bool ctma = CELLS && tmc;
     if (tm) {
       if (col.lt == 0) {
-        mbar_expect_tx(&bars[slot], k2BoxBytes + (ctma ? k2BoxBytesC : 0u));
+        mbar_expect_tx(&bars[slot], k2BoxBytes + (ctma ? k2BoxBytesC : 0u) + (tmr ? 8u * k2SlotR : 0u));
         tma_load_3d(us[slot], tm, &bars[slot], col.k0 - 1, col.j0 - 1, ia - 1 + g);
         if (ctma) tma_load_3d(cs[slot], tmc, &bars[slot], col.k0 - 1, col.j0 - 1, ia - 1 + g);
+        if (tmr) tma_load_3d(rs[slot], tmr, &bars[slot], col.k0 - 1, col.j0, ia - 1 + g);
       }
     } else {
       col.stage_v(us[slot], x, ia - 1 + g);
@@ -343,7 +350,7 @@ __device__ __forceinline__ void stream25x2(const Column2& col, const double* x, 
         __syncthreads();
         issue(S - 1 + (i - ia), (u + S - 1) % S);
         body(i, us[u % S], us[(u + 1) % S], us[(u + 2) % S],
-             CELLS ? cs[u % S] : nullptr, CELLS ? cs[(u + 1) % S] : nullptr);
+             CELLS ? cs[u % S] : nullptr, CELLS ? cs[(u + 1) % S] : nullptr, tmr ? rs[(u + 1) % S] : nullptr);
       }
     }
   }
@@ -365,7 +372,7 @@ __device__ __forceinline__ void load_two(const double* pm, const double* p0, con
 }
 
 constexpr int k2TopStages = 5;  // measured: 5 stages beat 8 (occupancy)
-constexpr size_t k2TopSmem = sizeof(double) * k2TopStages * (k2SlotU + k2SlotC);
+constexpr size_t k2TopSmem = sizeof(double) * k2TopStages * (k2SlotU + k2SlotC + k2SlotR);
 
 // Two rows per thread with a register window along i: each plane's 4 x 3
 // neighbourhood of the thread's two vertices is read from shared memory once
@@ -488,6 +495,7 @@ __global__ void __launch_bounds__(kSB, 3) k3_top2(const __grid_constant__ Top3 a
   __shared__ uint64_t bars[k2TopStages];
   auto us = reinterpret_cast<double(*)[k2SlotU]>(dyn2);
   auto cs = reinterpret_cast<double(*)[k2SlotC]>(dyn2 + k2TopStages * k2SlotU);
+  auto rs = reinterpret_cast<double(*)[k2SlotR]>(dyn2 + k2TopStages * (k2SlotU + k2SlotC));
   const Column2 col(a.N, a.ilo, a.ihi, a.chunk);
   const int N = a.N;
   const size_t NN = (size_t)N * N;
@@ -500,11 +508,17 @@ __global__ void __launch_bounds__(kSB, 3) k3_top2(const __grid_constant__ Top3 a
   const CUtensorMap* tmc = (KIND == OP_ELEMENT && a.use_tma == 2) ? &a.tmc : nullptr;
   stream25x2<k2TopStages, KIND == OP_ELEMENT>(col, a.u, a.op.e, us, cs, a.use_tma ? &a.tm : nullptr, bars,
       [&](int i, const double* pm, const double* p0, const double* pp, const double* cm,
-          const double* c0) {
+          const double* c0, const double* r0) {
         if (!ok0) return;
         const size_t v = (size_t)i * NN + col_off;
-        const double rhs0 = a.rhs ? __ldg(a.rhs + v) : 0.0;
-        const double rhs1 = (ok1 && a.rhs) ? __ldg(a.rhs + v + N) : 0.0;
+        double rhs0, rhs1;
+        if (r0) {
+          rhs0 = r0[2 * threadIdx.y * k2RowR + threadIdx.x + 1];
+          rhs1 = r0[(2 * threadIdx.y + 1) * k2RowR + threadIdx.x + 1];
+        } else {
+          rhs0 = a.rhs ? __ldg(a.rhs + v) : 0.0;
+          rhs1 = (ok1 && a.rhs) ? __ldg(a.rhs + v + N) : 0.0;
+        }
         double x0[27], x1[27];
         load_two(pm, p0, pp, xo, x0, x1);
         double au0, dg0, au1 = 0.0, dg1 = 1.0;
@@ -551,17 +565,17 @@ __global__ void __launch_bounds__(kSB, 3) k3_top2(const __grid_constant__ Top3 a
           if (a.rho) a.rho[v + N] = rho1;
         }
       },
-      tmc);
-  __shared__ double rs[kSB / 32], rm[kSB / 32];
+      tmc, a.rhs_tma ? &a.tmr : nullptr, rs);
+  __shared__ double red_s[kSB / 32], red_m[kSB / 32];
   for (int o = 16; o > 0; o >>= 1) {
     s += __shfl_down_sync(0xffffffffu, s, o);
     mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
   }
-  if ((col.lt & 31) == 0) { rs[col.lt >> 5] = s; rm[col.lt >> 5] = mx; }
+  if ((col.lt & 31) == 0) { red_s[col.lt >> 5] = s; red_m[col.lt >> 5] = mx; }
   __syncthreads();
   if (col.lt == 0) {
     double A = 0.0, B = 0.0;
-    for (int q = 0; q < kSB / 32; ++q) { A += rs[q]; B = fmax(B, rm[q]); }
+    for (int q = 0; q < kSB / 32; ++q) { A += red_s[q]; B = fmax(B, red_m[q]); }
     a.part_sum[blockIdx.x] = A;
     a.part_max[blockIdx.x] = B;
   }
