@@ -200,7 +200,8 @@ def test_3d_error_paths_raise_like_the_reference():
         sharding.plan(2, 8)  # too shallow for 8 ranks
 
 
-@pytest.mark.parametrize("variant,throttled", [("adafac-jac", False), ("additive", False), ("adafac-jac", True)])
+@pytest.mark.parametrize("variant,throttled", [("adafac-jac", False), ("additive", False), ("afacc", False),
+                                               ("adafac-jac", True)])
 def test_3d_prolongation_stream_equals_tile(variant, throttled, monkeypatch):
     """The TMA-fed finest-level prolongation (k3_up_tma over the cube-owned copy of P;
     used from depth 5 up) is bit-identical to the per-thread tiled kernel (TMG_UPQ=0),
