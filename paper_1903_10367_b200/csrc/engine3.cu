@@ -27,7 +27,7 @@ struct Lvl3 {
   size_t nv = 0, ncell = 0;
   double *u = nullptr, *rhs = nullptr, *g = nullptr, *rho = nullptr, *sm = nullptr, *carry = nullptr;
   double *eff = nullptr, *coef = nullptr, *tbl = nullptr, *P = nullptr;
-  double* Pc = nullptr;  // level ltop-1: cube-owned copy of P for the TMA-fed prolongation (k3_up_tma)
+  double* Pc = nullptr;  // levels ltop-1, ltop-2: cube-owned copy of P for the TMA-fed prolongation (k3_up_tma)
   double* coefp = nullptr;  // finest level: coef with rows padded to even length (TMA)
   double *bR = nullptr, *bT = nullptr;  // level ltop-1: restrictions from the fused fine pass
   Op3 op{};
@@ -865,9 +865,9 @@ int build(Engine3* e, const tmg_tree3* t) {
       Lvl3& c = e->L[l];
       TRY3(alloc3(e, &c.P, 125 * c.nv, false));
       TRY3(alloc3(e, &c.tbl, 27 * c.nv, false));
-      // BoxMG prolongation of the finest level as a TMA stream (k3_up_tma; TMG_UPQ=0: k3_up_tile)
+      // BoxMG prolongation of the two finest levels as TMA streams (k3_up_tma; TMG_UPQ=0: k3_up_tile)
       const char* upq = std::getenv("TMG_UPQ");
-      if (l == l1 - 1 && !(upq && upq[0] == '0') && c.N - 1 >= kQK) {
+      if (l >= l1 - 2 && !(upq && upq[0] == '0') && c.N - 1 >= kQK) {
         const size_t nc = (size_t)c.N - 1, Kp = (nc + kQK - 1) / kQK * kQK;
         TRY3(alloc3(e, &c.Pc, (size_t)kQS * nc * nc * Kp));
       }
