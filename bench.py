@@ -72,6 +72,8 @@ class Dist:
             import torch.distributed as td
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             if self.nccl:
+                # NCCL's init banner ("NCCL version ...") goes to stdout; rank 0 prints ONE JSON line
+                os.environ.setdefault("NCCL_DEBUG", "WARN")
                 torch.cuda.set_device(self.local)
                 td.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             else:

@@ -406,8 +406,10 @@ int launch_up_tma(Engine3* e, int l, const Up3& a) {
   if (!ok) return fail3(e, TMG_ECUDA, "tensor map encoding failed (k3_up_tma)");
   const int nc = a.Nc - 1;
   A.tilesK = (nc + kQK - 1) / kQK;
-  A.nI = nc;
-  A.steps = (long long)A.tilesK * ((nc + kQJ - 1) / kQJ) * nc;
+  A.I0 = a.ilo / 3;
+  A.nI = std::max(0, std::min(nc, (a.ihi + 2) / 3) - A.I0);
+  if (A.nI == 0) return TMG_OK;
+  A.steps = (long long)A.tilesK * ((nc + kQJ - 1) / kQJ) * A.nI;
   const int grid = (int)std::min<long long>(num_sms(), A.steps);
   A.per = (A.steps + grid - 1) / grid;
   cudaEvent_t e0_ = nullptr;
@@ -420,7 +422,7 @@ int launch_up_tma(Engine3* e, int l, const Up3& a) {
 }
 
 int launch_up_boxmg(Engine3* e, int l, const Up3& a) {
-  if (e->L[l - 1].Pc && !e->sharded && a.ilo == 1 && a.ihi == a.N - 1 && !a.pi) return launch_up_tma(e, l, a);
+  if (e->L[l - 1].Pc && !a.pi) return launch_up_tma(e, l, a);
   if (!kUseUpTile) {
     LAUNCH3(kname("k3_up", l), k3_up_cell<true>, e->L[l - 1].u_grid, 128, a);
     return TMG_OK;

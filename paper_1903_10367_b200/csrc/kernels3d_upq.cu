@@ -17,8 +17,9 @@
 //     u, g box {96, 6, 3}       the 27 fine vertices of each cube
 //     carry_c box {34, 3, 2}    the coarse corners
 //   u is updated in place in its slot and written back with one TMA store
-//   (cp.async.bulk.tensor shared -> global); boundary positions in the box are
-//   never modified, so storing them back is a no-op.
+//   (cp.async.bulk.tensor shared -> global); boundary positions in the box, and
+//   under slab sharding the fine planes outside the rank's [ilo, ihi), are never
+//   modified, so storing them back is a no-op.
 //
 // Per fine vertex the DAG is k3_up_tile's (corner order d = 7..0, weight 1.0 at
 // the centre slot), so the iterate is bitwise unchanged.
@@ -47,7 +48,7 @@ struct UpQ {
   CUtensorMap tg;  // g:  same box
   CUtensorMap tc;  // carry_c: {Nc, Nc, Nc}, box {34, 3, 2}
   Up3 a;
-  int tilesK, nI;
+  int tilesK, nI, I0;  // cube layers [I0, I0 + nI): those holding the fine planes [a.ilo, a.ihi)
   long long steps, per;
 };
 
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(kQT, 1) k3_up_tma(const __grid_constant__ UpQ 
   if (s0 >= s1) return;
   auto coords = [&](long long s, int& I, int& J0, int& K0) {
     const long long t = s / A.nI;
-    I = (int)(s - t * A.nI);
+    I = A.I0 + (int)(s - t * A.nI);
     K0 = (int)(t % A.tilesK) * kQK;
     J0 = (int)(t / A.tilesK) * kQJ;
   };
@@ -188,13 +189,14 @@ __global__ void __launch_bounds__(kQT, 1) k3_up_tma(const __grid_constant__ UpQ 
               }
               acc = acc + wt * c[di][dj][dk];
             }
-            const bool skip = (ri == 0 && I == 0) || (rj == 0 && J == 0) || (rk == 0 && K == 0);
+            const int i = 3 * I + ri;  // fine planes outside [ilo, ihi) (Dirichlet / another shard's) stay as loaded
+            const bool skip = i < a.ilo || i >= a.ihi || (rj == 0 && J == 0) || (rk == 0 && K == 0);
             if (!skip) {
               const int o = (ri * kQFJ + 3 * ty + rj) * kQFK + 3 * tx + rk;
               const double cv = acc + Gs[o];
               const double un = Us[o] + cv;
               Us[o] = un;
-              if (CARRY) a.carry[vid(N, 3 * I + ri, 3 * J + rj, 3 * K + rk)] = cv;
+              if (CARRY) a.carry[vid(N, i, 3 * J + rj, 3 * K + rk)] = cv;
               if (ri == 0 && rj == 0 && rk == 0) {  // FAS walk-down injection
                 int ii = I, jj = J, kk = K;
                 for (int lc = a.l - 1; lc >= a.l0; --lc) {

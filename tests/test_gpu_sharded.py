@@ -49,7 +49,8 @@ def sharded_local(mk, world, n, variant, **kw):
 
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("name,variant", [("config5-L4", "adafac-jac"), ("config3-L4", "adafac-jac"),
-                                          ("config5-L4", "additive"), ("config3-L4", "afacc")])
+                                          ("config5-L4", "additive"), ("config3-L4", "afacc"),
+                                          ("config5-L5", "adafac-jac")])
 def test_gpu_sharded_equals_serial(world, name, variant):
     mk = lambda: workloads.by_name(name)  # noqa: E731
     wl = mk()
