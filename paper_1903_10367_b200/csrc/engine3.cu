@@ -423,7 +423,9 @@ int launch_up_tma(Engine3* e, int l, const Up3& a) {
 
 int launch_up_boxmg(Engine3* e, int l, const Up3& a) {
   if (e->L[l - 1].Pc && !a.pi) return launch_up_tma(e, l, a);
-  if (!kUseUpTile) {
+  // small levels (< 32 coarse cells per axis): the cell-owned kernel has 9x the threads of the
+  // tiled one, which is latency-bound there (config 5: up L3 55 -> 17 us, L4 79 -> 20 us)
+  if (!kUseUpTile || a.Nc - 1 < kUX) {
     LAUNCH3(kname("k3_up", l), k3_up_cell<true>, e->L[l - 1].u_grid, 128, a);
     return TMG_OK;
   }
