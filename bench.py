@@ -395,10 +395,16 @@ def run_ours(args, dist: Dist):
     kbytes = bm.get(kname)
     achieved = kbytes / (kms / kcnt * 1e-3) / 1e9 if kbytes else None
     traffic = None
+    cycle_traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(args.workload, {}).get(kname)
+            tj = json.load(open(tpath)).get(args.workload, {})
+            traffic = tj.get(kname)
+            # the whole cycle's DRAM bytes (ncu, one launch per kernel of this cycle) when every
+            # kernel timed here was captured: actual HBM traffic, next to the algorithmic B_alg
+            if tj and all(k in tj for k in prof):
+                cycle_traffic = float(sum(tj[k] for k in prof))
         except ValueError:
             traffic = None
     roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -407,7 +413,9 @@ def run_ours(args, dist: Dist):
                 "share_of_cycle": kms / total_prof, "peak_source": peak_src,
                 "cycle_B_alg": bm["cycle"],
                 "cycle_achieved_GBps": bm["cycle"] / (ms_step * 1e-3) / 1e9,
-                "cycle_frac": bm["cycle"] / (ms_step * 1e-3) / 1e9 / peak}
+                "cycle_frac": bm["cycle"] / (ms_step * 1e-3) / 1e9 / peak,
+                "cycle_dram_bytes": cycle_traffic,
+                "cycle_dram_frac": (cycle_traffic / (ms_step * 1e-3) / 1e9 / peak) if cycle_traffic else None}
     eng.close()
 
     # ---- time to a 1e-8 residual reduction (north star; bench.py:200 stop rule) ----
