@@ -17,6 +17,7 @@
 #include "kernels3d_ffp.cu"
 #include "kernels3d_ffp4.cu"
 #include "kernels3d_upq.cu"
+#include "kernels3d_smr.cu"
 
 namespace {
 
@@ -106,6 +107,7 @@ struct Engine3 {
   std::map<int, cudaGraphExec_t> gcache;
   // throttled BoxMG setup: next level to receive BoxMG P + Galerkin rows (< lmin: done)
   bool ffp4 = false;  // version-4 fused pass (TMA plane sets, partial-sum smoothing)
+  bool smr = false;   // finest-level smoothing fused with the restriction into ltop-1 (k3_smr)
   int thr_next = -1;
   int* deg = nullptr;
 };
@@ -479,12 +481,81 @@ SmoothS make_smooth_s(Engine3* e, int l) {
   return a;
 }
 
+// k3_smr over the finest level: adaFACx smoothing (when `smooth`) and the restriction of rho / sm
+// into level ltop-1's bR / bT
+int launch_smr(Engine3* e, bool smooth) {
+  Lvl3& c = e->L[e->ltop];
+  Lvl3& cc = e->L[e->ltop - 1];
+  Smr A{};
+  A.N = c.N;
+  A.Nc = cc.N;
+  const int n = cc.N - 2;
+  A.tilesK = (n + kRK - 1) / kRK;
+  const int tiles = A.tilesK * ((n + kRJ - 1) / kRJ);
+  // coarse-plane chunks: about a whole number of waves of one CTA per SM
+  int best = 1;
+  double best_eff = 0.0;
+  for (int nch = 1; nch <= std::min(n, 32); ++nch) {
+    const int chunk = (n + nch - 1) / nch, nb = tiles * ((n + chunk - 1) / chunk);
+    const double waves = (double)nb / num_sms();
+    const double eff = waves / std::ceil(waves) * (double)chunk / (chunk + 1.0);
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = nch; }
+  }
+  A.chunk = (n + best - 1) / best;
+  A.jac = smooth ? 1 : 0;
+  A.zc = e->cfg.variant == VAR_AFACC ? 1 : 0;
+  A.scale = e->cfg.omega * 3.0 / 8.0;
+  A.bR = cc.bR;
+  A.bT = cc.bT;
+  const uint64_t N = (uint64_t)c.N, Nc = (uint64_t)cc.N;
+  const uint64_t dp[4] = {Nc, Nc, Nc, 125}, sp[3] = {Nc * 8, Nc * Nc * 8, Nc * Nc * Nc * 8};
+  const uint32_t bp[4] = {kPW, kRJ, 1, 25};
+  if (!tmap3(&A.tr, c.rho, N, N, N, N * 8, N * N * 8, kRW, kRH, 1) || !tmap4(&A.tp, cc.P, dp, sp, bp))
+    return fail3(e, TMG_ECUDA, "tensor map encoding failed (k3_smr)");
+  const dim3 grid(tiles, (n + A.chunk - 1) / A.chunk);
+  cudaEvent_t e0_ = nullptr;
+  TRY3(begin_k(e, &e0_));
+  k3_smr<<<grid, kRThreads, kSmrSmem, e->s>>>(A);
+  CKL3();
+  TRY3(end_k(e, kname("k3_smooth", e->ltop), e0_));
+  return TMG_OK;
+}
+
 int enqueue_down(Engine3* e, bool write) {
   const bool jac = e->cfg.variant == VAR_JAC;
   const bool boxmg = e->cfg.flavor == TMG_BOXMG;
   const dim3 sblk(kSX, kSY);
   for (int l = e->ltop; l > e->lc; --l) {
     Lvl3& c = e->L[l];
+    if (e->smr && l == e->ltop - 1) {  // restrictions formed by k3_smr
+      Down3 a = make_down(e, l, write);
+      a.bR = c.bR;
+      a.bT = c.bT;
+      if (jac) LAUNCH3(kname("k3_down", l), (k3_down_c<true, true, true>), c.c_grid, 128, a);
+      else LAUNCH3(kname("k3_down", l), (k3_down_c<true, false, true>), c.c_grid, 128, a);
+      if (jac && write && l > e->lmin) {
+        SmoothS sa = make_smooth_s(e, l);
+        sa.chunk = c.s2_chunk;
+        cudaEvent_t e0_ = nullptr;
+        TRY3(begin_k(e, &e0_));
+        k3_smooth2r<<<c.s2_blocks, dim3(kSX, k2Y / 2), k2RSmemV, e->s>>>(sa);
+        CKL3();
+        TRY3(end_k(e, kname("k3_smooth", l), e0_));
+      }
+      continue;
+    }
+    if (e->smr && l == e->ltop) {
+      Top3 a = make_top(e, l);
+      a.chunk = c.s2_chunk;
+      cudaEvent_t e0_ = nullptr;
+      TRY3(begin_k(e, &e0_));
+      if (c.op.kind == OP_CONST) k3_top2<OP_CONST><<<c.s2_blocks, dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
+      else k3_top2<OP_ELEMENT><<<c.s2_blocks, dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
+      CKL3();
+      TRY3(end_k(e, kname("k3_down", l), e0_));
+      TRY3(launch_smr(e, jac && write));
+      continue;
+    }
     if (l == e->ltop) {
       Top3 a = make_top(e, l);
       a.chunk = c.s2_chunk;
@@ -985,6 +1056,18 @@ int build(Engine3* e, const tmg_tree3* t) {
       e->ffp_chunk = (cc.N + nch - 1) / nch;
       e->ffp_blocks = t2 * ((cc.N + e->ffp_chunk - 1) / e->ffp_chunk);
       parts = std::max(parts, e->ffp_blocks);
+    }
+  }
+  // finest-level smoothing + restriction fused (k3_smr; TMG_SMR=0: k3_smooth2r + k3_down_c)
+  {
+    const char* env = std::getenv("TMG_SMR");
+    e->smr = !(env && env[0] == '0') && !e->ffp && cfg.flavor == TMG_BOXMG && cfg.variant != VAR_PI &&
+             l1 - 1 > e->lc;
+    if (e->smr) {
+      CK3(cudaFuncSetAttribute(k3_smr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmem));
+      Lvl3& cc = e->L[l1 - 1];
+      if (!cc.bR) TRY3(alloc3(e, &cc.bR, cc.nv));
+      if (!cc.bT) TRY3(alloc3(e, &cc.bT, cc.nv));
     }
   }
   e->nparts = parts;
