@@ -31,17 +31,19 @@
 namespace t3 {
 
 constexpr int kRK = 32, kRJ = 4;                  // coarse tile (K, J)
-constexpr int kRThreads = 2 * kRK * kRJ;          // 256: (coarse vertex, field)
+constexpr int kRTasks = 2 * kRK * kRJ;            // 256 restriction tasks: (coarse vertex, field)
+constexpr int kRThreads = 2 * kRTasks;            // 512: 256 smoothing threads + 256 restriction threads
 constexpr int kRW = 3 * kRK + 4, kRH = 3 * kRJ + 4;  // rho window 100 x 16
 constexpr int kSW = 3 * kRK + 2, kSH = 3 * kRJ + 2;  // sm window 98 x 14
 constexpr int kRSlot = ((kRW * kRH * 8 + 127) / 128) * 128 / 8;
-constexpr int kRStages = 4;                        // rho planes in flight
+constexpr int kRStages = 5;                        // rho plane ring
 constexpr int kPW = kRK + 2;                       // P box rows from K0 - 1 (16-byte aligned start): 34
 constexpr int kPBox = (kPW * kRJ * 25 + 15) / 16 * 16;  // one 25-slot P box (27.2 KB; 128-byte multiple)
-constexpr int kPStages = 3;                        // P sets (two boxes each) in flight
-constexpr int kSCols = (kSW * kSH + kRThreads - 1) / kRThreads;  // 6 sm columns per thread
+constexpr int kPStages = 2;                        // P sets (two boxes each)
+constexpr int kSBuf = (kSW * kSH + 15) / 16 * 16;  // one sm plane (double buffered)
+constexpr int kSCols = (kSW * kSH + kRTasks - 1) / kRTasks;  // 6 sm columns per smoothing thread
 constexpr int oRP = kRStages * kRSlot, oRS = oRP + kPStages * 2 * kPBox;
-constexpr size_t kSmrSmem = sizeof(double) * (oRS + kSW * kSH);
+constexpr size_t kSmrSmem = sizeof(double) * (oRS + 2 * kSBuf);
 
 struct Smr {
   CUtensorMap tr;  // rho of the finest level, box {100, 16, 1}
@@ -56,10 +58,12 @@ struct Smr {
 
 __device__ __forceinline__ int floor3s(int x) { return x >= 0 ? x / 3 : -((2 - x) / 3); }
 
+// Warp-specialised: threads [0, 256) complete sm(t-1) from rho(t) (phase C) while threads
+// [256, 512) restrict fine plane t-2 (phase D, one step behind, sm double buffered), so the two
+// latency-bound phases overlap; one CTA barrier per step.
 __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ Smr A) {
   extern __shared__ __align__(128) double sr[];
   __shared__ __align__(8) uint64_t bar[kRStages], pbar[kPStages];
-  double* Sb = sr + oRS;
   const int N = A.N, Nc = A.Nc, n = Nc - 2;
   const int tk = blockIdx.x % A.tilesK, tj = blockIdx.x / A.tilesK;
   const int K0 = 1 + tk * kRK, J0 = 1 + tj * kRJ;
@@ -67,45 +71,40 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
   if (Ia >= Ib) return;
   const int fk0 = 3 * K0 - 3, fj0 = 3 * J0 - 3;  // rho window origin (fine)
   const int p0 = 3 * Ia - 3, pEnd = 3 * Ib;       // rho planes streamed: [p0, pEnd]
-  const int s0 = 3 * Ia - 2;                      // first fine plane restricted (P sets: [s0, pEnd - 1])
+  const int s0 = 3 * Ia - 2;                      // fine planes restricted: [s0, pEnd - 1]
   const int lt = threadIdx.x;
+  const bool smoother = lt < kRTasks;
 
-  // sm columns of this thread and their pending partial sums
+  // smoothing threads: sm columns and their pending partial sums
   int scol[kSCols];
   bool sin_[kSCols];
   double SEa[kSCols], SCa[kSCols], XA[kSCols], SEb[kSCols], SCb[kSCols];
 #pragma unroll
   for (int m = 0; m < kSCols; ++m) {
-    const int q = lt + m * kRThreads;
+    const int q = lt + m * kRTasks;
     const int jj = q / kSW, kk = q - jj * kSW;
     const int j = fj0 + 1 + jj, k = fk0 + 1 + kk;
-    scol[m] = q < kSW * kSH ? q : -1;
+    scol[m] = (smoother && q < kSW * kSH) ? q : -1;
     sin_[m] = q < kSW * kSH && j >= 1 && k >= 1 && j <= N - 2 && k <= N - 2;
     SEa[m] = SCa[m] = XA[m] = SEb[m] = SCb[m] = 0.0;
   }
-  // restriction task: coarse (J, K) of the tile, field 0 rho / 1 sm (adjacent lanes)
-  const int fld = lt & 1, w = lt >> 1;
+  // restriction threads: coarse (J, K) of the tile, field 0 rho / 1 sm (adjacent lanes)
+  const int task = lt - kRTasks;
+  const int fld = task & 1, w = task >> 1;
   const int wj = w / kRK, wk = w % kRK;
   const int rJ = J0 + wj, rK = K0 + wk;
-  const bool rtask = (fld == 0 || A.jac) && rJ <= n && rK <= n;
+  const bool rtask = !smoother && (fld == 0 || A.jac) && rJ <= n && rK <= n;
   double accC = 0.0, accN = 0.0;
 
-  // which P boxes fine plane s needs: coarse plane m3 (offset o) in the chunk; m3 + 1 when o >= 1
-  auto pneed = [&](int s, bool& c, bool& nx) {
-    const int m3 = floor3s(s), o = s - 3 * m3;
-    c = m3 >= Ia && m3 < Ib;
-    nx = o >= 1 && m3 + 1 >= Ia && m3 + 1 < Ib;
-  };
-  auto issue_r = [&](int p) {  // thread 0: rho plane p into its slot
+  auto issue_r = [&](int p) {  // rho plane p into its slot
     const int sl = (p - p0) % kRStages;
     mbar_expect_tx(&bar[sl], (unsigned)(sizeof(double) * kRW * kRH));
     tma_load_3d(sr + sl * kRSlot, &A.tr, &bar[sl], fk0, fj0, p);
   };
-  auto issue_p = [&](int s) {  // thread 0: the P boxes of fine plane s into its set
+  auto issue_p = [&](int s) {  // the P boxes fine plane s meets into its set
     const int sl = (s - s0) % kPStages;
-    bool c, nx;
-    pneed(s, c, nx);
     const int m3 = floor3s(s), o = s - 3 * m3;
+    const bool c = m3 >= Ia && m3 < Ib, nx = o >= 1 && m3 + 1 >= Ia && m3 + 1 < Ib;
     mbar_expect_tx(&pbar[sl], (unsigned)(sizeof(double) * kPW * kRJ * 25) * ((c ? 1u : 0u) + (nx ? 1u : 0u)));
     double* dst = sr + oRP + sl * 2 * kPBox;
     if (c) tma_load_4d(dst, &A.tp, &pbar[sl], K0 - 1, J0, m3, (o + 2) * 25);
@@ -118,94 +117,98 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
   }
   __syncthreads();
   if (lt == 0) {
-    for (int p = p0; p <= min(pEnd, p0 + kRStages - 2); ++p) issue_r(p);
-    for (int s = s0; s <= min(pEnd - 1, s0 + kPStages - 2); ++s) issue_p(s);
+    for (int p = p0; p <= min(pEnd, p0 + 2); ++p) issue_r(p);
+    for (int s = s0; s <= min(pEnd - 1, s0 + kPStages - 1); ++s) issue_p(s);
   }
 
-  for (int p = p0; p <= pEnd; ++p) {
-    const int r = p - p0;
-    const int s = p - 1;  // the fine plane restricted this step
-    if (r >= 1) {
-      __syncthreads();  // D(p-1) has read the sm buffer, rho(p-2)'s slot and P(p-2)'s set
+  // step t: C completes sm(t-1) from rho(t); D restricts fine plane t-2
+  for (int t = p0; t <= pEnd + 1; ++t) {
+    if (t > p0) {
+      __syncthreads();  // step t-1 done: rho(t-3)'s slot and P(t-3)'s set are free, sm(t-2) is written
       if (lt == 0) {
         fence_proxy_async();
-        if (p + kRStages - 2 <= pEnd) issue_r(p + kRStages - 2);     // into the slot of plane p - 2
-        if (s >= s0 && s + kPStages - 1 <= pEnd - 1)  // into the set of plane s - 1
-          issue_p(s + kPStages - 1);
+        if (t + 2 <= pEnd) issue_r(t + 2);                              // into the slot of plane t - 3
+        if (t - 1 >= s0 + kPStages && t - 1 <= pEnd - 1) issue_p(t - 1);  // into the set of plane t - 3
       }
     }
-    mbar_wait(&bar[r % kRStages], (unsigned)(r / kRStages) & 1u);
-    const double* Rp = sr + (r % kRStages) * kRSlot;
-
-    // ---- C: sm(p - 1) completes; sm(p), sm(p + 1) advance ------------------------
-    if (A.jac) {
-      const bool sok = p - 1 >= 1 && p - 1 <= N - 2;
+    if (smoother) {
+      // ---- C: sm(t - 1) completes; sm(t), sm(t + 1) advance ------------------------
+      // every rho plane's TMA is waited for here (also without smoothing): a slot is re-armed only
+      // after its previous load completed, and no load is in flight when the CTA exits
+      const int r = t - p0;
+      if (t <= pEnd) mbar_wait(&bar[r % kRStages], (unsigned)(r / kRStages) & 1u);
+      if (A.jac && t <= pEnd) {
+        const double* Rp = sr + (r % kRStages) * kRSlot;
+        double* Sb = sr + oRS + ((t - 1) & 1) * kSBuf;
+        const bool sok = t - 1 >= 1 && t - 1 <= N - 2;
 #pragma unroll
-      for (int m = 0; m < kSCols; ++m) {
-        if (scol[m] < 0) continue;
-        const int q = scol[m];
-        const int jj = q / kSW, kk = q - jj * kSW;
-        const int r0 = (jj + 1) * kRW + (kk + 1);
-        const double f0 = Rp[r0 - kRW], f1 = Rp[r0 - 1], f2 = Rp[r0 + 1], f3 = Rp[r0 + kRW];
-        const double d0 = Rp[r0 - kRW - 1], d1 = Rp[r0 - kRW + 1], d2 = Rp[r0 + kRW - 1], d3 = Rp[r0 + kRW + 1];
-        const double xc = Rp[r0];
-        double se = (((SEa[m] + f0) + f1) + f2) + f3;
-        double sc = (((SCa[m] + d0) + d1) + d2) + d3;
-        double v = ((C_D8 * XA[m]) - (C_E6 * se)) - (C_C12 * sc);
-        v = v * A.scale;
-        Sb[q] = (sok && sin_[m]) ? v : 0.0;
-        SEa[m] = (((SEb[m] + d0) + d1) + d2) + d3;
-        SCa[m] = SCb[m];
-        XA[m] = xc;
-        SEb[m] = ((f0 + f1) + f2) + f3;
-        SCb[m] = ((d0 + d1) + d2) + d3;
+        for (int m = 0; m < kSCols; ++m) {
+          if (scol[m] < 0) continue;
+          const int q = scol[m];
+          const int jj = q / kSW, kk = q - jj * kSW;
+          const int r0 = (jj + 1) * kRW + (kk + 1);
+          const double f0 = Rp[r0 - kRW], f1 = Rp[r0 - 1], f2 = Rp[r0 + 1], f3 = Rp[r0 + kRW];
+          const double d0 = Rp[r0 - kRW - 1], d1 = Rp[r0 - kRW + 1], d2 = Rp[r0 + kRW - 1], d3 = Rp[r0 + kRW + 1];
+          const double xc = Rp[r0];
+          double se = (((SEa[m] + f0) + f1) + f2) + f3;
+          double sc = (((SCa[m] + d0) + d1) + d2) + d3;
+          double v = ((C_D8 * XA[m]) - (C_E6 * se)) - (C_C12 * sc);
+          v = v * A.scale;
+          Sb[q] = (sok && sin_[m]) ? v : 0.0;
+          SEa[m] = (((SEb[m] + d0) + d1) + d2) + d3;
+          SCa[m] = SCb[m];
+          XA[m] = xc;
+          SEb[m] = ((f0 + f1) + f2) + f3;
+          SCb[m] = ((d0 + d1) + d2) + d3;
+        }
       }
-      __syncthreads();  // sm(p - 1) complete in Sb
-    }
-
-    // ---- D: restriction of fine plane s = p - 1 (rho from its slot, sm from Sb) ------
-    if (s >= s0) {
-      const int ps = s - s0;
-      mbar_wait(&pbar[ps % kPStages], (unsigned)(ps / kPStages) & 1u);
-      const double* Pset = sr + oRP + (ps % kPStages) * 2 * kPBox + wj * kPW + wk + 1;
-      if (rtask) {
-        const int m3 = floor3s(s), o = s - 3 * m3;
-        const double* src;
-        int ld;
-        if (fld == 0) {
-          src = sr + ((r + kRStages - 1) % kRStages) * kRSlot + (3 * wj + 3) * kRW + 3 * wk + 3;
-          ld = kRW;
-        } else {
-          src = Sb + (3 * wj + 2) * kSW + 3 * wk + 2;
-          ld = kSW;
-        }
-        const bool zc = fld == 0 && A.zc;
-        if (m3 >= Ia && m3 < Ib) {  // coarse plane m3, fine offset o in {0, 1, 2}
-          double acc = accC;
-#pragma unroll
-          for (int q = 0; q < 25; ++q) {
-            const int oj = q / 5 - 2, ok = q % 5 - 2;
-            const bool ctr = o == 0 && q == 12;
-            const double wt = ctr ? 1.0 : Pset[q * kRJ * kPW];
-            double x = src[oj * ld + ok];
-            if (ctr && zc) x = 0.0;
-            acc = acc + wt * x;
+    } else {
+      // ---- D: restriction of fine plane s = t - 2 (rho from its slot, sm(s) from its buffer) ----
+      const int s = t - 2;
+      if (s >= s0) {
+        const int ps = s - s0, rs_ = s - p0;
+        mbar_wait(&pbar[ps % kPStages], (unsigned)(ps / kPStages) & 1u);
+        mbar_wait(&bar[rs_ % kRStages], (unsigned)(rs_ / kRStages) & 1u);  // rho(s): visibility of the TMA write
+        const double* Pset = sr + oRP + (ps % kPStages) * 2 * kPBox + wj * kPW + wk + 1;
+        if (rtask) {
+          const int m3 = floor3s(s), o = s - 3 * m3;
+          const double* src;
+          int ld;
+          if (fld == 0) {
+            src = sr + (rs_ % kRStages) * kRSlot + (3 * wj + 3) * kRW + 3 * wk + 3;
+            ld = kRW;
+          } else {
+            src = sr + oRS + (s & 1) * kSBuf + (3 * wj + 2) * kSW + 3 * wk + 2;
+            ld = kSW;
           }
-          accC = acc;
-          if (o == 2) (fld ? A.bT : A.bR)[((size_t)m3 * Nc + rJ) * Nc + rK] = acc;
-        }
-        if (o >= 1 && m3 + 1 >= Ia && m3 + 1 < Ib) {  // coarse plane m3 + 1, fine offset o - 3
-          double acc = accN;
+          const bool zc = fld == 0 && A.zc;
+          if (m3 >= Ia && m3 < Ib) {  // coarse plane m3, fine offset o in {0, 1, 2}
+            double acc = accC;
 #pragma unroll
-          for (int q = 0; q < 25; ++q) {
-            const int oj = q / 5 - 2, ok = q % 5 - 2;
-            acc = acc + Pset[kPBox + q * kRJ * kPW] * src[oj * ld + ok];
+            for (int q = 0; q < 25; ++q) {
+              const int oj = q / 5 - 2, ok = q % 5 - 2;
+              const bool ctr = o == 0 && q == 12;
+              const double wt = ctr ? 1.0 : Pset[q * kRJ * kPW];
+              double x = src[oj * ld + ok];
+              if (ctr && zc) x = 0.0;
+              acc = acc + wt * x;
+            }
+            accC = acc;
+            if (o == 2) (fld ? A.bT : A.bR)[((size_t)m3 * Nc + rJ) * Nc + rK] = acc;
           }
-          accN = acc;
-        }
-        if (o == 2) {
-          accC = accN;
-          accN = 0.0;
+          if (o >= 1 && m3 + 1 >= Ia && m3 + 1 < Ib) {  // coarse plane m3 + 1, fine offset o - 3
+            double acc = accN;
+#pragma unroll
+            for (int q = 0; q < 25; ++q) {
+              const int oj = q / 5 - 2, ok = q % 5 - 2;
+              acc = acc + Pset[kPBox + q * kRJ * kPW] * src[oj * ld + ok];
+            }
+            accN = acc;
+          }
+          if (o == 2) {
+            accC = accN;
+            accN = 0.0;
+          }
         }
       }
     }
