@@ -41,7 +41,9 @@ constexpr int kPW = kRK + 2;                       // P box rows from K0 - 1 (16
 constexpr int kPBox = (kPW * kRJ * 25 + 15) / 16 * 16;  // one 25-slot P box (27.2 KB; 128-byte multiple)
 constexpr int kPStages = 2;                        // P sets (two boxes each)
 constexpr int kSBuf = (kSW * kSH + 15) / 16 * 16;  // one sm plane (double buffered)
-constexpr int kSCols = (kSW * kSH + kRTasks - 1) / kRTasks;  // 6 sm columns per smoothing thread
+constexpr int kSPairs = (kSW * (kSH / 2) + kRTasks - 1) / kRTasks;  // 3 pairs of sm columns per smoothing thread
+constexpr int kSCols = 2 * kSPairs;
+static_assert(kSH % 2 == 0, "sm columns are paired along j");
 constexpr int oRP = kRStages * kRSlot, oRS = oRP + kPStages * 2 * kPBox;
 constexpr size_t kSmrSmem = sizeof(double) * (oRS + 2 * kSBuf);
 
@@ -75,19 +77,25 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
   const int lt = threadIdx.x;
   const bool smoother = lt < kRTasks;
 
-  // smoothing threads: sm columns and their pending partial sums
-  int scol[kSCols];
+  // smoothing threads: pairs of sm columns (jj, jj + 1) at kk -- the pair's 3 x 3 rho
+  // neighbourhoods share 6 of their 9 values (12 shared loads per 2 columns) -- and the
+  // columns' pending partial sums
+  int spair[kSPairs];
   bool sin_[kSCols];
   double SEa[kSCols], SCa[kSCols], XA[kSCols], SEb[kSCols], SCb[kSCols];
 #pragma unroll
-  for (int m = 0; m < kSCols; ++m) {
-    const int q = lt + m * kRTasks;
-    const int jj = q / kSW, kk = q - jj * kSW;
-    const int j = fj0 + 1 + jj, k = fk0 + 1 + kk;
-    scol[m] = (smoother && q < kSW * kSH) ? q : -1;
-    sin_[m] = q < kSW * kSH && j >= 1 && k >= 1 && j <= N - 2 && k <= N - 2;
-    SEa[m] = SCa[m] = XA[m] = SEb[m] = SCb[m] = 0.0;
+  for (int m = 0; m < kSPairs; ++m) {
+    const int q2 = lt + m * kRTasks;
+    const int jp = q2 / kSW, kk = q2 - jp * kSW;
+    spair[m] = (smoother && q2 < kSW * (kSH / 2)) ? q2 : -1;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = fj0 + 1 + 2 * jp + h, k = fk0 + 1 + kk;
+      sin_[2 * m + h] = q2 < kSW * (kSH / 2) && j >= 1 && k >= 1 && j <= N - 2 && k <= N - 2;
+    }
   }
+#pragma unroll
+  for (int m = 0; m < kSCols; ++m) SEa[m] = SCa[m] = XA[m] = SEb[m] = SCb[m] = 0.0;
   // restriction threads: coarse (J, K) of the tile, field 0 rho / 1 sm (adjacent lanes)
   const int task = lt - kRTasks;
   const int fld = task & 1, w = task >> 1;
@@ -142,24 +150,34 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
         double* Sb = sr + oRS + ((t - 1) & 1) * kSBuf;
         const bool sok = t - 1 >= 1 && t - 1 <= N - 2;
 #pragma unroll
-        for (int m = 0; m < kSCols; ++m) {
-          if (scol[m] < 0) continue;
-          const int q = scol[m];
-          const int jj = q / kSW, kk = q - jj * kSW;
-          const int r0 = (jj + 1) * kRW + (kk + 1);
-          const double f0 = Rp[r0 - kRW], f1 = Rp[r0 - 1], f2 = Rp[r0 + 1], f3 = Rp[r0 + kRW];
-          const double d0 = Rp[r0 - kRW - 1], d1 = Rp[r0 - kRW + 1], d2 = Rp[r0 + kRW - 1], d3 = Rp[r0 + kRW + 1];
-          const double xc = Rp[r0];
-          double se = (((SEa[m] + f0) + f1) + f2) + f3;
-          double sc = (((SCa[m] + d0) + d1) + d2) + d3;
-          double v = ((C_D8 * XA[m]) - (C_E6 * se)) - (C_C12 * sc);
-          v = v * A.scale;
-          Sb[q] = (sok && sin_[m]) ? v : 0.0;
-          SEa[m] = (((SEb[m] + d0) + d1) + d2) + d3;
-          SCa[m] = SCb[m];
-          XA[m] = xc;
-          SEb[m] = ((f0 + f1) + f2) + f3;
-          SCb[m] = ((d0 + d1) + d2) + d3;
+        for (int mp = 0; mp < kSPairs; ++mp) {
+          if (spair[mp] < 0) continue;
+          const int q2 = spair[mp];
+          const int jp = q2 / kSW, kk = q2 - jp * kSW;
+          // rows 2 jp - 1 .. 2 jp + 2, cols kk - 1 .. kk + 1 of the sm window (rho window + 1)
+          const int rb = (2 * jp) * kRW + kk;
+          double R[4][3];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) R[a][b] = Rp[rb + a * kRW + b];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int m = 2 * mp + h;
+            const double f0 = R[h][1], f1 = R[h + 1][0], f2 = R[h + 1][2], f3 = R[h + 2][1];
+            const double d0 = R[h][0], d1 = R[h][2], d2 = R[h + 2][0], d3 = R[h + 2][2];
+            const double xc = R[h + 1][1];
+            double se = (((SEa[m] + f0) + f1) + f2) + f3;
+            double sc = (((SCa[m] + d0) + d1) + d2) + d3;
+            double v = ((C_D8 * XA[m]) - (C_E6 * se)) - (C_C12 * sc);
+            v = v * A.scale;
+            Sb[(2 * jp + h) * kSW + kk] = (sok && sin_[m]) ? v : 0.0;
+            SEa[m] = (((SEb[m] + d0) + d1) + d2) + d3;
+            SCa[m] = SCb[m];
+            XA[m] = xc;
+            SEb[m] = ((f0 + f1) + f2) + f3;
+            SCb[m] = ((d0 + d1) + d2) + d3;
+          }
         }
       }
     } else {
