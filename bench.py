@@ -186,14 +186,16 @@ def bytes_model3(eng, wl):
     for l in range(l0, min(L, l0 + 2) + 1):
         if (3**l + 1) ** 3 <= 1024:
             lc = l
-    # k3_smr (the engine's default for BoxMG but adafac-pi): the finest level's smoothing and the
-    # restriction into L-1 run in one kernel named k3_smooth_L{L}; k3_down_L{L-1} reads b_R / b_T
+    # k3_smr (the engine's default for BoxMG but adafac-pi): a level's smoothing and its restriction
+    # into the next coarser level run in one kernel named k3_smooth_L{l}; k3_down_L{l-1} reads b_R / b_T
     smr = (boxmg and wl.variant != "adafac-pi" and L - 1 > lc and os.environ.get("TMG_SMR", "1") != "0"
            and os.environ.get("TMG_FFP", "0") not in ("1", "4"))
-    if smr:
-        nc, nf, nb = dofs[L - 1], dofs[L], (2 if jac else 1)
-        out[f"k3_smooth_L{L}"] = nf * 8 + nc * 992 + nc * 8 * nb
-        out[f"k3_down_L{L - 1}"] -= nf * 8 * nb + nc * 992 - nc * 8 * nb
+    if smr:  # every level l >= lc + 2 smooths and restricts into l - 1 in k3_smooth_L{l}
+        nb = 2 if jac else 1
+        for l in range(lc + 2, L + 1):
+            nc, nf = dofs[l - 1], dofs[l]
+            out[f"k3_smooth_L{l}"] = nf * 8 + nc * 992 + nc * 8 * nb
+            out[f"k3_down_L{l - 1}"] -= nf * 8 * nb + nc * 992 - nc * 8 * nb
     out["k3_chain"] = sum(out.get(f"k3_{k}_L{l}", 0) for l in range(l0, lc + 1)
                           for k in ("down", "smooth", "up"))
     fine = dofs[L]

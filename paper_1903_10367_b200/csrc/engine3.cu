@@ -107,7 +107,8 @@ struct Engine3 {
   std::map<int, cudaGraphExec_t> gcache;
   // throttled BoxMG setup: next level to receive BoxMG P + Galerkin rows (< lmin: done)
   bool ffp4 = false;  // version-4 fused pass (TMA plane sets, partial-sum smoothing)
-  bool smr = false;   // finest-level smoothing fused with the restriction into ltop-1 (k3_smr)
+  bool smr = false;   // smoothing fused with the restriction into the next level (k3_smr)
+  int smr_lo = 0;     // ... for the levels smr_lo..ltop
   int thr_next = -1;
   int* deg = nullptr;
 };
@@ -483,9 +484,9 @@ SmoothS make_smooth_s(Engine3* e, int l) {
 
 // k3_smr over the finest level: adaFACx smoothing (when `smooth`) and the restriction of rho / sm
 // into level ltop-1's bR / bT
-int launch_smr(Engine3* e, bool smooth) {
-  Lvl3& c = e->L[e->ltop];
-  Lvl3& cc = e->L[e->ltop - 1];
+int launch_smr(Engine3* e, int l, bool smooth) {
+  Lvl3& c = e->L[l];
+  Lvl3& cc = e->L[l - 1];
   Smr A{};
   A.N = c.N;
   A.Nc = cc.N;
@@ -517,7 +518,7 @@ int launch_smr(Engine3* e, bool smooth) {
   TRY3(begin_k(e, &e0_));
   k3_smr<<<grid, kRThreads, kSmrSmem, e->s>>>(A);
   CKL3();
-  TRY3(end_k(e, kname("k3_smooth", e->ltop), e0_));
+  TRY3(end_k(e, kname("k3_smooth", l), e0_));
   return TMG_OK;
 }
 
@@ -527,35 +528,6 @@ int enqueue_down(Engine3* e, bool write) {
   const dim3 sblk(kSX, kSY);
   for (int l = e->ltop; l > e->lc; --l) {
     Lvl3& c = e->L[l];
-    if (e->smr && l == e->ltop - 1) {  // restrictions formed by k3_smr
-      Down3 a = make_down(e, l, write);
-      a.bR = c.bR;
-      a.bT = c.bT;
-      if (jac) LAUNCH3(kname("k3_down", l), (k3_down_c<true, true, true>), c.c_grid, 128, a);
-      else LAUNCH3(kname("k3_down", l), (k3_down_c<true, false, true>), c.c_grid, 128, a);
-      if (jac && write && l > e->lmin) {
-        SmoothS sa = make_smooth_s(e, l);
-        sa.chunk = c.s2_chunk;
-        cudaEvent_t e0_ = nullptr;
-        TRY3(begin_k(e, &e0_));
-        k3_smooth2r<<<c.s2_blocks, dim3(kSX, k2Y / 2), k2RSmemV, e->s>>>(sa);
-        CKL3();
-        TRY3(end_k(e, kname("k3_smooth", l), e0_));
-      }
-      continue;
-    }
-    if (e->smr && l == e->ltop) {
-      Top3 a = make_top(e, l);
-      a.chunk = c.s2_chunk;
-      cudaEvent_t e0_ = nullptr;
-      TRY3(begin_k(e, &e0_));
-      if (c.op.kind == OP_CONST) k3_top2<OP_CONST><<<c.s2_blocks, dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
-      else k3_top2<OP_ELEMENT><<<c.s2_blocks, dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
-      CKL3();
-      TRY3(end_k(e, kname("k3_down", l), e0_));
-      TRY3(launch_smr(e, jac && write));
-      continue;
-    }
     if (l == e->ltop) {
       Top3 a = make_top(e, l);
       a.chunk = c.s2_chunk;
@@ -565,6 +537,12 @@ int enqueue_down(Engine3* e, bool write) {
       else k3_top2<OP_ELEMENT><<<c.s2_blocks, dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
       CKL3();
       TRY3(end_k(e, kname("k3_down", l), e0_));
+    } else if (e->smr && l + 1 >= e->smr_lo) {  // restrictions formed by k3_smr of level l + 1
+      Down3 a = make_down(e, l, write);
+      a.bR = c.bR;
+      a.bT = c.bT;
+      if (jac) LAUNCH3(kname("k3_down", l), (k3_down_c<true, true, true>), c.c_grid, 128, a);
+      else LAUNCH3(kname("k3_down", l), (k3_down_c<true, false, true>), c.c_grid, 128, a);
     } else {
       Down3 a = make_down(e, l, write);
       if (boxmg && jac) LAUNCH3(kname("k3_down", l), (k3_down_c<true, true>), c.c_grid, 128, a);
@@ -572,7 +550,9 @@ int enqueue_down(Engine3* e, bool write) {
       else if (jac) LAUNCH3(kname("k3_down", l), (k3_down_c<false, true>), c.c_grid, 128, a);
       else LAUNCH3(kname("k3_down", l), (k3_down_c<false, false>), c.c_grid, 128, a);
     }
-    if (jac && write && l > e->lmin) {
+    if (e->smr && l >= e->smr_lo) {
+      TRY3(launch_smr(e, l, jac && write));
+    } else if (jac && write && l > e->lmin) {
       SmoothS sa = make_smooth_s(e, l);
       sa.chunk = c.s2_chunk;
       cudaEvent_t e0_ = nullptr;
@@ -1063,11 +1043,14 @@ int build(Engine3* e, const tmg_tree3* t) {
     const char* env = std::getenv("TMG_SMR");
     e->smr = !(env && env[0] == '0') && !e->ffp && cfg.flavor == TMG_BOXMG && cfg.variant != VAR_PI &&
              l1 - 1 > e->lc;
+    e->smr_lo = e->lc + 2;  // every level whose coarser level is a grid (not chain) level
     if (e->smr) {
       CK3(cudaFuncSetAttribute(k3_smr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmem));
-      Lvl3& cc = e->L[l1 - 1];
-      if (!cc.bR) TRY3(alloc3(e, &cc.bR, cc.nv));
-      if (!cc.bT) TRY3(alloc3(e, &cc.bT, cc.nv));
+      for (int l = e->smr_lo - 1; l < l1; ++l) {
+        Lvl3& cc = e->L[l];
+        if (!cc.bR) TRY3(alloc3(e, &cc.bR, cc.nv));
+        if (!cc.bT) TRY3(alloc3(e, &cc.bT, cc.nv));
+      }
     }
   }
   e->nparts = parts;
