@@ -18,6 +18,8 @@
 #include "kernels3d_ffp4.cu"
 #include "kernels3d_upq.cu"
 #include "kernels3d_smr.cu"
+#include "kernels3d_updict.cu"
+#include "kernels3d_dict.cu"
 
 namespace {
 
@@ -29,6 +31,11 @@ struct Lvl3 {
   double *u = nullptr, *rhs = nullptr, *g = nullptr, *rho = nullptr, *sm = nullptr, *carry = nullptr;
   double *eff = nullptr, *coef = nullptr, *tbl = nullptr, *P = nullptr;
   double* Pc = nullptr;  // levels ltop-1, ltop-2: cube-owned copy of P for the TMA-fed prolongation (k3_up_tma)
+  // level ltop-1: row dictionaries of P (k3_smr) and Pc (k3_up_tma), kernels3d_dict.cu; null = dense
+  double *Pd = nullptr, *Pcd = nullptr;
+  uint32_t *Pdi = nullptr, *Pcdi = nullptr;
+  uint8_t* Ptab = nullptr;  // k3_up_tma step tables over Pc's dictionary
+  size_t Pdp = 0, Pdn = 0, Pcdp = 0, Pcdn = 0;
   double* coefp = nullptr;  // finest level: coef with rows padded to even length (TMA)
   double *bR = nullptr, *bT = nullptr;  // level ltop-1: restrictions from the fused fine pass
   Op3 op{};
@@ -333,9 +340,10 @@ bool cell_tmap(CUtensorMap* map, const double* base, int n) {
 }
 
 // Generic 3D tensor map over fp64 data (dims innermost first, byte strides of dims 1, 2).
-bool tmap3(CUtensorMap* map, const double* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
+bool tmap3(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
            uint64_t s2, uint32_t b0, uint32_t b1, uint32_t b2,
-           CUtensorMapL2promotion prom = CU_TENSOR_MAP_L2_PROMOTION_L2_128B) {
+           CUtensorMapL2promotion prom = CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+           CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT64) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -349,7 +357,7 @@ bool tmap3(CUtensorMap* map, const double* base, uint64_t d0, uint64_t d1, uint6
   const cuuint64_t strides[2] = {s1, s2};
   const cuuint32_t box[3] = {b0, b1, b2};
   const cuuint32_t estr[3] = {1, 1, 1};
-  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
+  return encode(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                 prom, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -417,8 +425,26 @@ int launch_up_tma(Engine3* e, int l, const Up3& a) {
   A.per = (A.steps + grid - 1) / grid;
   cudaEvent_t e0_ = nullptr;
   TRY3(begin_k(e, &e0_));
-  if (a.carry) k3_up_tma<true><<<grid, kQT, kUpTmaSmem, e->s>>>(A);
-  else k3_up_tma<false><<<grid, kQT, kUpTmaSmem, e->s>>>(A);
+  if (cc.Pcd) {  // weights from the row dictionary (k3_up_dict)
+    UpD D{};
+    D.tu = A.tu;
+    D.tg = A.tg;
+    D.tc = A.tc;
+    D.a = a;
+    D.dict = cc.Pcd;
+    D.tab = cc.Ptab;
+    D.tilesK = A.tilesK;
+    D.tilesJ = (int)((nc_ + kQJ - 1) / kQJ);
+    D.nI = A.nI;
+    D.I0 = A.I0;
+    D.steps = (int)A.steps;
+    D.per = (int)A.per;
+    if (a.carry) k3_up_dict<true><<<grid, kDThreads, kUpDictSmem, e->s>>>(D);
+    else k3_up_dict<false><<<grid, kDThreads, kUpDictSmem, e->s>>>(D);
+  } else {
+    if (a.carry) k3_up_tma<true><<<grid, kQT, kUpTmaSmem, e->s>>>(A);
+    else k3_up_tma<false><<<grid, kQT, kUpTmaSmem, e->s>>>(A);
+  }
   CKL3();
   TRY3(end_k(e, kname("k3_up", l), e0_));
   return TMG_OK;
@@ -513,10 +539,16 @@ int launch_smr(Engine3* e, int l, bool smooth) {
   const uint32_t bp[4] = {kPW, kRJ, 1, 25};
   if (!tmap3(&A.tr, c.rho, N, N, N, N * 8, N * N * 8, kRW, kRH, 1) || !tmap4(&A.tp, cc.P, dp, sp, bp))
     return fail3(e, TMG_ECUDA, "tensor map encoding failed (k3_smr)");
+  A.pd = cc.Pd;
+  const uint64_t Ncp = (Nc + 3) / 4 * 4;
+  if (cc.Pd && !tmap3(&A.ti, cc.Pdi, Nc, Nc, Nc, Ncp * 4, Ncp * Nc * 4, kRIW, kRJ, 2,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_DATA_TYPE_UINT32))
+    return fail3(e, TMG_ECUDA, "tensor map encoding failed (k3_smr index)");
   const dim3 grid(tiles, (n + A.chunk - 1) / A.chunk);
   cudaEvent_t e0_ = nullptr;
   TRY3(begin_k(e, &e0_));
-  k3_smr<<<grid, kRThreads, kSmrSmem, e->s>>>(A);
+  if (cc.Pd) k3_smr<true><<<grid, kRThreads, kSmrSmemD, e->s>>>(A);
+  else k3_smr<false><<<grid, kRThreads, kSmrSmem, e->s>>>(A);
   CKL3();
   TRY3(end_k(e, kname("k3_smooth", l), e0_));
   return TMG_OK;
@@ -810,13 +842,119 @@ Op3 element_op(double c, bool is_const, const double* coef) {
   return o;
 }
 
-// the cube-owned copy of level l's P (k3_up_tma), after every change of P
+// Row dictionary of a plane-major weight array (kernels3d_dict.cu): *dict / *idx stay null when
+// a hash collision shows up or the rows do not repeat enough (D > R / 4) to pay for the index.
+int build_dict(Engine3* e, const RowsView& v, size_t R, bool force, double** dict, uint32_t** idx, size_t* Dp,
+               size_t* Dout) {
+  *dict = nullptr;
+  *idx = nullptr;
+  *Dp = *Dout = 0;
+  if (R < 2 || R > 0x7fffffffULL) return TMG_OK;
+  const int n = (int)R;
+  uint64_t *k0 = nullptr, *k1 = nullptr;
+  uint32_t *v0 = nullptr, *v1 = nullptr, *hs = nullptr, *rs = nullptr, *lead = nullptr, *first = nullptr,
+           *nid = nullptr;
+  int* bad = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0, t1 = 0, t2 = 0, t3b = 0;
+  int rc = TMG_OK;
+  auto done = [&](int r) {
+    for (void* p : {(void*)k0, (void*)k1, (void*)v0, (void*)v1, (void*)hs, (void*)rs, (void*)lead, (void*)first,
+                    (void*)nid, (void*)bad, tmp})
+      if (p) cudaFree(p);
+    return r;
+  };
+#define CKD(call)                                                                                 \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      return done(fail3(e, TMG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)));       \
+  } while (0)
+  CKD(cudaMalloc(&k0, 8 * R));
+  CKD(cudaMalloc(&k1, 8 * R));
+  CKD(cudaMalloc(&v0, 4 * R));
+  CKD(cudaMalloc(&v1, 4 * R));
+  CKD(cudaMalloc(&hs, 4 * R));
+  CKD(cudaMalloc(&rs, 4 * R));
+  CKD(cudaMalloc(&lead, 4 * R));
+  CKD(cudaMalloc(&first, 4 * R));
+  CKD(cudaMalloc(&nid, 4 * R));
+  CKD(cudaMalloc(&bad, sizeof(int)));
+  CKD(cudaMemsetAsync(bad, 0, sizeof(int), e->s));
+  CKD(cub::DeviceRadixSort::SortPairs(nullptr, t1, k0, k1, v0, v1, n, 0, 64, e->s));
+  CKD(cub::DeviceScan::InclusiveScan(nullptr, t2, hs, rs, MaxU32{}, n, e->s));
+  CKD(cub::DeviceScan::ExclusiveSum(nullptr, t3b, first, nid, n, e->s));
+  tb = std::max(t1, std::max(t2, t3b));
+  CKD(cudaMalloc(&tmp, tb));
+  const unsigned g = (unsigned)std::min<size_t>(nblk(R, 256), 148 * 16);
+  kd_hash<<<g, 256, 0, e->s>>>(v, R, k0, v0);
+  CKD(cudaGetLastError());
+  t1 = tb;
+  CKD(cub::DeviceRadixSort::SortPairs(tmp, t1, k0, k1, v0, v1, n, 0, 64, e->s));
+  kd_heads<<<g, 256, 0, e->s>>>(k1, R, hs);
+  CKD(cudaGetLastError());
+  t2 = tb;
+  CKD(cub::DeviceScan::InclusiveScan(tmp, t2, hs, rs, MaxU32{}, n, e->s));
+  kd_leader<<<g, 256, 0, e->s>>>(v1, rs, R, lead);
+  kd_verify<<<g, 256, 0, e->s>>>(v, lead, R, first, bad);
+  CKD(cudaGetLastError());
+  t3b = tb;
+  CKD(cub::DeviceScan::ExclusiveSum(tmp, t3b, first, nid, n, e->s));
+  int hbad = 0;
+  uint32_t last[2] = {0, 0};
+  CKD(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, e->s));
+  CKD(cudaMemcpyAsync(&last[0], nid + (R - 1), 4, cudaMemcpyDeviceToHost, e->s));
+  CKD(cudaMemcpyAsync(&last[1], first + (R - 1), 4, cudaMemcpyDeviceToHost, e->s));
+  CKD(cudaStreamSynchronize(e->s));
+  const size_t D = (size_t)last[0] + last[1];
+  if (hbad || (D > R / 4 && !force)) return done(TMG_OK);
+  const size_t dp = kDictW;
+  if ((rc = alloc3(e, dict, D * kDictW)) != TMG_OK) return done(rc);
+  if ((rc = alloc3(e, idx, R / v.iinner * v.ipitch)) != TMG_OK) return done(rc);
+  kd_fill<<<g, 256, 0, e->s>>>(v, lead, nid, R, *idx, *dict);
+  CKD(cudaGetLastError());
+  CKD(cudaStreamSynchronize(e->s));
+#undef CKD
+  *Dp = dp;
+  *Dout = D;
+  return done(TMG_OK);
+}
+
+// the cube-owned copy of level l's P (k3_up_tma), after every change of P; and, at setup (the
+// throttled path rewrites P every cycle), the row dictionaries of P and Pc (TMG_PDICT=0: dense)
 int refresh_pc(Engine3* e, int l) {
   Lvl3& c = e->L[l];
   if (!c.Pc) return TMG_OK;
-  const size_t nc = (size_t)c.N - 1;
-  k3_p_cube<<<nblk(nc * nc * nc, 128), 128, 0, e->s>>>(c.P, c.Pc, c.N, (int)((nc + kQK - 1) / kQK * kQK));
+  const size_t nc = (size_t)c.N - 1, Kp = (nc + kQK - 1) / kQK * kQK;
+  k3_p_cube<<<nblk(nc * nc * nc, 128), 128, 0, e->s>>>(c.P, c.Pc, c.N, (int)Kp);
   CKL3();
+  const char* env = std::getenv("TMG_PDICT");
+  if (e->cfg.throttled || (env && env[0] == '0') || l != e->ltop - 1 || c.Pd || c.Pcd) return TMG_OK;
+  const bool force = env && env[0] == '2';
+  // Pc's dictionary feeds k3_up_tma; P's feeds k3_smr, which is instruction-bound either way and
+  // measured slower on the dictionary (5.2 vs 4.2 ms at config 5), so it is opt-in (TMG_PDICT_SMR=1)
+  const char* es = std::getenv("TMG_PDICT_SMR");
+  const char* eu = std::getenv("TMG_PDICT_UP");
+  if (!(eu && eu[0] == '0'))
+    TRY3(build_dict(e, RowsView{c.Pc, nc, Kp, nc * nc * Kp, kQS, nc, Kp}, nc * nc * nc, force, &c.Pcd, &c.Pcdi,
+                    &c.Pcdp, &c.Pcdn));
+  if (c.Pcd) {  // k3_up_tma's step tables; a step meeting more than kQRows rows keeps the dense stream
+    const int tK = (int)((nc + kQK - 1) / kQK), tJ = (int)((nc + kQJ - 1) / kQJ);
+    const size_t cnt = nc * (size_t)tJ * tK;
+    TRY3(alloc3(e, &c.Ptab, cnt * kQTabBytes, false));
+    int* dover = nullptr;  // (e->deg may hold the setup's degenerate-collapse flag)
+    TRY3(alloc3(e, &dover, 1));
+    k3_up_tables<<<nblk(cnt, 128), 128, 0, e->s>>>(c.Pcdi, (int)nc, (int)Kp, tK, tJ, c.Ptab, dover);
+    CKL3();
+    int over = 0;
+    CK3(cudaMemcpyAsync(&over, dover, sizeof(int), cudaMemcpyDeviceToHost, e->s));
+    CK3(cudaStreamSynchronize(e->s));
+    if (over) c.Pcd = nullptr, c.Pcdn = 0;
+  }
+  if (es && es[0] == '1') {
+    const size_t Nc = c.N, Ncp = (Nc + 3) / 4 * 4;  // id rows padded to 16 bytes
+    TRY3(build_dict(e, RowsView{c.P, c.nv, 0, c.nv, 125, Nc, Ncp}, c.nv, force, &c.Pd, &c.Pdi, &c.Pdp, &c.Pdn));
+  }
   return TMG_OK;
 }
 
@@ -900,6 +1038,8 @@ int build(Engine3* e, const tmg_tree3* t) {
   CK3(cudaFuncSetAttribute(k3_smooth2r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2RSmemV));
   CK3(cudaFuncSetAttribute(k3_up_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpTmaSmem));
   CK3(cudaFuncSetAttribute(k3_up_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpTmaSmem));
+  CK3(cudaFuncSetAttribute(k3_up_dict<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpDictSmem));
+  CK3(cudaFuncSetAttribute(k3_up_dict<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpDictSmem));
   TRY3(alloc3(e, &e->deg, 1));
   e->thr_next = l0 - 1;
   if (cfg.flavor == TMG_GEOMETRIC) {
@@ -1045,7 +1185,8 @@ int build(Engine3* e, const tmg_tree3* t) {
              l1 - 1 > e->lc;
     e->smr_lo = e->lc + 2;  // every level whose coarser level is a grid (not chain) level
     if (e->smr) {
-      CK3(cudaFuncSetAttribute(k3_smr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmem));
+      CK3(cudaFuncSetAttribute(k3_smr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmem));
+      CK3(cudaFuncSetAttribute(k3_smr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmemD));
       for (int l = e->smr_lo - 1; l < l1; ++l) {
         Lvl3& cc = e->L[l];
         if (!cc.bR) TRY3(alloc3(e, &cc.bR, cc.nv));
@@ -1281,6 +1422,18 @@ int e3_phase(Engine3* e, int phase, int level, std::string& err) {
     --e->thr_next;
   }
   return phase3(e, phase, level);
+}
+
+int e3_storage(Engine3* e, int level, int64_t* out, std::string& err) {
+  e->err = &err;
+  TRY3(check_level(e, level));
+  const Lvl3& c = e->L[level];
+  const int64_t nc = c.N - 1;
+  out[0] = c.P ? (int64_t)c.nv : 0;
+  out[1] = c.Pd ? (int64_t)c.Pdn : 0;
+  out[2] = c.Pc ? nc * nc * nc : 0;
+  out[3] = c.Pcd ? (int64_t)c.Pcdn : 0;
+  return TMG_OK;
 }
 
 int e3_field(Engine3* e, int field, int level, uint64_t* ptr, int64_t* count, std::string& err) {

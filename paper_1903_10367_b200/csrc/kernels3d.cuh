@@ -25,6 +25,7 @@ constexpr int kTX = 32, kTY = 4, kTZ = 2;  // threads along k, j, i
 constexpr int kBlock = kTX * kTY * kTZ;
 constexpr int kChainBlock = 512;
 constexpr int kMaxLevels = 10;
+constexpr int kDictW = 128;  // weight-dictionary row pitch in doubles (kernels3d_dict.cu)
 
 enum OpKind : int { OP_CONST = 0, OP_ELEMENT = 1, OP_TABLE = 2 };
 enum Variant : int { VAR_ADDITIVE = 0, VAR_EXP = 1, VAR_BPX = 2, VAR_AFACC = 3, VAR_PI = 4, VAR_JAC = 5 };

@@ -46,6 +46,14 @@ constexpr int kSCols = 2 * kSPairs;
 static_assert(kSH % 2 == 0, "sm columns are paired along j");
 constexpr int oRP = kRStages * kRSlot, oRS = oRP + kPStages * 2 * kPBox;
 constexpr size_t kSmrSmem = sizeof(double) * (oRS + 2 * kSBuf);
+// dictionary variant: no P ring; with rho plane p (ring slot) its TMA also brings the tile's
+// dictionary ids of coarse planes floor3(p), floor3(p) + 1 (box 32 x 4 x 2 uint32)
+// (box from K0 - 1: TMA faults on box rows that do not start 16-byte aligned)
+constexpr int kRIW = kRK + 4;                  // 36 ids per row
+constexpr int kRIds = 2 * kRIW * kRJ / 2;      // in doubles (144: a 128-byte multiple)
+constexpr int oRId = kRStages * kRSlot;
+constexpr int oRSd = oRId + kRStages * kRIds;
+constexpr size_t kSmrSmemD = sizeof(double) * (oRSd + 2 * kSBuf);
 
 struct Smr {
   CUtensorMap tr;  // rho of the finest level, box {100, 16, 1}
@@ -56,6 +64,8 @@ struct Smr {
   double scale;    // omega*3/8
   double* bR;
   double* bT;
+  CUtensorMap ti;      // dictionary variant: ids of the coarse vertices {Nc, Nc, Nc} uint32, box {32, 4, 2}
+  const double* pd;    // P rows pd[id * kDictW + slot]
 };
 
 __device__ __forceinline__ int floor3s(int x) { return x >= 0 ? x / 3 : -((2 - x) / 3); }
@@ -63,6 +73,10 @@ __device__ __forceinline__ int floor3s(int x) { return x >= 0 ? x / 3 : -((2 - x
 // Warp-specialised: threads [0, 256) complete sm(t-1) from rho(t) (phase C) while threads
 // [256, 512) restrict fine plane t-2 (phase D, one step behind, sm double buffered), so the two
 // latency-bound phases overlap; one CTA barrier per step.
+// DICT: level ltop-1's P as a row dictionary (kernels3d_dict.cu): no P ring, each restriction
+// thread reads its vertex's weights from the plane-major dictionary (L1-cached, the rows of a
+// warp's vertices have neighbouring ids), the same doubles in the same order.
+template <bool DICT>
 __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ Smr A) {
   extern __shared__ __align__(128) double sr[];
   __shared__ __align__(8) uint64_t bar[kRStages], pbar[kPStages];
@@ -74,6 +88,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
   const int fk0 = 3 * K0 - 3, fj0 = 3 * J0 - 3;  // rho window origin (fine)
   const int p0 = 3 * Ia - 3, pEnd = 3 * Ib;       // rho planes streamed: [p0, pEnd]
   const int s0 = 3 * Ia - 2;                      // fine planes restricted: [s0, pEnd - 1]
+  constexpr int oS = DICT ? oRSd : oRS;           // sm double buffer
   const int lt = threadIdx.x;
   const bool smoother = lt < kRTasks;
 
@@ -106,10 +121,12 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
 
   auto issue_r = [&](int p) {  // rho plane p into its slot
     const int sl = (p - p0) % kRStages;
-    mbar_expect_tx(&bar[sl], (unsigned)(sizeof(double) * kRW * kRH));
+    mbar_expect_tx(&bar[sl], (unsigned)(sizeof(double) * kRW * kRH) + (DICT ? 8u * kRIds : 0u));
     tma_load_3d(sr + sl * kRSlot, &A.tr, &bar[sl], fk0, fj0, p);
+    if (DICT) tma_load_3d(sr + oRId + sl * kRIds, &A.ti, &bar[sl], K0 - 1, J0, floor3s(p));
   };
   auto issue_p = [&](int s) {  // the P boxes fine plane s meets into its set
+    if (DICT) return;
     const int sl = (s - s0) % kPStages;
     const int m3 = floor3s(s), o = s - 3 * m3;
     const bool c = m3 >= Ia && m3 < Ib, nx = o >= 1 && m3 + 1 >= Ia && m3 + 1 < Ib;
@@ -147,7 +164,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
       if (t <= pEnd) mbar_wait(&bar[r % kRStages], (unsigned)(r / kRStages) & 1u);
       if (A.jac && t <= pEnd) {
         const double* Rp = sr + (r % kRStages) * kRSlot;
-        double* Sb = sr + oRS + ((t - 1) & 1) * kSBuf;
+        double* Sb = sr + oS + ((t - 1) & 1) * kSBuf;
         const bool sok = t - 1 >= 1 && t - 1 <= N - 2;
 #pragma unroll
         for (int mp = 0; mp < kSPairs; ++mp) {
@@ -185,7 +202,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
       const int s = t - 2;
       if (s >= s0) {
         const int ps = s - s0, rs_ = s - p0;
-        mbar_wait(&pbar[ps % kPStages], (unsigned)(ps / kPStages) & 1u);
+        if (!DICT) mbar_wait(&pbar[ps % kPStages], (unsigned)(ps / kPStages) & 1u);
         mbar_wait(&bar[rs_ % kRStages], (unsigned)(rs_ / kRStages) & 1u);  // rho(s): visibility of the TMA write
         const double* Pset = sr + oRP + (ps % kPStages) * 2 * kPBox + wj * kPW + wk + 1;
         if (rtask) {
@@ -196,17 +213,26 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
             src = sr + (rs_ % kRStages) * kRSlot + (3 * wj + 3) * kRW + 3 * wk + 3;
             ld = kRW;
           } else {
-            src = sr + oRS + (s & 1) * kSBuf + (3 * wj + 2) * kSW + 3 * wk + 2;
+            src = sr + oS + (s & 1) * kSBuf + (3 * wj + 2) * kSW + 3 * wk + 2;
             ld = kSW;
           }
           const bool zc = fld == 0 && A.zc;
+          // DICT: the weights of slots (o + 2) * 25 + q (plane m3) / (o - 1) * 25 + q (plane m3 + 1)
+          const double* wc = nullptr;
+          const double* wn = nullptr;
+          if (DICT) {  // ids of coarse planes m3, m3 + 1 arrived with rho(s); rows are 128 doubles
+            const uint32_t* ids =
+                reinterpret_cast<const uint32_t*>(sr + oRId + (rs_ % kRStages) * kRIds) + wj * kRIW + wk + 1;
+            wc = A.pd + (size_t)ids[0] * kDictW + (o + 2) * 25;
+            wn = A.pd + (size_t)ids[kRIW * kRJ] * kDictW + (o - 1) * 25;
+          }
           if (m3 >= Ia && m3 < Ib) {  // coarse plane m3, fine offset o in {0, 1, 2}
             double acc = accC;
 #pragma unroll
             for (int q = 0; q < 25; ++q) {
               const int oj = q / 5 - 2, ok = q % 5 - 2;
               const bool ctr = o == 0 && q == 12;
-              const double wt = ctr ? 1.0 : Pset[q * kRJ * kPW];
+              const double wt = ctr ? 1.0 : DICT ? __ldg(wc + q) : Pset[q * kRJ * kPW];
               double x = src[oj * ld + ok];
               if (ctr && zc) x = 0.0;
               acc = acc + wt * x;
@@ -219,7 +245,8 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
 #pragma unroll
             for (int q = 0; q < 25; ++q) {
               const int oj = q / 5 - 2, ok = q % 5 - 2;
-              acc = acc + Pset[kPBox + q * kRJ * kPW] * src[oj * ld + ok];
+              const double wt = DICT ? __ldg(wn + q) : Pset[kPBox + q * kRJ * kPW];
+              acc = acc + wt * src[oj * ld + ok];
             }
             accN = acc;
           }

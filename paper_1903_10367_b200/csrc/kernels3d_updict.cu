@@ -1,0 +1,279 @@
+// BoxMG prolongation of the finest level over the row dictionary of the
+// cube-owned weights (k3_up_dict; kernels3d_dict.cu builds the dictionary).
+//
+// k3_up_tma streams 124 weights per coarse cube from HBM (14.5 GB of its 23.6 GB
+// per config-5 cycle).  Where the coefficient is blockwise constant, those rows
+// are repeats of a few thousand distinct rows, so here only u, g and the coarse
+// carry stream from HBM and the weights come from the dictionary (L2-resident):
+//
+//   step = one layer I of a 32 (K) x 2 (J) tile of coarse cubes (as k3_up_tma)
+//   table(step)  256 B, setup-built (k3_up_tables): the step's distinct rows
+//                (<= kQRows) and each cube's index into them
+//   rows(step)   one 992-byte bulk copy per distinct row, from L2
+//   u, g, carry  TMA boxes (evict-first in L2, so the dictionary stays)
+//
+// Warp-specialised: warp 6 is the producer -- it keeps the three rings (slots,
+// tables, rows) ahead of the consumers, and after the consumers of a step have
+// arrived on its `done` barrier stores the step's u with one TMA store and
+// refills the slot.  Warps 0-5 are consumers: cube fine planes ri = 0, 1, 2 on
+// two warps each (32 cubes along K per warp), weights from the staged rows in
+// shared memory.  Per fine vertex the DAG is k3_up_tile's (corners d = 7..0,
+// weight 1.0 at the centre slot), so the iterate is bitwise unchanged.
+#include <type_traits>
+
+#include "kernels3d.cuh"
+
+namespace t3 {
+
+constexpr int kQRows = 32, kQRowS = 130;  // rows per step (cap), row stride in doubles (1040 B)
+constexpr int kQTabBytes = 256;           // {n, ids[kQRows]} uint32, local[64] uint8 at byte 132
+constexpr int oDU = 0, oDG = qal16(kQUd), oDC = oDG + qal16(kQUd);
+constexpr int kDSlot = oDC + qal16(kQCd);
+constexpr int kDNS = 3, kDNT = 8, kDTD = 6, kDNR = 4, kDRD = 3;
+constexpr int kDCons = 6 * 32, kDThreads = kDCons + 32;  // consumers + one producer warp
+constexpr int oDTab = kDNS * kDSlot, oDRows = oDTab + kDNT * kQTabBytes / 8, kDRowSlot = kQRows * kQRowS;
+constexpr size_t kUpDictSmem = sizeof(double) * (oDRows + kDNR * kDRowSlot);
+constexpr unsigned kDBytes = (unsigned)sizeof(double) * (2 * kQUd + kQCd);
+constexpr unsigned kDRowBytes = (unsigned)sizeof(double) * kQS;  // 992 of a row's 1 KB
+
+struct UpD {
+  CUtensorMap tu, tg, tc;  // as k3_up_tma
+  Up3 a;
+  const double* dict;      // Pc rows dict[id * kDictW + q]
+  const uint8_t* tab;      // step tables, index (I * tilesJ + J0 / 2) * tilesK + K0 / 32
+  int tilesK, tilesJ, nI, I0, steps, per;
+};
+
+// step tables: one thread per (layer I, J tile, K tile); *over = 1 when a step meets more than
+// kQRows distinct rows (the dense stream is kept then)
+__global__ void k3_up_tables(const uint32_t* __restrict__ ids, int nc, int Kp, int tilesK, int tilesJ,
+                             uint8_t* __restrict__ tab, int* over) {
+  const size_t cnt = (size_t)nc * tilesJ * tilesK;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += (size_t)gridDim.x * blockDim.x) {
+    const int tk = (int)(t % tilesK), tj = (int)((t / tilesK) % tilesJ), I = (int)(t / ((size_t)tilesK * tilesJ));
+    uint32_t rows[kQRows];
+    uint8_t loc[kQT];
+    int n = 0;
+    for (int c = 0; c < kQT; ++c) {
+      const int J = tj * kQJ + c / kQK, K = tk * kQK + c % kQK;
+      loc[c] = 0;
+      if (J >= nc || K >= nc) continue;
+      const uint32_t id = ids[((size_t)I * nc + J) * Kp + K];
+      int m = 0;
+      while (m < n && rows[m] != id) ++m;
+      if (m == n) {
+        if (n == kQRows) {
+          atomicOr(over, 1);
+          m = 0;
+        } else {
+          rows[n++] = id;
+        }
+      }
+      loc[c] = (uint8_t)m;
+    }
+    uint32_t* T = reinterpret_cast<uint32_t*>(tab + t * kQTabBytes);
+    T[0] = (uint32_t)n;
+    for (int m = 0; m < kQRows; ++m) T[1 + m] = m < n ? rows[m] : 0u;
+    for (int c = 0; c < kQT; ++c) tab[t * kQTabBytes + 132 + c] = loc[c];
+  }
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+// streamed boxes marked evict-first in L2 (the dictionary they would push out is reused)
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_3d_ef(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               int c2, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3, %4}], [%5], %6;" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d_ef(const CUtensorMap* map, const void* src, int c0, int c1, int c2,
+                                                uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;" ::
+                   "l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(src)), "l"(pol)
+               : "memory");
+}
+
+template <bool CARRY>
+__global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant__ UpD A) {
+  extern __shared__ __align__(128) double sq[];
+  __shared__ __align__(8) uint64_t full[kDNS], done[kDNS], tful[kDNT], rful[kDNR];
+  const Up3& a = A.a;
+  const int Nc = a.Nc, nc = Nc - 1, N = a.N;
+  const int lt = threadIdx.x;
+  const int s0 = blockIdx.x * A.per, s1 = min(A.steps, s0 + A.per);
+  if (s0 >= s1) return;
+  auto coords = [&](int s, int& I, int& J0, int& K0) {  // 32-bit: steps < 2^31
+    const int t = s / A.nI;
+    I = A.I0 + (s - t * A.nI);
+    const int tj = t / A.tilesK;
+    K0 = (t - tj * A.tilesK) * kQK;
+    J0 = tj * kQJ;
+  };
+  auto tab_of = [&](int r) { return reinterpret_cast<const uint8_t*>(sq + oDTab + (r % kDNT) * (kQTabBytes / 8)); };
+  if (lt == 0) {
+    for (int q = 0; q < kDNS; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&done[q], kDCons / 32);
+    }
+    for (int q = 0; q < kDNT; ++q) mbar_init(&tful[q], 1);
+    for (int q = 0; q < kDNR; ++q) mbar_init(&rful[q], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (lt >= kDCons) {  // ---------------- producer warp ----------------
+    if (lt != kDCons) return;
+    const uint64_t pol = policy_evict_first();
+    auto load = [&](int s) {  // u, g, carry_c of step s into slot (s - s0) % kDNS
+      int I, J0, K0;
+      coords(s, I, J0, K0);
+      const int r = s - s0;
+      double* b = sq + (r % kDNS) * kDSlot;
+      uint64_t* br = &full[r % kDNS];
+      mbar_expect_tx(br, kDBytes);
+      tma_load_3d_ef(b + oDG, &A.tg, br, 3 * K0, 3 * J0, 3 * I, pol);
+      tma_load_3d(b + oDC, &A.tc, br, K0, J0, I);
+      tma_load_3d_ef(b + oDU, &A.tu, br, 3 * K0, 3 * J0, 3 * I, pol);
+    };
+    auto table = [&](int s) {
+      int I, J0, K0;
+      coords(s, I, J0, K0);
+      const int r = s - s0;
+      mbar_expect_tx(&tful[r % kDNT], kQTabBytes);
+      bulk_load(sq + oDTab + (r % kDNT) * (kQTabBytes / 8),
+                A.tab + (((size_t)I * A.tilesJ + J0 / kQJ) * A.tilesK + K0 / kQK) * kQTabBytes, kQTabBytes,
+                &tful[r % kDNT]);
+    };
+    auto rows = [&](int s) {  // the table of step s is in (waited here)
+      const int r = s - s0;
+      mbar_wait(&tful[r % kDNT], (unsigned)(r / kDNT) & 1u);
+      const uint32_t* T = reinterpret_cast<const uint32_t*>(tab_of(r));
+      const int n = (int)T[0];
+      double* R = sq + oDRows + (r % kDNR) * kDRowSlot;
+      uint64_t* rb = &rful[r % kDNR];
+      mbar_expect_tx(rb, kDRowBytes * (unsigned)n);
+      for (int m = 0; m < n; ++m) bulk_load(R + m * kQRowS, A.dict + (size_t)T[1 + m] * kDictW, kDRowBytes, rb);
+    };
+    for (int s = s0; s < min(s1, s0 + kDNS); ++s) load(s);
+    for (int s = s0; s < min(s1, s0 + kDTD); ++s) table(s);
+    for (int s = s0; s < min(s1, s0 + kDRD); ++s) rows(s);
+    for (int k = s0; k < s1; ++k) {  // step k computed -> store it, refill the rings
+      const int r = k - s0;
+      mbar_wait(&done[r % kDNS], (unsigned)(r / kDNS) & 1u);
+      int I, J0, K0;
+      coords(k, I, J0, K0);
+      fence_proxy_async();
+      tma_store_3d_ef(&A.tu, sq + (r % kDNS) * kDSlot + oDU, 3 * K0, 3 * J0, 3 * I, pol);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      // the table slot of step k + kDTD last held step k + kDTD - kDNT (< k: done); the row slot of
+      // step k + kDRD last held step k + kDRD - kDNR (<= k: done)
+      if (k + kDTD < s1) table(k + kDTD);
+      if (k + kDRD < s1) rows(k + kDRD);
+      if (k + kDNS < s1) {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // step k's u left the slot
+        load(k + kDNS);
+      }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    return;
+  }
+
+  // ---------------- consumers: warps 0-5, cube plane ri = warp / 2 ----------------
+  const int rg = lt >> 6, cl = lt & 63, tx = cl & 31, ty = cl >> 5;
+  int I, J0, K0;  // coordinates of step s, advanced incrementally
+  coords(s0, I, J0, K0);
+  for (int s = s0; s < s1; ++s) {
+    const int r = s - s0;
+    if (s > s0 && ++I == A.I0 + A.nI) {
+      I = A.I0;
+      K0 += kQK;
+      if (K0 >= A.tilesK * kQK) {
+        K0 = 0;
+        J0 += kQJ;
+      }
+    }
+    double* b = sq + (r % kDNS) * kDSlot;
+    mbar_wait(&full[r % kDNS], (unsigned)(r / kDNS) & 1u);
+    mbar_wait(&tful[r % kDNT], (unsigned)(r / kDNT) & 1u);
+    mbar_wait(&rful[r % kDNR], (unsigned)(r / kDNR) & 1u);
+    const int J = J0 + ty, K = K0 + tx;
+    if (J < nc && K < nc) {
+      const double* Wd = sq + oDRows + (r % kDNR) * kDRowSlot + kQRowS * tab_of(r)[132 + cl];
+      const double* Gs = b + oDG;
+      const double* Cs = b + oDC;
+      double* Us = b + oDU;
+      double c[2][2][2];
+#pragma unroll
+      for (int di = 0; di < 2; ++di)
+#pragma unroll
+        for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+          for (int dk = 0; dk < 2; ++dk) c[di][dj][dk] = Cs[(di * kQCJ + ty + dj) * kQCK + tx + dk];
+      auto run = [&](auto R0) {  // fine plane ri of the cube; q = its first stored term
+        constexpr int ri = decltype(R0)::value;
+        int q = ri == 0 ? 0 : ri == 1 ? 24 : 74;
+#pragma unroll
+        for (int rj = 0; rj < 3; ++rj)
+#pragma unroll
+          for (int rk = 0; rk < 3; ++rk) {
+            double acc = 0.0;
+#pragma unroll
+            for (int d = 7; d >= 0; --d) {
+              const int di = (d >> 2) & 1, dj = (d >> 1) & 1, dk = d & 1;
+              if ((di && !ri) || (dj && !rj) || (dk && !rk)) continue;
+              const int sl = pslot(ri - 3 * di, rj - 3 * dj, rk - 3 * dk);
+              double wt = 1.0;
+              if (sl != 62) {
+                wt = Wd[q];
+                ++q;
+              }
+              acc = acc + wt * c[di][dj][dk];
+            }
+            const int i = 3 * I + ri;  // fine planes outside [ilo, ihi) stay as loaded
+            const bool skip = i < a.ilo || i >= a.ihi || (rj == 0 && J == 0) || (rk == 0 && K == 0);
+            if (!skip) {
+              const int o = (ri * kQFJ + 3 * ty + rj) * kQFK + 3 * tx + rk;
+              const double cv = acc + Gs[o];
+              const double un = Us[o] + cv;
+              Us[o] = un;
+              if (CARRY) a.carry[vid(N, i, 3 * J + rj, 3 * K + rk)] = cv;
+              if (ri == 0 && rj == 0 && rk == 0) {  // FAS walk-down injection
+                int ii = I, jj = J, kk = K;
+                for (int lc = a.l - 1; lc >= a.l0; --lc) {
+                  a.ul[lc][vid(a.Nl[lc], ii, jj, kk)] = un;
+                  if (ii % 3 || jj % 3 || kk % 3) break;
+                  ii /= 3;
+                  jj /= 3;
+                  kk /= 3;
+                }
+              }
+            }
+          }
+      };
+      if (rg == 0) run(std::integral_constant<int, 0>{});
+      else if (rg == 1) run(std::integral_constant<int, 1>{});
+      else run(std::integral_constant<int, 2>{});
+    }
+    fence_proxy_async();  // this thread's generic-proxy writes of u, before the async-proxy store
+    __syncwarp();
+    if ((lt & 31) == 0) mbar_arrive(&done[r % kDNS]);
+  }
+}
+
+}  // namespace t3

@@ -383,6 +383,13 @@ class GpuEngine:
         self._host_stale = True
         return {names[k].decode(): (ms[k], cnt[k]) for k in range(nk.value)}
 
+    def weight_storage(self, level: int) -> dict:
+        """3D: how level `level`'s BoxMG weights are stored (``tmg3_storage``): rows of P and
+        of its cube-owned copy, and the distinct rows of their dictionaries (0 = dense)."""
+        out = (C.c_int64 * 4)()
+        _abi.check(_abi.lib().tmg3_storage(self._h, level, out))
+        return {"p_rows": out[0], "p_distinct": out[1], "pc_rows": out[2], "pc_distinct": out[3]}
+
     def launches_per_cycle(self) -> int:
         n = C.c_int32()
         _abi.check(_abi.lib().tmg_launches_per_cycle(self._h, C.byref(n)))

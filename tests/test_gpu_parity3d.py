@@ -217,3 +217,50 @@ def test_3d_prolongation_stream_equals_tile(variant, throttled, monkeypatch):
     assert [s.linf for s in h1] == [s.linf for s in h2]
     for l in range(1, 6):
         assert np.array_equal(wl1.tree.u[l], wl2.tree.u[l]), f"level {l}"
+
+
+@pytest.mark.parametrize("variant", ["adafac-jac", "additive", "afacc"])
+@pytest.mark.parametrize("wname", ["config5-L5", "random-L5"])
+def test_3d_weight_dictionary_equals_dense(variant, wname, monkeypatch):
+    """Level ltop-1's BoxMG weights as bitwise-verified row dictionaries (k3_smr's DICT variant,
+    k3_up_dict; TMG_PDICT=2 forces them even where rows barely repeat) give the same iterate,
+    bit for bit, as the dense P / Pc streams (TMG_PDICT=0)."""
+    def make():
+        if wname == "config5-L5":
+            return workloads.config5(levels=5, block=27)  # config 5's block size (9 level-4 cells)
+        wl = workloads.by_name("config5-L5")
+        rng = np.random.default_rng(7)
+        wl.tree.eps[5][...] = 10.0 ** rng.uniform(-2, 2, wl.tree.eps[5].shape)  # per-cell: few repeats
+        return wl
+
+    n = 4
+    monkeypatch.setenv("TMG_PDICT", "2")
+    monkeypatch.setenv("TMG_PDICT_SMR", "1")
+    wl1 = make()
+    e1, h1 = gpu_run(wl1, n, variant)
+    st = e1.weight_storage(4)
+    assert 0 < st["p_distinct"] <= st["p_rows"], st
+    if wname == "config5-L5":
+        assert 0 < st["pc_distinct"] <= st["pc_rows"], st
+    else:  # per-cell coefficients: a prolongation step meets > 32 distinct rows, dense stream kept
+        assert st["pc_distinct"] == 0, st
+    monkeypatch.setenv("TMG_PDICT", "0")
+    wl2 = make()
+    e2, h2 = gpu_run(wl2, n, variant)
+    assert e2.weight_storage(4)["p_distinct"] == 0
+    assert [s.l2h for s in h1] == [s.l2h for s in h2]
+    assert [s.linf for s in h1] == [s.linf for s in h2]
+    for l in range(1, 6):
+        assert np.array_equal(wl1.tree.u[l], wl2.tree.u[l]), f"level {l}"
+
+
+def test_3d_weight_dictionary_default_on_blocks():
+    """On blockwise-constant coefficients (config 5's structure) the default setup stores level
+    ltop-1's cube-owned weights (the prolongation's) as a dictionary: far fewer distinct rows
+    than coarse cubes; P itself stays dense for the restriction unless TMG_PDICT_SMR=1."""
+    wl = workloads.config5(levels=5, block=27)  # config 5's block size (9 level-4 cells)
+    eng, _ = gpu_run(wl, 1)
+    st = eng.weight_storage(wl.tree.depth - 1)
+    print(st)
+    assert st["p_distinct"] == 0, st
+    assert 0 < st["pc_distinct"] <= st["pc_rows"] // 4, st
