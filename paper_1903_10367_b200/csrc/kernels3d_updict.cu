@@ -29,8 +29,8 @@ constexpr int kQRows = 32, kQRowS = 130;  // rows per step (cap), row stride in 
 constexpr int kQTabBytes = 256;           // {n, ids[kQRows]} uint32, local[64] uint8 at byte 132
 constexpr int oDU = 0, oDG = qal16(kQUd), oDC = oDG + qal16(kQUd);
 constexpr int kDSlot = oDC + qal16(kQCd);
-constexpr int kDNS = 3, kDNT = 8, kDTD = 6, kDNR = 4, kDRD = 3;
-constexpr int kDCons = 6 * 32, kDThreads = kDCons + 32;  // consumers + one producer warp
+constexpr int kDNS = 3, kDNT = 8, kDTD = 6, kDNR = 4, kDRD = 3, kDPF = 4;
+constexpr int kDCons = 6 * 32, kDThreads = kDCons + 64;  // consumers + two producer warps
 constexpr int oDTab = kDNS * kDSlot, oDRows = oDTab + kDNT * kQTabBytes / 8, kDRowSlot = kQRows * kQRowS;
 constexpr size_t kUpDictSmem = sizeof(double) * (oDRows + kDNR * kDRowSlot);
 constexpr unsigned kDBytes = (unsigned)sizeof(double) * (2 * kQUd + kQCd);
@@ -83,6 +83,15 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
                    smem_addr(dst)),
                "l"(src), "r"(bytes), "r"(smem_addr(bar))
                : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
@@ -138,7 +147,11 @@ __global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant
   __syncthreads();
 
   if (lt >= kDCons) {  // ---------------- producer warp ----------------
-    if (lt != kDCons) return;
+    // warp 6 streams (lane 0: the TMA boxes, the u stores -- bulk groups are per thread); warp 7
+    // stages (lane 0: the tables; lanes 0..n-1: a step's row copies in parallel)
+    const int lane = (lt - kDCons) & 31;
+    const bool streamer = lt < kDCons + 32;
+    const bool l0 = lane == 0;
     const uint64_t pol = policy_evict_first();
     auto load = [&](int s) {  // u, g, carry_c of step s into slot (s - s0) % kDNS
       int I, J0, K0;
@@ -150,6 +163,15 @@ __global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant
       tma_load_3d_ef(b + oDG, &A.tg, br, 3 * K0, 3 * J0, 3 * I, pol);
       tma_load_3d(b + oDC, &A.tc, br, K0, J0, I);
       tma_load_3d_ef(b + oDU, &A.tu, br, 3 * K0, 3 * J0, 3 * I, pol);
+    };
+    // L2 prefetch of step s's streamed boxes and table, kDPF steps before their loads
+    auto prefetch = [&](int s) {
+      int I, J0, K0;
+      coords(s, I, J0, K0);
+      tma_prefetch_3d(&A.tg, 3 * K0, 3 * J0, 3 * I);
+      tma_prefetch_3d(&A.tu, 3 * K0, 3 * J0, 3 * I);
+      tma_prefetch_3d(&A.tc, K0, J0, I);
+      bulk_prefetch(A.tab + (((size_t)I * A.tilesJ + J0 / kQJ) * A.tilesK + K0 / kQK) * kQTabBytes, kQTabBytes);
     };
     auto table = [&](int s) {
       int I, J0, K0;
@@ -165,32 +187,45 @@ __global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant
       mbar_wait(&tful[r % kDNT], (unsigned)(r / kDNT) & 1u);
       const uint32_t* T = reinterpret_cast<const uint32_t*>(tab_of(r));
       const int n = (int)T[0];
-      double* R = sq + oDRows + (r % kDNR) * kDRowSlot;
       uint64_t* rb = &rful[r % kDNR];
-      mbar_expect_tx(rb, kDRowBytes * (unsigned)n);
-      for (int m = 0; m < n; ++m) bulk_load(R + m * kQRowS, A.dict + (size_t)T[1 + m] * kDictW, kDRowBytes, rb);
+      if (l0) mbar_expect_tx(rb, kDRowBytes * (unsigned)n);
+      __syncwarp();
+      if (lane < n)
+        bulk_load(sq + oDRows + (r % kDNR) * kDRowSlot + lane * kQRowS, A.dict + (size_t)T[1 + lane] * kDictW,
+                  kDRowBytes, rb);
     };
-    for (int s = s0; s < min(s1, s0 + kDNS); ++s) load(s);
-    for (int s = s0; s < min(s1, s0 + kDTD); ++s) table(s);
+    if (streamer) {
+      if (!l0) return;
+      for (int s = s0; s < min(s1, s0 + kDNS); ++s) load(s);
+      for (int s = s0 + kDNS; s < min(s1, s0 + kDNS + kDPF); ++s) prefetch(s);
+      for (int k = s0; k < s1; ++k) {  // step k computed -> store its u, refill its slot
+        const int r = k - s0;
+        mbar_wait(&done[r % kDNS], (unsigned)(r / kDNS) & 1u);
+        int I, J0, K0;
+        coords(k, I, J0, K0);
+        fence_proxy_async();
+        tma_store_3d_ef(&A.tu, sq + (r % kDNS) * kDSlot + oDU, 3 * K0, 3 * J0, 3 * I, pol);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (k + kDNS < s1) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // step k's u left the slot
+          load(k + kDNS);
+        }
+        if (k + kDNS + kDPF < s1) prefetch(k + kDNS + kDPF);
+      }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      return;
+    }
+    if (l0)
+      for (int s = s0; s < min(s1, s0 + kDTD); ++s) table(s);
     for (int s = s0; s < min(s1, s0 + kDRD); ++s) rows(s);
-    for (int k = s0; k < s1; ++k) {  // step k computed -> store it, refill the rings
+    for (int k = s0; k < s1; ++k) {  // step k computed -> its table / row slots are free
       const int r = k - s0;
       mbar_wait(&done[r % kDNS], (unsigned)(r / kDNS) & 1u);
-      int I, J0, K0;
-      coords(k, I, J0, K0);
-      fence_proxy_async();
-      tma_store_3d_ef(&A.tu, sq + (r % kDNS) * kDSlot + oDU, 3 * K0, 3 * J0, 3 * I, pol);
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      // the table slot of step k + kDTD last held step k + kDTD - kDNT (< k: done); the row slot of
-      // step k + kDRD last held step k + kDRD - kDNR (<= k: done)
-      if (k + kDTD < s1) table(k + kDTD);
+      // the table slot of step k + kDTD last held step k + kDTD - kDNT (< k: done)
+      if (l0 && k + kDTD < s1) table(k + kDTD);
+      // the row slot of step k + kDRD last held step k + kDRD - kDNR (<= k: done)
       if (k + kDRD < s1) rows(k + kDRD);
-      if (k + kDNS < s1) {
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // step k's u left the slot
-        load(k + kDNS);
-      }
     }
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     return;
   }
 
