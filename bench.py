@@ -375,6 +375,9 @@ def run_ours(args, dist: Dist):
     eng.rhs.update(wl.rhs)
     eng.advance_many(max(args.warmup, 3))
     launches = eng.launches_per_cycle()
+    # level ltop-1's BoxMG weights: dense or row dictionary (kernels3d_dict.cu), as built at setup
+    storage = (eng.weight_storage(wl.ltop - 1) if wl.dim == 3 and wl.flavor == "boxmg" and wl.ltop > wl.tree.lmin
+               else None)
     updates = eng.advance_many(1)[0].updates  # count_updates (solvers.py:449-459)
     clk = ClockSampler(dev)
     clk.start()
@@ -512,7 +515,8 @@ def run_ours(args, dist: Dist):
                        "parallelism": "replicas" if dist.ws > 1 else "single",
                        "l2": f"flushed ({FLUSH_BYTES >> 20} MiB write) before every timed cycle",
                        "ms_per_step_l2_warm": ms_warm / args.steps,
-                       "total_updates_per_s": dist.ws * updates / (ms_step * 1e-3)},
+                       "total_updates_per_s": dist.ws * updates / (ms_step * 1e-3),
+                       "weight_storage": storage},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "time_to_1e-8": ttt,
             "gpu_launches": launches * args.steps,

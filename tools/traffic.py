@@ -38,7 +38,7 @@ assert starts, "no 3D cycle in the launch list"
 res = {}
 cur = up = None
 for e in seq[starts[-2] if len(starts) > 1 else starts[-1]:]:
-    fn = e["name"].split("(")[0].replace("void ", "").split("<")[0]
+    fn = e["name"].split("(")[0].replace("void ", "").split("<")[0].split("::")[-1]
     b = e.get("dram__bytes_read.sum", 0) + e.get("dram__bytes_write.sum", 0)
     if fn.startswith("k3_top") or fn == "k3_ffp":
         if res.get(f"k3_down_L{top}") is not None and cur is not None:
