@@ -929,7 +929,7 @@ int refresh_pc(Engine3* e, int l) {
   k3_p_cube<<<nblk(nc * nc * nc, 128), 128, 0, e->s>>>(c.P, c.Pc, c.N, (int)Kp);
   CKL3();
   const char* env = std::getenv("TMG_PDICT");
-  if (e->cfg.throttled || (env && env[0] == '0') || l != e->ltop - 1 || c.Pd || c.Pcd) return TMG_OK;
+  if (e->cfg.throttled || (env && env[0] == '0') || l < e->ltop - 2 || c.Pd || c.Pcd) return TMG_OK;
   const bool force = env && env[0] == '2';
   // Pc's dictionary feeds k3_up_tma; P's feeds k3_smr, which is instruction-bound either way and
   // measured slower on the dictionary (5.2 vs 4.2 ms at config 5), so it is opt-in (TMG_PDICT_SMR=1)

@@ -40,7 +40,7 @@ constexpr int kRStages = 5;                        // rho plane ring
 constexpr int kPW = kRK + 2;                       // P box rows from K0 - 1 (16-byte aligned start): 34
 constexpr int kPBox = (kPW * kRJ * 25 + 15) / 16 * 16;  // one 25-slot P box (27.2 KB; 128-byte multiple)
 constexpr int kPStages = 2;                        // P sets (two boxes each)
-constexpr int kSBuf = (kSW * kSH + 15) / 16 * 16;  // one sm plane (double buffered)
+constexpr int kSBuf = (kRW * kSH + 15) / 16 * 16;  // one sm plane (double buffered), pitch kRW like rho's
 constexpr int kSPairs = (kSW * (kSH / 2) + kRTasks - 1) / kRTasks;  // 3 pairs of sm columns per smoothing thread
 constexpr int kSCols = 2 * kSPairs;
 static_assert(kSH % 2 == 0, "sm columns are paired along j");
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
             double sc = (((SCa[m] + d0) + d1) + d2) + d3;
             double v = ((C_D8 * XA[m]) - (C_E6 * se)) - (C_C12 * sc);
             v = v * A.scale;
-            Sb[(2 * jp + h) * kSW + kk] = (sok && sin_[m]) ? v : 0.0;
+            Sb[(2 * jp + h) * kRW + kk] = (sok && sin_[m]) ? v : 0.0;
             SEa[m] = (((SEb[m] + d0) + d1) + d2) + d3;
             SCa[m] = SCb[m];
             XA[m] = xc;
@@ -208,13 +208,11 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
         if (rtask) {
           const int m3 = floor3s(s), o = s - 3 * m3;
           const double* src;
-          int ld;
+          constexpr int ld = kRW;  // both windows: immediate offsets in the sums
           if (fld == 0) {
             src = sr + (rs_ % kRStages) * kRSlot + (3 * wj + 3) * kRW + 3 * wk + 3;
-            ld = kRW;
           } else {
-            src = sr + oS + (s & 1) * kSBuf + (3 * wj + 2) * kSW + 3 * wk + 2;
-            ld = kSW;
+            src = sr + oS + (s & 1) * kSBuf + (3 * wj + 2) * kRW + 3 * wk + 2;
           }
           const bool zc = fld == 0 && A.zc;
           // DICT: the weights of slots (o + 2) * 25 + q (plane m3) / (o - 1) * 25 + q (plane m3 + 1)
