@@ -142,11 +142,13 @@ int tmg3_shard(tmg_handle* h, int32_t ls, const int32_t* lo, const int32_t* hi);
 int tmg3_phase(tmg_handle* h, int32_t phase, int32_t level);
 /* device address and element count of a field of a level (zero-copy views) */
 int tmg3_field(tmg_handle* h, int32_t field, int32_t level, uint64_t* ptr, int64_t* count);
-/* storage of level `level`'s BoxMG weights (no reference counterpart): out[0] rows of P
+/* storage of level `level`'s BoxMG operators (no reference counterpart): out[0] rows of P
  * (coarse vertices), out[1] distinct rows in its row dictionary (0 = stored dense), out[2]
  * rows of the cube-owned copy Pc (coarse cubes; 0 = none), out[3] distinct rows of Pc's
- * dictionary.  Dictionaries (lossless, bitwise-verified) are built at setup for level ltop-1
- * when rows repeat (piecewise-constant coefficients); TMG_PDICT=0 disables, 2 forces them. */
+ * dictionary, out[4] rows of the Galerkin table, out[5] distinct rows of its dictionary.
+ * Dictionaries (lossless, bitwise-verified) are built at setup for levels ltop-1 (and
+ * ltop-2) when rows repeat (piecewise-constant coefficients); TMG_PDICT=0 disables, 2 forces
+ * them. */
 int tmg3_storage(tmg_handle* h, int32_t level, int64_t* out);
 /* the cudaStream_t every phase is enqueued on */
 int tmg3_stream(tmg_handle* h, uint64_t* stream);

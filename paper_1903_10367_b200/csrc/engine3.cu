@@ -35,6 +35,9 @@ struct Lvl3 {
   double *Pd = nullptr, *Pcd = nullptr;
   uint32_t *Pdi = nullptr, *Pcdi = nullptr;
   uint8_t* Ptab = nullptr;  // k3_up_tma step tables over Pc's dictionary
+  double* Td = nullptr;      // level ltop-1: the Galerkin rows as a row dictionary (op.tdict)
+  uint32_t* Tdi = nullptr;
+  size_t Tdn = 0;
   size_t Pdp = 0, Pdn = 0, Pcdp = 0, Pcdn = 0;
   double* coefp = nullptr;  // finest level: coef with rows padded to even length (TMA)
   double *bR = nullptr, *bT = nullptr;  // level ltop-1: restrictions from the fused fine pass
@@ -951,6 +954,13 @@ int refresh_pc(Engine3* e, int l) {
     CK3(cudaStreamSynchronize(e->s));
     if (over) c.Pcd = nullptr, c.Pcdn = 0;
   }
+  // the Galerkin rows (k3_down_c's operator at level ltop-1) -- opt-in (TMG_PDICT_GAL=1): at config 5
+  // they have 1.24 M distinct rows and the per-lane row loads made k3_down_c slower (0.85 vs 0.65 ms)
+  const char* eg = std::getenv("TMG_PDICT_GAL");
+  if (l == e->ltop - 1 && eg && eg[0] == '1') {
+    size_t tdp = 0;
+    TRY3(build_dict(e, RowsView{c.tbl, c.nv, 0, c.nv, 27, c.nv, c.nv}, c.nv, force, &c.Td, &c.Tdi, &tdp, &c.Tdn));
+  }
   if (es && es[0] == '1') {
     const size_t Nc = c.N, Ncp = (Nc + 3) / 4 * 4;  // id rows padded to 16 bytes
     TRY3(build_dict(e, RowsView{c.P, c.nv, 0, c.nv, 125, Nc, Ncp}, c.nv, force, &c.Pd, &c.Pdi, &c.Pdp, &c.Pdn));
@@ -1078,6 +1088,8 @@ int build(Engine3* e, const tmg_tree3* t) {
       c.op = Op3{};
       c.op.kind = OP_TABLE;
       c.op.tbl = c.tbl;
+      c.op.tdict = c.Td;  // (null = dense planes)
+      c.op.tidx = c.Tdi;
     }
     if (cfg.throttled) e->thr_next = l1 - 1;
   }
@@ -1433,6 +1445,8 @@ int e3_storage(Engine3* e, int level, int64_t* out, std::string& err) {
   out[1] = c.Pd ? (int64_t)c.Pdn : 0;
   out[2] = c.Pc ? nc * nc * nc : 0;
   out[3] = c.Pcd ? (int64_t)c.Pcdn : 0;
+  out[4] = c.tbl ? (int64_t)c.nv : 0;
+  out[5] = c.Td ? (int64_t)c.Tdn : 0;
   return TMG_OK;
 }
 

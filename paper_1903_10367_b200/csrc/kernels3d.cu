@@ -100,8 +100,14 @@ __device__ __forceinline__ void op_apply(const Op3& op, const double* u, int N, 
   } else {
     const size_t nv = (size_t)N * N * N;
     double w[27];
+    if (op.tdict) {
+      const double* row = op.tdict + (size_t)__ldg(op.tidx + v) * kDictW;
 #pragma unroll
-    for (int t = 0; t < 27; ++t) w[t] = LD::ld(op.tbl + (size_t)t * nv + v);
+      for (int t = 0; t < 27; ++t) w[t] = __ldg(row + t);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 27; ++t) w[t] = LD::ld(op.tbl + (size_t)t * nv + v);
+    }
     double acc = 0.0;
 #pragma unroll
     for (int t = 0; t < 27; ++t) acc = acc + w[t] * x[t];

@@ -43,6 +43,10 @@ struct Op3 {
   double cdiag;       // const: K_D * (c + c + ... 8 times, sequential)
   const double* e;    // element: per-cell coefficient eff*h
   const double* tbl;  // table: 27 planes over the vertex grid, plane tap = (di+1)*9+(dj+1)*3+(dk+1)
+  // table as a row dictionary (kernels3d_dict.cu; level ltop-1's Galerkin rows): tap t of vertex v
+  // is tdict[tidx[v] * kDictW + t]
+  const double* tdict;
+  const uint32_t* tidx;
 };
 
 struct Grid {

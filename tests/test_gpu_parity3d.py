@@ -236,10 +236,12 @@ def test_3d_weight_dictionary_equals_dense(variant, wname, monkeypatch):
     n = 4
     monkeypatch.setenv("TMG_PDICT", "2")
     monkeypatch.setenv("TMG_PDICT_SMR", "1")
+    monkeypatch.setenv("TMG_PDICT_GAL", "1")
     wl1 = make()
     e1, h1 = gpu_run(wl1, n, variant)
     st = e1.weight_storage(4)
     assert 0 < st["p_distinct"] <= st["p_rows"], st
+    assert 0 < st["galerkin_distinct"] <= st["galerkin_rows"], st
     if wname == "config5-L5":
         assert 0 < st["pc_distinct"] <= st["pc_rows"], st
     else:  # per-cell coefficients: a prolongation step meets > 32 distinct rows, dense stream kept
@@ -264,3 +266,4 @@ def test_3d_weight_dictionary_default_on_blocks():
     print(st)
     assert st["p_distinct"] == 0, st
     assert 0 < st["pc_distinct"] <= st["pc_rows"] // 4, st
+    assert st["galerkin_distinct"] == 0, st
