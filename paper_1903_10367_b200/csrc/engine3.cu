@@ -35,6 +35,7 @@ struct Lvl3 {
   double *Pd = nullptr, *Pcd = nullptr;
   uint32_t *Pdi = nullptr, *Pcdi = nullptr;
   uint8_t* Ptab = nullptr;  // k3_up_tma step tables over Pc's dictionary
+  uint8_t* Pstab = nullptr;  // k3_smr tile-plane tables over P's dictionary
   double* Td = nullptr;      // level ltop-1: the Galerkin rows as a row dictionary (op.tdict)
   uint32_t* Tdi = nullptr;
   size_t Tdn = 0;
@@ -543,10 +544,8 @@ int launch_smr(Engine3* e, int l, bool smooth) {
   if (!tmap3(&A.tr, c.rho, N, N, N, N * 8, N * N * 8, kRW, kRH, 1) || !tmap4(&A.tp, cc.P, dp, sp, bp))
     return fail3(e, TMG_ECUDA, "tensor map encoding failed (k3_smr)");
   A.pd = cc.Pd;
-  const uint64_t Ncp = (Nc + 3) / 4 * 4;
-  if (cc.Pd && !tmap3(&A.ti, cc.Pdi, Nc, Nc, Nc, Ncp * 4, Ncp * Nc * 4, kRIW, kRJ, 2,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_DATA_TYPE_UINT32))
-    return fail3(e, TMG_ECUDA, "tensor map encoding failed (k3_smr index)");
+  A.ptab = cc.Pstab;
+  A.tilesJ = (n + kRJ - 1) / kRJ;
   const dim3 grid(tiles, (n + A.chunk - 1) / A.chunk);
   cudaEvent_t e0_ = nullptr;
   TRY3(begin_k(e, &e0_));
@@ -934,8 +933,8 @@ int refresh_pc(Engine3* e, int l) {
   const char* env = std::getenv("TMG_PDICT");
   if (e->cfg.throttled || (env && env[0] == '0') || l < e->ltop - 2 || c.Pd || c.Pcd) return TMG_OK;
   const bool force = env && env[0] == '2';
-  // Pc's dictionary feeds k3_up_tma; P's feeds k3_smr, which is instruction-bound either way and
-  // measured slower on the dictionary (5.2 vs 4.2 ms at config 5), so it is opt-in (TMG_PDICT_SMR=1)
+  // Pc's dictionary feeds k3_up_dict (TMG_PDICT_UP=0: dense), P's the restriction in k3_smr
+  // (TMG_PDICT_SMR=0: dense)
   const char* es = std::getenv("TMG_PDICT_SMR");
   const char* eu = std::getenv("TMG_PDICT_UP");
   if (!(eu && eu[0] == '0'))
@@ -961,9 +960,22 @@ int refresh_pc(Engine3* e, int l) {
     size_t tdp = 0;
     TRY3(build_dict(e, RowsView{c.tbl, c.nv, 0, c.nv, 27, c.nv, c.nv}, c.nv, force, &c.Td, &c.Tdi, &tdp, &c.Tdn));
   }
-  if (es && es[0] == '1') {
+  if (!(es && es[0] == '0')) {
     const size_t Nc = c.N, Ncp = (Nc + 3) / 4 * 4;  // id rows padded to 16 bytes
     TRY3(build_dict(e, RowsView{c.P, c.nv, 0, c.nv, 125, Nc, Ncp}, c.nv, force, &c.Pd, &c.Pdi, &c.Pdp, &c.Pdn));
+    if (c.Pd) {  // k3_smr's tile-plane tables; a tile plane meeting more than kRRows rows keeps the dense P
+      const int n = c.N - 2, tK = (n + kRK - 1) / kRK, tJ = (n + kRJ - 1) / kRJ;
+      const size_t cnt = (size_t)n * tJ * tK;
+      TRY3(alloc3(e, &c.Pstab, cnt * kRTabBytes, false));
+      int* dover = nullptr;
+      TRY3(alloc3(e, &dover, 1));
+      k3_smr_tables<<<nblk(cnt, 128), 128, 0, e->s>>>(c.Pdi, c.N, (int)Ncp, tK, tJ, c.Pstab, dover);
+      CKL3();
+      int over = 0;
+      CK3(cudaMemcpyAsync(&over, dover, sizeof(int), cudaMemcpyDeviceToHost, e->s));
+      CK3(cudaStreamSynchronize(e->s));
+      if (over) c.Pd = nullptr, c.Pdn = 0;
+    }
   }
   return TMG_OK;
 }

@@ -46,14 +46,56 @@ constexpr int kSCols = 2 * kSPairs;
 static_assert(kSH % 2 == 0, "sm columns are paired along j");
 constexpr int oRP = kRStages * kRSlot, oRS = oRP + kPStages * 2 * kPBox;
 constexpr size_t kSmrSmem = sizeof(double) * (oRS + 2 * kSBuf);
-// dictionary variant: no P ring; with rho plane p (ring slot) its TMA also brings the tile's
-// dictionary ids of coarse planes floor3(p), floor3(p) + 1 (box 32 x 4 x 2 uint32)
-// (box from K0 - 1: TMA faults on box rows that do not start 16-byte aligned)
-constexpr int kRIW = kRK + 4;                  // 36 ids per row
-constexpr int kRIds = 2 * kRIW * kRJ / 2;      // in doubles (144: a 128-byte multiple)
-constexpr int oRId = kRStages * kRSlot;
-constexpr int oRSd = oRId + kRStages * kRIds;
+// dictionary variant (P of the coarse level as a row dictionary, kernels3d_dict.cu): no P ring.
+// For each coarse plane m of the tile a setup-built table (k3_smr_tables: the plane's <= kRRows
+// distinct rows, each vertex's index into them) arrives by bulk copy 9 fine steps before the
+// plane is first restricted into, and the rows themselves (one 1000-byte bulk copy each, from
+// L2) 3 steps before, into a ring of three planes' row sets -- the weights are then read from
+// shared memory as the dense boxes are, at 8 + 8 KB per coarse plane instead of 136 KB of HBM.
+constexpr int kRRows = 32, kRRowS = 130;             // rows per tile plane (cap), row stride (doubles)
+constexpr int kRTabBytes = 272;                      // {n, ids[32]} uint32, local[128] uint8 at byte 132
+constexpr int kRTabLoc = 132;
+constexpr int kRNT = 6;                              // table ring (coarse planes)
+constexpr int oRTab = kRStages * kRSlot;
+constexpr int oRRows = oRTab + kRNT * kRTabBytes / 8;
+constexpr int kRRowSet = kRRows * kRRowS;
+constexpr int oRSd = oRRows + 3 * kRRowSet;
 constexpr size_t kSmrSmemD = sizeof(double) * (oRSd + 2 * kSBuf);
+constexpr unsigned kRRowBytes = 126 * 8;  // 125 weights, rounded to 16 bytes (rows are 1 KB)
+
+// tables of the dictionary variant: one thread per (coarse plane m, tile); *over = 1 when a tile
+// plane meets more than kRRows distinct rows (the dense P stream is kept then)
+__global__ void k3_smr_tables(const uint32_t* __restrict__ ids, int Nc, int Ncp, int tilesK, int tilesJ,
+                              uint8_t* __restrict__ tab, int* over) {
+  const int n = Nc - 2;
+  const size_t cnt = (size_t)n * tilesJ * tilesK;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += (size_t)gridDim.x * blockDim.x) {
+    const int tk = (int)(t % tilesK), tj = (int)((t / tilesK) % tilesJ), m = 1 + (int)(t / ((size_t)tilesK * tilesJ));
+    uint32_t rows[kRRows];
+    int cntr = 0;
+    uint8_t* T8 = tab + t * kRTabBytes;
+    for (int c = 0; c < kRK * kRJ; ++c) {
+      const int J = 1 + tj * kRJ + c / kRK, K = 1 + tk * kRK + c % kRK;
+      int loc = 0;
+      if (J <= n && K <= n) {
+        const uint32_t id = ids[((size_t)m * Nc + J) * Ncp + K];
+        while (loc < cntr && rows[loc] != id) ++loc;
+        if (loc == cntr) {
+          if (cntr == kRRows) {
+            atomicOr(over, 1);
+            loc = 0;
+          } else {
+            rows[cntr++] = id;
+          }
+        }
+      }
+      T8[kRTabLoc + c] = (uint8_t)loc;
+    }
+    uint32_t* T = reinterpret_cast<uint32_t*>(T8);
+    T[0] = (uint32_t)cntr;
+    for (int q = 0; q < kRRows; ++q) T[1 + q] = q < cntr ? rows[q] : 0u;
+  }
+}
 
 struct Smr {
   CUtensorMap tr;  // rho of the finest level, box {100, 16, 1}
@@ -64,8 +106,9 @@ struct Smr {
   double scale;    // omega*3/8
   double* bR;
   double* bT;
-  CUtensorMap ti;      // dictionary variant: ids of the coarse vertices {Nc, Nc, Nc} uint32, box {32, 4, 2}
-  const double* pd;    // P rows pd[id * kDictW + slot]
+  const double* pd;     // dictionary variant: P rows pd[id * kDictW + slot]
+  const uint8_t* ptab;  // ... and the tile-plane tables, index ((m - 1) * tilesJ + tj) * tilesK + tk
+  int tilesJ;
 };
 
 __device__ __forceinline__ int floor3s(int x) { return x >= 0 ? x / 3 : -((2 - x) / 3); }
@@ -79,7 +122,7 @@ __device__ __forceinline__ int floor3s(int x) { return x >= 0 ? x / 3 : -((2 - x
 template <bool DICT>
 __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ Smr A) {
   extern __shared__ __align__(128) double sr[];
-  __shared__ __align__(8) uint64_t bar[kRStages], pbar[kPStages];
+  __shared__ __align__(8) uint64_t bar[kRStages], pbar[kPStages], tbar[kRNT], rbar[3];
   const int N = A.N, Nc = A.Nc, n = Nc - 2;
   const int tk = blockIdx.x % A.tilesK, tj = blockIdx.x / A.tilesK;
   const int K0 = 1 + tk * kRK, J0 = 1 + tj * kRJ;
@@ -121,9 +164,35 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
 
   auto issue_r = [&](int p) {  // rho plane p into its slot
     const int sl = (p - p0) % kRStages;
-    mbar_expect_tx(&bar[sl], (unsigned)(sizeof(double) * kRW * kRH) + (DICT ? 8u * kRIds : 0u));
+    mbar_expect_tx(&bar[sl], (unsigned)(sizeof(double) * kRW * kRH));
     tma_load_3d(sr + sl * kRSlot, &A.tr, &bar[sl], fk0, fj0, p);
-    if (DICT) tma_load_3d(sr + oRId + sl * kRIds, &A.ti, &bar[sl], K0 - 1, J0, floor3s(p));
+  };
+  // DICT: coarse plane m's table (slot m % kRNT) / rows (set m % 3)
+  // (slots and barrier phases count planes from this CTA's first, Ia)
+  auto tab_of = [&](int m) {
+    return reinterpret_cast<const uint8_t*>(sr + oRTab + ((m - Ia) % kRNT) * (kRTabBytes / 8));
+  };
+  auto issue_tab = [&](int m) {  // thread lt == kRTasks (restriction warp 0, lane 0)
+    if (m < Ia || m >= Ib) return;
+    uint64_t* tb = &tbar[(m - Ia) % kRNT];
+    mbar_expect_tx(tb, kRTabBytes);
+    bulk_load(sr + oRTab + ((m - Ia) % kRNT) * (kRTabBytes / 8),
+              A.ptab + (((size_t)(m - 1) * A.tilesJ + tj) * A.tilesK + tk) * kRTabBytes, kRTabBytes, tb);
+  };
+  auto rows_of = [&](int m) { return sr + oRRows + ((m - Ia) % 3) * kRRowSet; };
+  auto wait_plane = [&](int m) {  // table and rows of plane m are in
+    mbar_wait(&tbar[(m - Ia) % kRNT], (unsigned)((m - Ia) / kRNT) & 1u);
+    mbar_wait(&rbar[(m - Ia) % 3], (unsigned)((m - Ia) / 3) & 1u);
+  };
+  auto issue_rows = [&](int m, int lane) {  // restriction warp 0, lane-parallel
+    if (m < Ia || m >= Ib) return;
+    mbar_wait(&tbar[(m - Ia) % kRNT], (unsigned)((m - Ia) / kRNT) & 1u);
+    const uint32_t* T = reinterpret_cast<const uint32_t*>(tab_of(m));
+    const int nr = (int)T[0];
+    uint64_t* rb = &rbar[(m - Ia) % 3];
+    if (lane == 0) mbar_expect_tx(rb, kRRowBytes * (unsigned)nr);
+    __syncwarp();
+    if (lane < nr) bulk_load(rows_of(m) + lane * kRRowS, A.pd + (size_t)T[1 + lane] * kDictW, kRRowBytes, rb);
   };
   auto issue_p = [&](int s) {  // the P boxes fine plane s meets into its set
     if (DICT) return;
@@ -138,12 +207,20 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
   if (lt == 0) {
     for (int q = 0; q < kRStages; ++q) mbar_init(&bar[q], 1);
     for (int q = 0; q < kPStages; ++q) mbar_init(&pbar[q], 1);
+    for (int q = 0; q < kRNT; ++q) mbar_init(&tbar[q], 1);
+    for (int q = 0; q < 3; ++q) mbar_init(&rbar[q], 1);
     mbar_fence_init();
   }
   __syncthreads();
   if (lt == 0) {
     for (int p = p0; p <= min(pEnd, p0 + 2); ++p) issue_r(p);
     for (int s = s0; s <= min(pEnd - 1, s0 + kPStages - 1); ++s) issue_p(s);
+  }
+  // DICT schedule: at step t = 3m' (m' = t / 3): the table of plane m' + 3 and the rows of plane
+  // m' + 1 (plane m is restricted into at steps 3m .. 3m + 4)
+  if (DICT && lt == kRTasks) {
+    issue_tab(p0 / 3 + 1);
+    issue_tab(p0 / 3 + 2);
   }
 
   // step t: C completes sm(t-1) from rho(t); D restricts fine plane t-2
@@ -155,6 +232,13 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
         if (t + 2 <= pEnd) issue_r(t + 2);                              // into the slot of plane t - 3
         if (t - 1 >= s0 + kPStages && t - 1 <= pEnd - 1) issue_p(t - 1);  // into the set of plane t - 3
       }
+    }
+    // table slot of plane t/3 + 3 last held plane t/3 - 3 (last read at step t - 5); row set of
+    // plane t/3 + 1 last held plane t/3 - 2 (last read at step t - 2)
+    if (DICT && t % 3 == 0 && lt >= kRTasks && lt < kRTasks + 32) {
+      fence_proxy_async();
+      if (lt == kRTasks) issue_tab(t / 3 + 3);
+      issue_rows(t / 3 + 1, lt - kRTasks);
     }
     if (smoother) {
       // ---- C: sm(t - 1) completes; sm(t), sm(t + 1) advance ------------------------
@@ -218,11 +302,15 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
           // DICT: the weights of slots (o + 2) * 25 + q (plane m3) / (o - 1) * 25 + q (plane m3 + 1)
           const double* wc = nullptr;
           const double* wn = nullptr;
-          if (DICT) {  // ids of coarse planes m3, m3 + 1 arrived with rho(s); rows are 128 doubles
-            const uint32_t* ids =
-                reinterpret_cast<const uint32_t*>(sr + oRId + (rs_ % kRStages) * kRIds) + wj * kRIW + wk + 1;
-            wc = A.pd + (size_t)ids[0] * kDictW + (o + 2) * 25;
-            wn = A.pd + (size_t)ids[kRIW * kRJ] * kDictW + (o - 1) * 25;
+          if (DICT) {  // rows of planes m3, m3 + 1 staged in their sets
+            if (m3 >= Ia && m3 < Ib) {
+              wait_plane(m3);
+              wc = rows_of(m3) + tab_of(m3)[kRTabLoc + w] * kRRowS + (o + 2) * 25;
+            }
+            if (o >= 1 && m3 + 1 >= Ia && m3 + 1 < Ib) {
+              wait_plane(m3 + 1);
+              wn = rows_of(m3 + 1) + tab_of(m3 + 1)[kRTabLoc + w] * kRRowS + (o - 1) * 25;
+            }
           }
           if (m3 >= Ia && m3 < Ib) {  // coarse plane m3, fine offset o in {0, 1, 2}
             double acc = accC;
@@ -230,7 +318,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
             for (int q = 0; q < 25; ++q) {
               const int oj = q / 5 - 2, ok = q % 5 - 2;
               const bool ctr = o == 0 && q == 12;
-              const double wt = ctr ? 1.0 : DICT ? __ldg(wc + q) : Pset[q * kRJ * kPW];
+              const double wt = ctr ? 1.0 : DICT ? wc[q] : Pset[q * kRJ * kPW];
               double x = src[oj * ld + ok];
               if (ctr && zc) x = 0.0;
               acc = acc + wt * x;
@@ -243,7 +331,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
 #pragma unroll
             for (int q = 0; q < 25; ++q) {
               const int oj = q / 5 - 2, ok = q % 5 - 2;
-              const double wt = DICT ? __ldg(wn + q) : Pset[kPBox + q * kRJ * kPW];
+              const double wt = DICT ? wn[q] : Pset[kPBox + q * kRJ * kPW];
               acc = acc + wt * src[oj * ld + ok];
             }
             accN = acc;
