@@ -303,12 +303,10 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
           const double* wc = nullptr;
           const double* wn = nullptr;
           if (DICT) {  // rows of planes m3, m3 + 1 staged in their sets
-            if (m3 >= Ia && m3 < Ib) {
-              wait_plane(m3);
-              wc = rows_of(m3) + tab_of(m3)[kRTabLoc + w] * kRRowS + (o + 2) * 25;
-            }
+            // a plane is waited for once, at its first use (as plane m3 + 1, fine offset o = 1)
+            if (m3 >= Ia && m3 < Ib) wc = rows_of(m3) + tab_of(m3)[kRTabLoc + w] * kRRowS + (o + 2) * 25;
             if (o >= 1 && m3 + 1 >= Ia && m3 + 1 < Ib) {
-              wait_plane(m3 + 1);
+              if (o == 1) wait_plane(m3 + 1);
               wn = rows_of(m3 + 1) + tab_of(m3 + 1)[kRTabLoc + w] * kRRowS + (o - 1) * 25;
             }
           }
