@@ -18,6 +18,7 @@
 #include "kernels3d_ffp4.cu"
 #include "kernels3d_upq.cu"
 #include "kernels3d_smr.cu"
+#include "kernels3d_top4.cu"
 #include "kernels3d_updict.cu"
 #include "kernels3d_dict.cu"
 
@@ -473,6 +474,15 @@ int launch_up_boxmg(Engine3* e, int l, const Up3& a) {
   return TMG_OK;
 }
 
+// element operator with every plane through TMA: the four-rows-per-thread kernel (TMG_TOP4=0: k3_top2)
+bool use_top4(const Top3& a) {
+  static const bool on = [] {
+    const char* v = std::getenv("TMG_TOP4");
+    return !(v && v[0] == '0');
+  }();
+  return on && a.use_tma == 2 && a.rhs_tma;
+}
+
 Top3 make_top(Engine3* e, int l) {
   Lvl3& c = e->L[l];
   Top3 a{};
@@ -568,6 +578,7 @@ int enqueue_down(Engine3* e, bool write) {
       cudaEvent_t e0_ = nullptr;
       TRY3(begin_k(e, &e0_));
       if (c.op.kind == OP_CONST) k3_top2<OP_CONST><<<c.s2_blocks, dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
+      else if (use_top4(a)) k3_top4<<<c.s2_blocks, dim3(kT4X, kT4Y), k2TopSmem, e->s>>>(a);
       else k3_top2<OP_ELEMENT><<<c.s2_blocks, dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
       CKL3();
       TRY3(end_k(e, kname("k3_down", l), e0_));
@@ -1057,6 +1068,7 @@ int build(Engine3* e, const tmg_tree3* t) {
   }
   CK3(cudaFuncSetAttribute(k3_top2<OP_CONST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2TopSmem));
   CK3(cudaFuncSetAttribute(k3_top2<OP_ELEMENT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2TopSmem));
+  CK3(cudaFuncSetAttribute(k3_top4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2TopSmem));
   CK3(cudaFuncSetAttribute(k3_smooth2r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2RSmemV));
   CK3(cudaFuncSetAttribute(k3_up_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpTmaSmem));
   CK3(cudaFuncSetAttribute(k3_up_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpTmaSmem));
@@ -1291,6 +1303,8 @@ int phase3(Engine3* e, int phase, int l) {
         TRY3(begin_k(e, &e0_));
         if (c.op.kind == OP_CONST)
           k3_top2<OP_CONST><<<e->own_blocks2[l], dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
+        else if (use_top4(a))
+          k3_top4<<<e->own_blocks2[l], dim3(kT4X, kT4Y), k2TopSmem, e->s>>>(a);
         else
           k3_top2<OP_ELEMENT><<<e->own_blocks2[l], dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
         CKL3();
