@@ -33,12 +33,16 @@ for r in rows:
              "usecond": 1e-6, "msecond": 1e-3, "nsecond": 1e-9}.get(unit, 1)
     e[d["Metric Name"]] = float(d["Metric Value"].replace(",", "")) * scale
 seq = list(launches.values())
-starts = [k for k, e in enumerate(seq) if e["name"].split("(")[0].split("<")[0].endswith(("k3_top", "k3_top2", "k3_top_s", "k3_top2r", "k3_ffp"))]
+def base(name):
+    return name.split("(")[0].replace("void ", "").split("<")[0].split("::")[-1]
+
+
+starts = [k for k, e in enumerate(seq) if base(e["name"]) in ("k3_top", "k3_top2", "k3_top4", "k3_top_s", "k3_top2r", "k3_ffp")]
 assert starts, "no 3D cycle in the launch list"
 res = {}
 cur = up = None
 for e in seq[starts[-2] if len(starts) > 1 else starts[-1]:]:
-    fn = e["name"].split("(")[0].replace("void ", "").split("<")[0].split("::")[-1]
+    fn = base(e["name"])
     b = e.get("dram__bytes_read.sum", 0) + e.get("dram__bytes_write.sum", 0)
     if fn.startswith("k3_top") or fn == "k3_ffp":
         if res.get(f"k3_down_L{top}") is not None and cur is not None:
