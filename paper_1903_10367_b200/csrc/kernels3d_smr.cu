@@ -154,13 +154,16 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
   }
 #pragma unroll
   for (int m = 0; m < kSCols; ++m) SEa[m] = SCa[m] = XA[m] = SEb[m] = SCb[m] = 0.0;
-  // restriction threads: coarse (J, K) of the tile, field 0 rho / 1 sm (adjacent lanes)
+  // restriction threads: coarse (J, K) of the tile, both fields (rho, sm) -- one weight load feeds
+  // both products; role r owns the coarse planes m with (m - Ia) % 2 == r (warps 8-11: r = 0,
+  // 12-15: r = 1), so a thread keeps its plane's two sums over all five fine planes it meets
   const int task = lt - kRTasks;
-  const int fld = task & 1, w = task >> 1;
+  const int role = (task >> 7) & 1, w = task & (kRK * kRJ - 1);
+  static_assert(kRK * kRJ == 128, "two restriction roles of 128 vertices");
   const int wj = w / kRK, wk = w % kRK;
   const int rJ = J0 + wj, rK = K0 + wk;
-  const bool rtask = !smoother && (fld == 0 || A.jac) && rJ <= n && rK <= n;
-  double accC = 0.0, accN = 0.0;
+  const bool rtask = !smoother && rJ <= n && rK <= n;
+  double accR = 0.0, accS = 0.0;
 
   auto issue_r = [&](int p) {  // rho plane p into its slot
     const int sl = (p - p0) % kRStages;
@@ -288,56 +291,64 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
         const int ps = s - s0, rs_ = s - p0;
         if (!DICT) mbar_wait(&pbar[ps % kPStages], (unsigned)(ps / kPStages) & 1u);
         mbar_wait(&bar[rs_ % kRStages], (unsigned)(rs_ / kRStages) & 1u);  // rho(s): visibility of the TMA write
-        const double* Pset = sr + oRP + (ps % kPStages) * 2 * kPBox + wj * kPW + wk + 1;
-        if (rtask) {
-          const int m3 = floor3s(s), o = s - 3 * m3;
-          const double* src;
+        // fine plane s feeds coarse plane m3 (offset o) and, for o >= 1, m3 + 1 (offset o - 3);
+        // this role's plane among them (warp-uniform)
+        const int m3 = floor3s(s), o = s - 3 * m3;
+        int m = -1, off = 0;
+        if (((m3 - Ia) & 1) == role) {
+          m = m3;
+          off = o;
+        } else if (o >= 1) {
+          m = m3 + 1;
+          off = o - 3;
+        }
+        if (rtask && m >= Ia && m < Ib) {
           constexpr int ld = kRW;  // both windows: immediate offsets in the sums
-          if (fld == 0) {
-            src = sr + (rs_ % kRStages) * kRSlot + (3 * wj + 3) * kRW + 3 * wk + 3;
+          const double* xr = sr + (rs_ % kRStages) * kRSlot + (3 * wj + 3) * kRW + 3 * wk + 3;
+          const double* xs = sr + oS + (s & 1) * kSBuf + (3 * wj + 2) * kRW + 3 * wk + 2;
+          // the weights of slots (off + 2) * 25 + q of plane m: DICT from the plane's staged rows
+          // (waited for once, at the plane's first fine plane, off = -2), else its P box
+          const double* wp;
+          int ws;
+          if (DICT) {
+            if (off == -2) wait_plane(m);
+            wp = rows_of(m) + tab_of(m)[kRTabLoc + w] * kRRowS + (off + 2) * 25;
+            ws = 1;
           } else {
-            src = sr + oS + (s & 1) * kSBuf + (3 * wj + 2) * kRW + 3 * wk + 2;
+            wp = sr + oRP + (ps % kPStages) * 2 * kPBox + wj * kPW + wk + 1 + (m == m3 ? 0 : kPBox);
+            ws = kRJ * kPW;
           }
-          const bool zc = fld == 0 && A.zc;
-          // DICT: the weights of slots (o + 2) * 25 + q (plane m3) / (o - 1) * 25 + q (plane m3 + 1)
-          const double* wc = nullptr;
-          const double* wn = nullptr;
-          if (DICT) {  // rows of planes m3, m3 + 1 staged in their sets
-            // a plane is waited for once, at its first use (as plane m3 + 1, fine offset o = 1)
-            if (m3 >= Ia && m3 < Ib) wc = rows_of(m3) + tab_of(m3)[kRTabLoc + w] * kRRowS + (o + 2) * 25;
-            if (o >= 1 && m3 + 1 >= Ia && m3 + 1 < Ib) {
-              if (o == 1) wait_plane(m3 + 1);
-              wn = rows_of(m3 + 1) + tab_of(m3 + 1)[kRTabLoc + w] * kRRowS + (o - 1) * 25;
-            }
-          }
-          if (m3 >= Ia && m3 < Ib) {  // coarse plane m3, fine offset o in {0, 1, 2}
-            double acc = accC;
+          double aR = accR, aS = accS;
+          if (A.jac) {
 #pragma unroll
             for (int q = 0; q < 25; ++q) {
               const int oj = q / 5 - 2, ok = q % 5 - 2;
-              const bool ctr = o == 0 && q == 12;
-              const double wt = ctr ? 1.0 : DICT ? wc[q] : Pset[q * kRJ * kPW];
-              double x = src[oj * ld + ok];
-              if (ctr && zc) x = 0.0;
-              acc = acc + wt * x;
+              const bool ctr = off == 0 && q == 12;
+              const double wt = ctr ? 1.0 : wp[q * ws];
+              double x = xr[oj * ld + ok];
+              if (ctr && A.zc) x = 0.0;
+              aR = aR + wt * x;
+              aS = aS + wt * xs[oj * ld + ok];
             }
-            accC = acc;
-            if (o == 2) (fld ? A.bT : A.bR)[((size_t)m3 * Nc + rJ) * Nc + rK] = acc;
-          }
-          if (o >= 1 && m3 + 1 >= Ia && m3 + 1 < Ib) {  // coarse plane m3 + 1, fine offset o - 3
-            double acc = accN;
+          } else {
 #pragma unroll
             for (int q = 0; q < 25; ++q) {
               const int oj = q / 5 - 2, ok = q % 5 - 2;
-              const double wt = DICT ? wn[q] : Pset[kPBox + q * kRJ * kPW];
-              acc = acc + wt * src[oj * ld + ok];
+              const bool ctr = off == 0 && q == 12;
+              const double wt = ctr ? 1.0 : wp[q * ws];
+              double x = xr[oj * ld + ok];
+              if (ctr && A.zc) x = 0.0;
+              aR = aR + wt * x;
             }
-            accN = acc;
           }
-          if (o == 2) {
-            accC = accN;
-            accN = 0.0;
+          if (off == 2) {  // plane m complete
+            const size_t ix = ((size_t)m * Nc + rJ) * Nc + rK;
+            A.bR[ix] = aR;
+            if (A.jac) A.bT[ix] = aS;
+            aR = aS = 0.0;
           }
+          accR = aR;
+          accS = aS;
         }
       }
     }
