@@ -1166,6 +1166,15 @@ int build(Engine3* e, const tmg_tree3* t) {
         const int t2 = ((c.N - 2 + kSX - 1) / kSX) * ((c.N - 2 + k2Y - 1) / k2Y);
         int n2 = (148 * 12 + t2 - 1) / t2;
         n2 = std::max(1, std::min(n2, std::max(1, (c.N - 2) / 4)));
+        if (t2 >= 148 * 3) {  // tiles fill a wave of 3 CTAs per SM: chunks by wave efficiency x halo
+          double best_eff = 0.0;
+          for (int nch = 1; nch <= 8; ++nch) {
+            const int ch = (c.N - 2 + nch - 1) / nch, nb = t2 * ((c.N - 2 + ch - 1) / ch);
+            const double waves = (double)nb / (148 * 3);
+            const double eff = waves / std::ceil(waves) * (double)ch / (ch + 2.0);
+            if (eff > best_eff + 1e-9) { best_eff = eff; n2 = nch; }
+          }
+        }
         c.s2_chunk = (c.N - 2 + n2 - 1) / n2;
         c.s2_blocks = t2 * ((c.N - 2 + c.s2_chunk - 1) / c.s2_chunk);
       }
