@@ -17,13 +17,19 @@
 //           sm columns of the 98 x 14 window and keeps, per column, the
 //           sequential edge / corner sums of the pending sm planes (the DAG
 //           of const_from is plane-major), so every rho plane is read once;
-//   D       thread (coarse vertex, field) adds fine plane p-1 of rho / sm to
-//           two running sums (coarse planes m and m+1 it feeds), the 25 (ob,
-//           oc) terms of the plane in order -- the oracle's o-order over the
-//           125 offsets -- and stores a coarse plane's sum when it completes.
-// Both threads of a (vertex, rho / sm) pair are adjacent lanes, so the P
-// weight they share is one load.  Same per-element DAGs as k3_smooth2r and
-// k3_down_c: b_R, b_T and everything after them are bitwise unchanged.
+//   D       thread (coarse vertex, role) adds fine plane p-1 of rho and sm to
+//           the two running sums of the coarse plane its role owns (the two
+//           roles own alternate planes, so a plane's sums stay in one thread
+//           over the five fine planes it meets), the 25 (ob, oc) terms of the
+//           plane in order -- the oracle's o-order over the 125 offsets -- and
+//           stores them when the plane completes.
+// One weight load feeds both fields' products.  Same per-element DAGs as
+// k3_smooth2r and k3_down_c: b_R, b_T and everything after them are bitwise
+// unchanged.  Measured alternatives (config 5, L6): 768 smoothing threads with
+// one column pair each (64 registers) 3.43 vs 3.17 ms; the restriction threads
+// also completing the window's last 174 column pairs 3.52 ms; 16-byte weight
+// loads no change -- the kernel is bound by shared-memory bandwidth (l1tex
+// 68 %: about 230 KB of shared loads per fine plane step) and the step barrier.
 #include <cuda.h>
 
 #include "kernels3d.cuh"
