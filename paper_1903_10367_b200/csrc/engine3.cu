@@ -522,6 +522,26 @@ SmoothS make_smooth_s(Engine3* e, int l) {
   return a;
 }
 
+// k3_smr layout (measured at config 5, L6): one restriction thread per coarse vertex carrying both
+// planes and both fields (default; TMG_SMR_RV=0: two roles owning alternate planes, 3.17 vs
+// 3.07 ms), smoothing threads owning groups of 7 sm columns (default; TMG_SMR_GH=2: pairs, 3.05 vs
+// 2.97 ms)
+static int smr_rv() {
+  static const int v = [] {
+    const char* s = getenv("TMG_SMR_RV");
+    return s ? atoi(s) : 1;
+  }();
+  return v;
+}
+
+static int smr_gh() {
+  static const int v = [] {
+    const char* s = getenv("TMG_SMR_GH");
+    return s ? atoi(s) : 7;
+  }();
+  return v;
+}
+
 // k3_smr over the finest level: adaFACx smoothing (when `smooth`) and the restriction of rho / sm
 // into level ltop-1's bR / bT
 int launch_smr(Engine3* e, int l, bool smooth) {
@@ -559,8 +579,16 @@ int launch_smr(Engine3* e, int l, bool smooth) {
   const dim3 grid(tiles, (n + A.chunk - 1) / A.chunk);
   cudaEvent_t e0_ = nullptr;
   TRY3(begin_k(e, &e0_));
-  if (cc.Pd) k3_smr<true><<<grid, kRThreads, kSmrSmemD, e->s>>>(A);
-  else k3_smr<false><<<grid, kRThreads, kSmrSmem, e->s>>>(A);
+  if (smr_rv() == 1 && smr_gh() == 7) {
+    if (cc.Pd) k3_smr<true, 1, 7><<<grid, kRTasks + kRK * kRJ, kSmrSmemD, e->s>>>(A);
+    else k3_smr<false, 1, 7><<<grid, kRTasks + kRK * kRJ, kSmrSmem, e->s>>>(A);
+  } else if (smr_rv() == 1) {
+    if (cc.Pd) k3_smr<true, 1, 2><<<grid, kRTasks + kRK * kRJ, kSmrSmemD, e->s>>>(A);
+    else k3_smr<false, 1, 2><<<grid, kRTasks + kRK * kRJ, kSmrSmem, e->s>>>(A);
+  } else {
+    if (cc.Pd) k3_smr<true, 0, 2><<<grid, kRThreads, kSmrSmemD, e->s>>>(A);
+    else k3_smr<false, 0, 2><<<grid, kRThreads, kSmrSmem, e->s>>>(A);
+  }
   CKL3();
   TRY3(end_k(e, kname("k3_smooth", l), e0_));
   return TMG_OK;
@@ -1230,8 +1258,12 @@ int build(Engine3* e, const tmg_tree3* t) {
              l1 - 1 > e->lc;
     e->smr_lo = e->lc + 2;  // every level whose coarser level is a grid (not chain) level
     if (e->smr) {
-      CK3(cudaFuncSetAttribute(k3_smr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmem));
-      CK3(cudaFuncSetAttribute(k3_smr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmemD));
+      CK3(cudaFuncSetAttribute(k3_smr<false, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmem));
+      CK3(cudaFuncSetAttribute(k3_smr<true, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmemD));
+      CK3(cudaFuncSetAttribute(k3_smr<false, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmem));
+      CK3(cudaFuncSetAttribute(k3_smr<true, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmemD));
+      CK3(cudaFuncSetAttribute(k3_smr<false, 1, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmem));
+      CK3(cudaFuncSetAttribute(k3_smr<true, 1, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmemD));
       for (int l = e->smr_lo - 1; l < l1; ++l) {
         Lvl3& cc = e->L[l];
         if (!cc.bR) TRY3(alloc3(e, &cc.bR, cc.nv));

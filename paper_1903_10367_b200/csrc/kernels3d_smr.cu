@@ -25,7 +25,12 @@
 //           stores them when the plane completes.
 // One weight load feeds both fields' products.  Same per-element DAGs as
 // k3_smooth2r and k3_down_c: b_R, b_T and everything after them are bitwise
-// unchanged.  Measured alternatives (config 5, L6): 768 smoothing threads with
+// unchanged.  Default layout (engine3.cu: smr_rv / smr_gh): 256 smoothing threads
+// owning groups of 7 sm columns (27 shared loads per 7 columns), 128 restriction
+// threads, one per coarse vertex, carrying both coarse planes a fine plane feeds
+// and both fields (the 5 x 5 x 2 window is read once for both planes) --
+// 2.97 ms at config 5 L6 against 3.17 ms for the two-role / pairs layout
+// (RV = 0, GH = 2).  Measured alternatives of the two-role layout: 768 smoothing threads with
 // one column pair each (64 registers) 3.43 vs 3.17 ms; the restriction threads
 // also completing the window's last 174 column pairs 3.52 ms; 16-byte weight
 // loads no change -- the kernel is bound by shared-memory bandwidth (l1tex
@@ -47,8 +52,12 @@ constexpr int kPW = kRK + 2;                       // P box rows from K0 - 1 (16
 constexpr int kPBox = (kPW * kRJ * 25 + 15) / 16 * 16;  // one 25-slot P box (27.2 KB; 128-byte multiple)
 constexpr int kPStages = 2;                        // P sets (two boxes each)
 constexpr int kSBuf = (kRW * kSH + 15) / 16 * 16;  // one sm plane (double buffered), pitch kRW like rho's
-constexpr int kSPairs = (kSW * (kSH / 2) + kRTasks - 1) / kRTasks;  // 3 pairs of sm columns per smoothing thread
-constexpr int kSCols = 2 * kSPairs;
+// a smoothing thread owns groups of GH sm columns (rows jj .. jj + GH - 1 at kk): GH = 2 (pairs, 3
+// per thread, 12 shared loads per 2 columns) or GH = 7 (half the window's height, one group per
+// thread, 27 loads per 7 columns)
+template <int GH>
+constexpr int kSPer = (kSW * (kSH / GH) + kRTasks - 1) / kRTasks;
+static_assert(kSH % 2 == 0 && kSH % 7 == 0, "column groups tile the sm window");
 static_assert(kSH % 2 == 0, "sm columns are paired along j");
 constexpr int oRP = kRStages * kRSlot, oRS = oRP + kPStages * 2 * kPBox;
 constexpr size_t kSmrSmem = sizeof(double) * (oRS + 2 * kSBuf);
@@ -125,8 +134,35 @@ __device__ __forceinline__ int floor3s(int x) { return x >= 0 ? x / 3 : -((2 - x
 // DICT: level ltop-1's P as a row dictionary (kernels3d_dict.cu): no P ring, each restriction
 // thread reads its vertex's weights from the plane-major dictionary (L1-cached, the rows of a
 // warp's vertices have neighbouring ids), the same doubles in the same order.
-template <bool DICT>
-__global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ Smr A) {
+// RV = 1 (TMG_SMR_RV=1): one restriction thread per coarse vertex carrying both coarse planes and
+// both fields (x loaded once for both planes), 128 restriction threads (384 per CTA)
+template <bool C, bool NX, bool JAC>
+__device__ __forceinline__ void terms2(const double* wc, const double* wn, int ws, const double* xr,
+                                       const double* xs, bool ctr0, bool zc, double& cR, double& cS,
+                                       double& nR, double& nS) {
+  constexpr int ld = kRW;
+#pragma unroll
+  for (int q = 0; q < 25; ++q) {
+    const int oj = q / 5 - 2, ok = q % 5 - 2;
+    const double x = xr[oj * ld + ok];
+    const double y = JAC ? xs[oj * ld + ok] : 0.0;
+    if (C) {
+      const bool ctr = ctr0 && q == 12;
+      const double wt = ctr ? 1.0 : wc[q * ws];
+      cR = cR + wt * ((ctr && zc) ? 0.0 : x);
+      if (JAC) cS = cS + wt * y;
+    }
+    if (NX) {
+      const double wt = wn[q * ws];
+      nR = nR + wt * x;
+      if (JAC) nS = nS + wt * y;
+    }
+  }
+}
+
+template <bool DICT, int RV, int GH>
+__global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_smr(const __grid_constant__ Smr A) {
+  constexpr int kSPairs = kSPer<GH>, kSCols = GH * kSPairs, kSGroups = kSW * (kSH / GH);
   extern __shared__ __align__(128) double sr[];
   __shared__ __align__(8) uint64_t bar[kRStages], pbar[kPStages], tbar[kRNT], rbar[3];
   const int N = A.N, Nc = A.Nc, n = Nc - 2;
@@ -141,9 +177,9 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
   const int lt = threadIdx.x;
   const bool smoother = lt < kRTasks;
 
-  // smoothing threads: pairs of sm columns (jj, jj + 1) at kk -- the pair's 3 x 3 rho
-  // neighbourhoods share 6 of their 9 values (12 shared loads per 2 columns) -- and the
-  // columns' pending partial sums
+  // smoothing threads: groups of GH sm columns (jj .. jj + GH - 1) at kk -- the group's 3 x 3 rho
+  // neighbourhoods share rows (3 (GH + 2) shared loads per GH columns) -- and the columns'
+  // pending partial sums
   int spair[kSPairs];
   bool sin_[kSCols];
   double SEa[kSCols], SCa[kSCols], XA[kSCols], SEb[kSCols], SCb[kSCols];
@@ -151,11 +187,11 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
   for (int m = 0; m < kSPairs; ++m) {
     const int q2 = lt + m * kRTasks;
     const int jp = q2 / kSW, kk = q2 - jp * kSW;
-    spair[m] = (smoother && q2 < kSW * (kSH / 2)) ? q2 : -1;
+    spair[m] = (smoother && q2 < kSGroups) ? q2 : -1;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int j = fj0 + 1 + 2 * jp + h, k = fk0 + 1 + kk;
-      sin_[2 * m + h] = q2 < kSW * (kSH / 2) && j >= 1 && k >= 1 && j <= N - 2 && k <= N - 2;
+    for (int h = 0; h < GH; ++h) {
+      const int j = fj0 + 1 + GH * jp + h, k = fk0 + 1 + kk;
+      sin_[GH * m + h] = q2 < kSGroups && j >= 1 && k >= 1 && j <= N - 2 && k <= N - 2;
     }
   }
 #pragma unroll
@@ -164,12 +200,12 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
   // both products; role r owns the coarse planes m with (m - Ia) % 2 == r (warps 8-11: r = 0,
   // 12-15: r = 1), so a thread keeps its plane's two sums over all five fine planes it meets
   const int task = lt - kRTasks;
-  const int role = (task >> 7) & 1, w = task & (kRK * kRJ - 1);
+  const int role = RV ? 0 : (task >> 7) & 1, w = task & (kRK * kRJ - 1);
   static_assert(kRK * kRJ == 128, "two restriction roles of 128 vertices");
   const int wj = w / kRK, wk = w % kRK;
   const int rJ = J0 + wj, rK = K0 + wk;
   const bool rtask = !smoother && rJ <= n && rK <= n;
-  double accR = 0.0, accS = 0.0;
+  double accR = 0.0, accS = 0.0, accNR = 0.0, accNS = 0.0;
 
   auto issue_r = [&](int p) {  // rho plane p into its slot
     const int sl = (p - p0) % kRStages;
@@ -264,16 +300,16 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
           if (spair[mp] < 0) continue;
           const int q2 = spair[mp];
           const int jp = q2 / kSW, kk = q2 - jp * kSW;
-          // rows 2 jp - 1 .. 2 jp + 2, cols kk - 1 .. kk + 1 of the sm window (rho window + 1)
-          const int rb = (2 * jp) * kRW + kk;
-          double R[4][3];
+          // rows GH jp - 1 .. GH jp + GH, cols kk - 1 .. kk + 1 of the sm window (rho window + 1)
+          const int rb = (GH * jp) * kRW + kk;
+          double R[GH + 2][3];
 #pragma unroll
-          for (int a = 0; a < 4; ++a)
+          for (int a = 0; a < GH + 2; ++a)
 #pragma unroll
             for (int b = 0; b < 3; ++b) R[a][b] = Rp[rb + a * kRW + b];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int m = 2 * mp + h;
+          for (int h = 0; h < GH; ++h) {
+            const int m = GH * mp + h;
             const double f0 = R[h][1], f1 = R[h + 1][0], f2 = R[h + 1][2], f3 = R[h + 2][1];
             const double d0 = R[h][0], d1 = R[h][2], d2 = R[h + 2][0], d3 = R[h + 2][2];
             const double xc = R[h + 1][1];
@@ -281,7 +317,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
             double sc = (((SCa[m] + d0) + d1) + d2) + d3;
             double v = ((C_D8 * XA[m]) - (C_E6 * se)) - (C_C12 * sc);
             v = v * A.scale;
-            Sb[(2 * jp + h) * kRW + kk] = (sok && sin_[m]) ? v : 0.0;
+            Sb[(GH * jp + h) * kRW + kk] = (sok && sin_[m]) ? v : 0.0;
             SEa[m] = (((SEb[m] + d0) + d1) + d2) + d3;
             SCa[m] = SCb[m];
             XA[m] = xc;
@@ -300,6 +336,50 @@ __global__ void __launch_bounds__(kRThreads, 1) k3_smr(const __grid_constant__ S
         // fine plane s feeds coarse plane m3 (offset o) and, for o >= 1, m3 + 1 (offset o - 3);
         // this role's plane among them (warp-uniform)
         const int m3 = floor3s(s), o = s - 3 * m3;
+        if constexpr (RV == 1) {
+          const bool c = m3 >= Ia && m3 < Ib, nx = o >= 1 && m3 + 1 >= Ia && m3 + 1 < Ib;
+          if (rtask) {
+            const double* xr = sr + (rs_ % kRStages) * kRSlot + (3 * wj + 3) * kRW + 3 * wk + 3;
+            const double* xs = sr + oS + (s & 1) * kSBuf + (3 * wj + 2) * kRW + 3 * wk + 2;
+            const double* wc = nullptr;
+            const double* wn = nullptr;
+            int ws;
+            if (DICT) {
+              if (c) wc = rows_of(m3) + tab_of(m3)[kRTabLoc + w] * kRRowS + (o + 2) * 25;
+              if (nx) {
+                if (o == 1) wait_plane(m3 + 1);
+                wn = rows_of(m3 + 1) + tab_of(m3 + 1)[kRTabLoc + w] * kRRowS + (o - 1) * 25;
+              }
+              ws = 1;
+            } else {
+              wc = sr + oRP + (ps % kPStages) * 2 * kPBox + wj * kPW + wk + 1;
+              wn = wc + kPBox;
+              ws = kRJ * kPW;
+            }
+            const bool c0 = o == 0, zc = A.zc != 0;
+            if (c && nx) {
+              if (A.jac) terms2<true, true, true>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
+              else terms2<true, true, false>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
+            } else if (c) {
+              if (A.jac) terms2<true, false, true>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
+              else terms2<true, false, false>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
+            } else if (nx) {
+              if (A.jac) terms2<false, true, true>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
+              else terms2<false, true, false>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
+            }
+            if (o == 2) {
+              if (c) {
+                const size_t ix = ((size_t)m3 * Nc + rJ) * Nc + rK;
+                A.bR[ix] = accR;
+                if (A.jac) A.bT[ix] = accS;
+              }
+              accR = accNR;
+              accS = accNS;
+              accNR = accNS = 0.0;
+            }
+          }
+          continue;
+        }
         int m = -1, off = 0;
         if (((m3 - Ia) & 1) == role) {
           m = m3;
