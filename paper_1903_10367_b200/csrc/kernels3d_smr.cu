@@ -33,8 +33,12 @@
 // (RV = 0, GH = 2).  Measured alternatives of the two-role layout: 768 smoothing threads with
 // one column pair each (64 registers) 3.43 vs 3.17 ms; the restriction threads
 // also completing the window's last 174 column pairs 3.52 ms; 16-byte weight
-// loads no change -- the kernel is bound by shared-memory bandwidth (l1tex
+// loads no change -- that layout was bound by shared-memory bandwidth (l1tex
 // 68 %: about 230 KB of shared loads per fine plane step) and the step barrier.
+// The default layout runs at l1tex 53 % with barrier stalls first (29 %); a
+// balanced schedule deferring parts of the offset -2 / -1 groups by one fine
+// plane (42 | 42 | 41 terms per step instead of 25 | 50 | 50, six rho slots,
+// three sm buffers; bitwise) measured slower, 3.29-3.44 vs 3.0 ms.
 #include <cuda.h>
 
 #include "kernels3d.cuh"
