@@ -526,20 +526,15 @@ SmoothS make_smooth_s(Engine3* e, int l) {
 // planes and both fields (default; TMG_SMR_RV=0: two roles owning alternate planes, 3.17 vs
 // 3.07 ms), smoothing threads owning groups of 7 sm columns (default; TMG_SMR_GH=2: pairs, 3.05 vs
 // 2.97 ms)
+// (read at every launch: an engine's cycle graph is captured once)
 static int smr_rv() {
-  static const int v = [] {
-    const char* s = getenv("TMG_SMR_RV");
-    return s ? atoi(s) : 1;
-  }();
-  return v;
+  const char* s = getenv("TMG_SMR_RV");
+  return s ? atoi(s) : 1;
 }
 
 static int smr_gh() {
-  static const int v = [] {
-    const char* s = getenv("TMG_SMR_GH");
-    return s ? atoi(s) : 7;
-  }();
-  return v;
+  const char* s = getenv("TMG_SMR_GH");
+  return s ? atoi(s) : 7;
 }
 
 // k3_smr over the finest level: adaFACx smoothing (when `smooth`) and the restriction of rho / sm

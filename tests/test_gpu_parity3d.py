@@ -256,6 +256,34 @@ def test_3d_weight_dictionary_equals_dense(variant, wname, monkeypatch):
         assert np.array_equal(wl1.tree.u[l], wl2.tree.u[l]), f"level {l}"
 
 
+@pytest.mark.parametrize("layout", [("0", "2"), ("1", "2")])
+@pytest.mark.parametrize("wname", ["config5-L5", "random-L5"])
+def test_3d_smr_layouts_equal(layout, wname, monkeypatch):
+    """k3_smr's thread layouts -- the default (restriction thread per coarse vertex over both
+    planes and fields, 7-column smoothing groups) and the earlier ones (TMG_SMR_RV=0: two roles
+    owning alternate planes; TMG_SMR_GH=2: column pairs) -- give the same iterate bit for bit,
+    on the dictionary (blockwise eps) and the dense (per-cell eps) weight paths."""
+    def make():
+        if wname == "config5-L5":
+            return workloads.config5(levels=5, block=27)
+        wl = workloads.by_name("config5-L5")
+        rng = np.random.default_rng(11)
+        wl.tree.eps[5][...] = 10.0 ** rng.uniform(-2, 2, wl.tree.eps[5].shape)
+        return wl
+
+    n = 4
+    wl1 = make()
+    e1, h1 = gpu_run(wl1, n, "adafac-jac")
+    monkeypatch.setenv("TMG_SMR_RV", layout[0])
+    monkeypatch.setenv("TMG_SMR_GH", layout[1])
+    wl2 = make()
+    e2, h2 = gpu_run(wl2, n, "adafac-jac")
+    assert [s.l2h for s in h1] == [s.l2h for s in h2]
+    assert [s.linf for s in h1] == [s.linf for s in h2]
+    for l in range(1, 6):
+        assert np.array_equal(wl1.tree.u[l], wl2.tree.u[l]), f"level {l}"
+
+
 def test_3d_weight_dictionary_default_on_blocks():
     """On blockwise-constant coefficients (config 5's structure) the default setup stores level
     ltop-1's weights (P for the restriction, the cube-owned copy for the prolongation) as
