@@ -132,6 +132,10 @@ int tmg_dim(tmg_handle* h);
 #define TMG_PH_UP 3     /* level l >= ls: carry + update on owned planes        */
 #define TMG_PH_INJECT 4 /* FAS injection ls -> lmin on the replicated levels    */
 #define TMG_PH_REDUCE 5 /* fold this cycle's stats partials into TMG_F_PART     */
+#define TMG_PH_SMR 6    /* level l > ls with tmg3_fused: adaFACx smoothing of l fused with the
+                           restriction into the owned planes of l - 1 (replaces SMOOTH of l and
+                           the restriction in DOWN of l - 1; rho of l needs 3 halo planes below
+                           and 1 above, sm needs none) */
 #define TMG_F_U 0
 #define TMG_F_RHO 1
 #define TMG_F_SM 2
@@ -140,6 +144,8 @@ int tmg_dim(tmg_handle* h);
 #define TMG_F_PART 5 /* 2 doubles: sum of squares, max (all-reduced across ranks) */
 int tmg3_shard(tmg_handle* h, int32_t ls, const int32_t* lo, const int32_t* hi);
 int tmg3_phase(tmg_handle* h, int32_t phase, int32_t level);
+/* *out = 1 when the sharded cycle of level `level` runs TMG_PH_SMR instead of TMG_PH_SMOOTH */
+int tmg3_fused(tmg_handle* h, int32_t level, int32_t* out);
 /* device address and element count of a field of a level (zero-copy views) */
 int tmg3_field(tmg_handle* h, int32_t field, int32_t level, uint64_t* ptr, int64_t* count);
 /* storage of level `level`'s BoxMG operators (no reference counterpart): out[0] rows of P

@@ -20,7 +20,7 @@ VARIANT_IDS = {"additive": 0, "additive-exp": 1, "bpx": 2, "afacc": 3, "adafac-p
                "adafac-jac": 5, "multiplicative-v10": 6}
 FLAVOR_IDS = {"geometric": 0, "boxmg": 1}
 TABLE_A, TABLE_DIAG, TABLE_P, TABLE_RT, TABLE_EFFEPS = 0, 1, 2, 3, 4
-PH_DOWN, PH_SMOOTH, PH_REPL, PH_UP, PH_INJECT, PH_REDUCE = 0, 1, 2, 3, 4, 5
+PH_DOWN, PH_SMOOTH, PH_REPL, PH_UP, PH_INJECT, PH_REDUCE, PH_SMR = 0, 1, 2, 3, 4, 5, 6
 F_U, F_RHO, F_SM, F_CARRY, F_G, F_PART = 0, 1, 2, 3, 4, 5
 
 EXPORTS = ("tmg_create", "tmg_rebuild", "tmg_set_rhs", "tmg_set_u", "tmg_get_u",
@@ -28,7 +28,7 @@ EXPORTS = ("tmg_create", "tmg_rebuild", "tmg_set_rhs", "tmg_set_u", "tmg_get_u",
            "tmg_level_counts", "tmg_get_kinds", "tmg_get_table", "tmg_time_cycles",
            "tmg_profile_cycles", "tmg_launches_per_cycle", "tmg_destroy", "tmg_last_error",
            "tmg_device_count", "tmg3_create", "tmg3_rebuild", "tmg_dim", "tmg3_shard", "tmg3_phase",
-           "tmg3_field", "tmg3_stream", "tmg3_history", "tmg3_storage")
+           "tmg3_field", "tmg3_stream", "tmg3_history", "tmg3_storage", "tmg3_fused")
 
 
 class Config(C.Structure):
@@ -96,6 +96,7 @@ def lib() -> C.CDLL:
         "tmg3_field": ([H, C.c_int32, C.c_int32, P(C.c_uint64), P(C.c_int64)], C.c_int),
         "tmg3_stream": ([H, P(C.c_uint64)], C.c_int),
         "tmg3_storage": ([H, C.c_int32, P(C.c_int64)], C.c_int),
+        "tmg3_fused": ([H, C.c_int32, P(C.c_int32)], C.c_int),
         "tmg3_history": ([H, C.c_int32, C.c_void_p], C.c_int),
     }
     for name, (args, res) in sig.items():

@@ -833,6 +833,11 @@ int tmg3_storage(tmg_handle* h, int32_t level, int64_t* out) {
   return e3_storage(h->e3, level, out, g_err);
 }
 
+int tmg3_fused(tmg_handle* h, int32_t level, int32_t* out) {
+  if (!h || !h->e3 || !out) return fail(TMG_EINVAL, "null argument or not a 3D handle");
+  return e3_fused(h->e3, level, out, g_err);
+}
+
 int tmg3_stream(tmg_handle* h, uint64_t* stream) {
   if (!h || !h->e3 || !stream) return fail(TMG_EINVAL, "null argument or not a 3D handle");
   return e3_stream(h->e3, stream);

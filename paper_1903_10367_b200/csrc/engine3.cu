@@ -539,15 +539,21 @@ static int smr_gh() {
 
 // k3_smr over the finest level: adaFACx smoothing (when `smooth`) and the restriction of rho / sm
 // into level ltop-1's bR / bT
-int launch_smr(Engine3* e, int l, bool smooth) {
+// (sharded: the coarse planes [clo, chi) a rank owns; its rho must hold 3 planes below and 1 above
+// the fine planes it owns)
+int launch_smr(Engine3* e, int l, bool smooth, int clo = -1, int chi = -1) {
   Lvl3& c = e->L[l];
   Lvl3& cc = e->L[l - 1];
   Smr A{};
   A.N = c.N;
   A.Nc = cc.N;
-  const int n = cc.N - 2;
-  A.tilesK = (n + kRK - 1) / kRK;
-  const int tiles = A.tilesK * ((n + kRJ - 1) / kRJ);
+  A.ilo = clo < 0 ? 1 : clo;
+  A.ihi = chi < 0 ? cc.N - 1 : chi;
+  const int n = A.ihi - A.ilo;  // coarse planes restricted into
+  if (n <= 0) return TMG_OK;
+  const int nk = cc.N - 2;  // interior coarse vertices along K and J
+  A.tilesK = (nk + kRK - 1) / kRK;
+  const int tiles = A.tilesK * ((nk + kRJ - 1) / kRJ);
   // coarse-plane chunks: about a whole number of waves of one CTA per SM
   int best = 1;
   double best_eff = 0.0;
@@ -570,7 +576,7 @@ int launch_smr(Engine3* e, int l, bool smooth) {
     return fail3(e, TMG_ECUDA, "tensor map encoding failed (k3_smr)");
   A.pd = cc.Pd;
   A.ptab = cc.Pstab;
-  A.tilesJ = (n + kRJ - 1) / kRJ;
+  A.tilesJ = (nk + kRJ - 1) / kRJ;
   const dim3 grid(tiles, (n + A.chunk - 1) / A.chunk);
   cudaEvent_t e0_ = nullptr;
   TRY3(begin_k(e, &e0_));
@@ -1318,6 +1324,13 @@ void tiling(int N, int ilo, int ihi, int* chunk, int* blocks, int ty = kSY) {
 int interior_lo(Engine3* e, int l) { return std::max(1, e->own_lo[l]); }
 int interior_hi(Engine3* e, int l) { return std::min(e->L[l].N - 1, e->own_hi[l]); }
 
+// sharded cycle: level l's adaFACx smoothing runs fused with the restriction into l - 1 (k3_smr
+// over the owned coarse planes of l - 1, phase TMG_PH_SMR) -- the grid levels above the shard
+// level where the single-GPU cycle fuses them
+bool fused3(const Engine3* e, int l) {
+  return e->sharded && e->smr && e->cfg.variant == VAR_JAC && l > e->ls && l <= e->ltop && l >= e->smr_lo;
+}
+
 int phase3(Engine3* e, int phase, int l) {
   const bool jac = e->cfg.variant == VAR_JAC;
   const bool boxmg = e->cfg.flavor == TMG_BOXMG;
@@ -1345,6 +1358,13 @@ int phase3(Engine3* e, int phase, int l) {
           k3_top2<OP_ELEMENT><<<e->own_blocks2[l], dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
         CKL3();
         TRY3(end_k(e, kname("k3_down", l), e0_));
+      } else if (fused3(e, l + 1)) {  // restrictions formed by TMG_PH_SMR of level l + 1
+        Down3 a = make_down(e, l, true);
+        a.ilo = lo;
+        a.ihi = hi;
+        a.bR = c.bR;
+        a.bT = c.bT;
+        LAUNCH3(kname("k3_down", l), (k3_down_c<true, true, true>), c.c_grid, 128, a);
       } else {
         Down3 a = make_down(e, l, true);
         a.ilo = lo;
@@ -1370,6 +1390,10 @@ int phase3(Engine3* e, int phase, int l) {
       CKL3();
       TRY3(end_k(e, kname("k3_smooth", l), e0_));
       return TMG_OK;
+    }
+    case TMG_PH_SMR: {
+      if (!fused3(e, l)) return fail3(e, TMG_EINVAL, "SMR: level's smoothing is not fused (tmg3_fused)");
+      return launch_smr(e, l, true, interior_lo(e, l - 1), interior_hi(e, l - 1));
     }
     case TMG_PH_REDUCE: {
       LAUNCH3("k3_reduce_parts", k3_reduce_parts, 1, 512, e->part_sum, e->part_max, e->top_parts, e->red);
@@ -1496,6 +1520,13 @@ int e3_phase(Engine3* e, int phase, int level, std::string& err) {
     --e->thr_next;
   }
   return phase3(e, phase, level);
+}
+
+int e3_fused(Engine3* e, int level, int32_t* out, std::string& err) {
+  e->err = &err;
+  TRY3(check_level(e, level));
+  *out = fused3(e, level) ? 1 : 0;
+  return TMG_OK;
 }
 
 int e3_storage(Engine3* e, int level, int64_t* out, std::string& err) {

@@ -32,5 +32,6 @@ int e3_shard(Engine3* e, int ls, const int32_t* lo, const int32_t* hi, std::stri
 int e3_phase(Engine3* e, int phase, int level, std::string& err);
 int e3_field(Engine3* e, int field, int level, uint64_t* ptr, int64_t* count, std::string& err);
 int e3_storage(Engine3* e, int level, int64_t* out, std::string& err);
+int e3_fused(Engine3* e, int level, int32_t* out, std::string& err);
 int e3_stream(Engine3* e, uint64_t* s);
 int e3_history(Engine3* e, int count, tmg_stats* out, std::string& err);

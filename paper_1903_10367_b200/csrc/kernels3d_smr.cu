@@ -128,6 +128,7 @@ struct Smr {
   const double* pd;     // dictionary variant: P rows pd[id * kDictW + slot]
   const uint8_t* ptab;  // ... and the tile-plane tables, index ((m - 1) * tilesJ + tj) * tilesK + tk
   int tilesJ;
+  int ilo, ihi;  // coarse planes [ilo, ihi) this launch restricts into (sharded: the owned ones)
 };
 
 __device__ __forceinline__ int floor3s(int x) { return x >= 0 ? x / 3 : -((2 - x) / 3); }
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
   const int N = A.N, Nc = A.Nc, n = Nc - 2;
   const int tk = blockIdx.x % A.tilesK, tj = blockIdx.x / A.tilesK;
   const int K0 = 1 + tk * kRK, J0 = 1 + tj * kRJ;
-  const int Ia = 1 + blockIdx.y * A.chunk, Ib = min(n + 1, Ia + A.chunk);  // coarse planes [Ia, Ib)
+  const int Ia = A.ilo + blockIdx.y * A.chunk, Ib = min(A.ihi, Ia + A.chunk);  // coarse planes [Ia, Ib)
   if (Ia >= Ib) return;
   const int fk0 = 3 * K0 - 3, fj0 = 3 * J0 - 3;  // rho window origin (fine)
   const int p0 = 3 * Ia - 3, pEnd = 3 * Ib;       // rho planes streamed: [p0, pEnd]

@@ -16,6 +16,10 @@ phases:
 phase                       exchange after it
 ==========================  ==================================================
 DOWN(l), l = ltop..ls       rho_l: planes a-2, a-1 from rank r-1, b from r+1
+                            (a-3 .. a-1 and b when l is fused, below)
+SMR(l) (adaFACx, l > ls,    -- (the smoothing of l runs fused with the
+tmg3_fused; else SMOOTH)    restriction into the owned planes of l-1: sm
+                            never leaves the chip, DOWN(l-1) reads b_R, b_T)
 SMOOTH(l) (adaFACx)         sm_l: planes a-2, a-1 from rank r-1
 (l == ls)                   all-gather rho_ls, sm_ls (the replicated level
                             ls-1 restricts from them)
@@ -246,6 +250,13 @@ class GpuShard:
     def phase(self, ph: int, level: int = 0) -> None:
         _abi.check(_abi.lib().tmg3_phase(self.eng._h, ph, level))
 
+    def fused(self, level: int) -> bool:
+        """Whether the engine runs level's smoothing fused with the restriction (PH_SMR)."""
+        import ctypes as C
+        v = C.c_int32()
+        _abi.check(_abi.lib().tmg3_fused(self.eng._h, level, C.byref(v)))
+        return bool(v.value)
+
     def close(self) -> None:
         """Drop the zero-copy views (call before the engine is closed)."""
         self._views.clear()
@@ -269,9 +280,18 @@ class ShardedEngine3:
         self.pl = shards[0].pl
         self.jac = variant == "adafac-jac"
         self.lmin = lmin
+        self._fz = {}
 
     def _views(self, field, level):
         return [s.view(field, level) for s in self.shards]
+
+    def _fused(self, level) -> bool:
+        if level not in self._fz:
+            f = {bool(getattr(s, "fused", lambda _l: False)(level)) for s in self.shards}
+            if len(f) != 1:
+                raise RuntimeError(f"shards disagree on the fused smoothing of level {level}")
+            self._fz[level] = f.pop()
+        return self._fz[level]
 
     def cycle(self) -> None:
         pl, tr = self.pl, self.tr
@@ -279,6 +299,13 @@ class ShardedEngine3:
         for l in range(top, ls - 1, -1):
             for s in self.shards:
                 s.phase(_abi.PH_DOWN, l)
+            if self.jac and l > ls and self._fused(l):
+                # smoothing fused with the restriction into l - 1 (sm stays on chip): rho needs
+                # the 3 planes below (sm of the 2 below) and 1 above, no sm halo
+                tr.halo(self._views(_abi.F_RHO, l), l, 3, 1)
+                for s in self.shards:
+                    s.phase(_abi.PH_SMR, l)
+                continue
             tr.halo(self._views(_abi.F_RHO, l), l, 2, 1)
             if self.jac:
                 for s in self.shards:

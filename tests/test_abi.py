@@ -61,7 +61,7 @@ def test_product_package_never_imports_the_oracle():
 def test_3d_entry_points_declared_and_bound():
     decl = declared_symbols()
     for name in ("tmg3_create", "tmg3_rebuild", "tmg3_shard", "tmg3_phase", "tmg3_field",
-                 "tmg3_stream", "tmg3_history", "tmg_dim"):
+                 "tmg3_stream", "tmg3_history", "tmg3_fused", "tmg_dim"):
         assert name in decl, name
     L = _abi.lib()
     for name in decl:

@@ -66,6 +66,9 @@ def test_gpu_sharded_equals_serial(world, name, variant):
             assert np.array_equal(wls[r].tree.u[l][lo:hi], wl.tree.u[l][lo:hi]), f"rank {r} level {l}"
         for l in range(wl.tree.lmin, pl.ls):
             assert np.array_equal(wls[r].tree.u[l], wl.tree.u[l]), f"rank {r} replicated level {l}"
+    if variant == "adafac-jac" and name.startswith("config5"):
+        # BoxMG adaFACx: the finest level's smoothing runs fused with the restriction (PH_SMR)
+        assert shards[0].fused(top) and not shards[0].fused(pl.ls)
 
 
 def test_gpu_sharded_throttled_equals_serial():
