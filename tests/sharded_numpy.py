@@ -18,8 +18,9 @@ from paper_1903_10367_b200 import _abi
 
 
 class NumpyShard:
-    def __init__(self, wl, pl, rank, variant=None, flavor=None):
+    def __init__(self, wl, pl, rank, variant=None, flavor=None, fuse=False):
         self.pl, self.rank = pl, rank
+        self.fuse = fuse  # emulate tmg3_fused / PH_SMR on the levels above ls
         L = wl.tree.depth
         t = mg3d.Tree(L, wl.tree.lmin)
         t.eps[L] = wl.tree.eps[L].copy()
@@ -108,6 +109,18 @@ class NumpyShard:
         self.carry[l][own] = c[own]
         self.t.u[l][own] = self.t.u[l][own] + c[own]
 
+    def _smr(self, l):
+        """PH_SMR: sm of the owned planes and of the 2 below them, from this shard's rho alone
+        (fresh only with the 3-below / 1-above rho halo), never exchanged; DOWN(l-1) restricts it."""
+        s = mg3d.apply_const(self.rho[l], 1.0)
+        s *= self.cfg.omega * 3.0 / 8.0
+        lo, hi = self.pl.interior(l, self.rank)
+        a = max(lo - 2, 1)
+        self.sm[l][a:hi, 1:-1, 1:-1] = s[a:hi, 1:-1, 1:-1]
+
+    def fused(self, level):
+        return self.fuse and self.cfg.variant == "adafac-jac" and self.pl.ls < level <= self.top
+
     # -- phases -----------------------------------------------------------------
     def phase(self, ph, level=0):
         ls, top, l0 = self.pl.ls, self.top, self.l0
@@ -117,6 +130,9 @@ class NumpyShard:
         elif ph == _abi.PH_SMOOTH:
             if self.cfg.variant == "adafac-jac" and level > l0:
                 self._smooth(level, self._own(level))
+        elif ph == _abi.PH_SMR:
+            assert self.fused(level), level
+            self._smr(level)
         elif ph == _abi.PH_REDUCE:
             pass
         elif ph == _abi.PH_REPL:

@@ -68,16 +68,17 @@ CASES = [("config3", 3, "adafac-jac", "geometric"), ("config5", 3, "adafac-jac",
          ("config3", 4, "adafac-jac", "geometric")]
 
 
+@pytest.mark.parametrize("fuse", [False, True])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("name,levels,variant,flavor", CASES)
-def test_local_sharded_equals_oracle(world, name, levels, variant, flavor):
+def test_local_sharded_equals_oracle(world, name, levels, variant, flavor, fuse):
     mk = workloads.config3 if name == "config3" else workloads.config5
     wl = mk(levels=levels)
     try:
         pl = sharding.plan(levels, world)
     except ValueError:
         pytest.skip("too shallow for this world size")
-    shards = [NumpyShard(wl, pl, r, variant, flavor) for r in range(world)]
+    shards = [NumpyShard(wl, pl, r, variant, flavor, fuse=fuse) for r in range(world)]
     eng = sharding.ShardedEngine3(shards, sharding.LocalTransport(pl), variant)
     n = 4
     hist = eng.run(n)
@@ -87,7 +88,7 @@ def test_local_sharded_equals_oracle(world, name, levels, variant, flavor):
     assert hist == shards[0].history(n)
 
 
-def _gloo_worker(rank, world, port, outdir, name, levels, variant, flavor):
+def _gloo_worker(rank, world, port, outdir, name, levels, variant, flavor, fuse=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -95,7 +96,7 @@ def _gloo_worker(rank, world, port, outdir, name, levels, variant, flavor):
         mk = workloads.config3 if name == "config3" else workloads.config5
         wl = mk(levels=levels)
         pl = sharding.plan(levels, world)
-        shard = NumpyShard(wl, pl, rank, variant, flavor)
+        shard = NumpyShard(wl, pl, rank, variant, flavor, fuse=fuse)
         eng = sharding.ShardedEngine3([shard], sharding.DistTransport(pl, rank), variant)
         hist = eng.run(3)
         np.savez(os.path.join(outdir, f"r{rank}.npz"),
@@ -105,13 +106,14 @@ def _gloo_worker(rank, world, port, outdir, name, levels, variant, flavor):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,variant,flavor", [("config3", "adafac-jac", "geometric"),
-                                                 ("config5", "adafac-jac", "boxmg")])
-def test_gloo_two_ranks_equal_oracle(name, variant, flavor):
+@pytest.mark.parametrize("name,variant,flavor,fuse", [("config3", "adafac-jac", "geometric", False),
+                                                      ("config5", "adafac-jac", "boxmg", False),
+                                                      ("config5", "adafac-jac", "boxmg", True)])
+def test_gloo_two_ranks_equal_oracle(name, variant, flavor, fuse):
     world, levels = 2, 3
-    port = 29500 + (os.getpid() % 1000)
+    port = 29500 + (os.getpid() % 1000) + (7 if fuse else 0)
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_gloo_worker, args=(world, port, d, name, levels, variant, flavor), nprocs=world,
+        mp.spawn(_gloo_worker, args=(world, port, d, name, levels, variant, flavor, fuse), nprocs=world,
                  join=True)
         mk = workloads.config3 if name == "config3" else workloads.config5
         wl = mk(levels=levels)
