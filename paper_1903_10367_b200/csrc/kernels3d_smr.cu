@@ -273,9 +273,21 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
     issue_tab(p0 / 3 + 2);
   }
 
-  // step t: C completes sm(t-1) from rho(t); D restricts fine plane t-2
+  // step t: C completes sm(t-1) from rho(t); D restricts fine plane t-2.  Running counters (no
+  // integer division in the step): rsl / rph = ring slot and barrier parity of rho(t), m3c / oc =
+  // floor(s / 3) and s mod 3 of s = t - 2 (p0 is a multiple of 3)
+  int rsl = 0, m3c = Ia - 2, oc = 1;
+  unsigned rph = 0u;
   for (int t = p0; t <= pEnd + 1; ++t) {
     if (t > p0) {
+      if (++rsl == kRStages) {
+        rsl = 0;
+        rph ^= 1u;
+      }
+      if (++oc == 3) {
+        oc = 0;
+        ++m3c;
+      }
       __syncthreads();  // step t-1 done: rho(t-3)'s slot and P(t-3)'s set are free, sm(t-2) is written
       if (lt == 0) {
         fence_proxy_async();
@@ -285,19 +297,18 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
     }
     // table slot of plane t/3 + 3 last held plane t/3 - 3 (last read at step t - 5); row set of
     // plane t/3 + 1 last held plane t/3 - 2 (last read at step t - 2)
-    if (DICT && t % 3 == 0 && lt >= kRTasks && lt < kRTasks + 32) {
+    if (DICT && oc == 1 && lt >= kRTasks && lt < kRTasks + 32) {  // t % 3 == 0, t / 3 == m3c + 1
       fence_proxy_async();
-      if (lt == kRTasks) issue_tab(t / 3 + 3);
-      issue_rows(t / 3 + 1, lt - kRTasks);
+      if (lt == kRTasks) issue_tab(m3c + 4);
+      issue_rows(m3c + 2, lt - kRTasks);
     }
     if (smoother) {
       // ---- C: sm(t - 1) completes; sm(t), sm(t + 1) advance ------------------------
       // every rho plane's TMA is waited for here (also without smoothing): a slot is re-armed only
       // after its previous load completed, and no load is in flight when the CTA exits
-      const int r = t - p0;
-      if (t <= pEnd) mbar_wait(&bar[r % kRStages], (unsigned)(r / kRStages) & 1u);
+      if (t <= pEnd) mbar_wait(&bar[rsl], rph);
       if (A.jac && t <= pEnd) {
-        const double* Rp = sr + (r % kRStages) * kRSlot;
+        const double* Rp = sr + rsl * kRSlot;
         double* Sb = sr + oS + ((t - 1) & 1) * kSBuf;
         const bool sok = t - 1 >= 1 && t - 1 <= N - 2;
 #pragma unroll
@@ -336,15 +347,17 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
       const int s = t - 2;
       if (s >= s0) {
         const int ps = s - s0, rs_ = s - p0;
+        const int ssl = rsl >= 2 ? rsl - 2 : rsl + kRStages - 2;  // slot / parity of rho(s)
+        const unsigned sph = rsl >= 2 ? rph : rph ^ 1u;
         if (!DICT) mbar_wait(&pbar[ps % kPStages], (unsigned)(ps / kPStages) & 1u);
-        mbar_wait(&bar[rs_ % kRStages], (unsigned)(rs_ / kRStages) & 1u);  // rho(s): visibility of the TMA write
+        mbar_wait(&bar[ssl], sph);  // rho(s): visibility of the TMA write
         // fine plane s feeds coarse plane m3 (offset o) and, for o >= 1, m3 + 1 (offset o - 3);
         // this role's plane among them (warp-uniform)
-        const int m3 = floor3s(s), o = s - 3 * m3;
+        const int m3 = m3c, o = oc;
         if constexpr (RV == 1) {
           const bool c = m3 >= Ia && m3 < Ib, nx = o >= 1 && m3 + 1 >= Ia && m3 + 1 < Ib;
           if (rtask) {
-            const double* xr = sr + (rs_ % kRStages) * kRSlot + (3 * wj + 3) * kRW + 3 * wk + 3;
+            const double* xr = sr + ssl * kRSlot + (3 * wj + 3) * kRW + 3 * wk + 3;
             const double* xs = sr + oS + (s & 1) * kSBuf + (3 * wj + 2) * kRW + 3 * wk + 2;
             const double* wc = nullptr;
             const double* wn = nullptr;
