@@ -185,18 +185,20 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
   // smoothing threads: groups of GH sm columns (jj .. jj + GH - 1) at kk -- the group's 3 x 3 rho
   // neighbourhoods share rows (3 (GH + 2) shared loads per GH columns) -- and the columns'
   // pending partial sums
-  int spair[kSPairs];
-  bool sin_[kSCols];
+  // per group: its window offset (rows GH jp .., column kk) and the interior mask of its columns
+  int sbase[kSPairs];
+  unsigned smask[kSPairs];
   double SEa[kSCols], SCa[kSCols], XA[kSCols], SEb[kSCols], SCb[kSCols];
 #pragma unroll
   for (int m = 0; m < kSPairs; ++m) {
     const int q2 = lt + m * kRTasks;
     const int jp = q2 / kSW, kk = q2 - jp * kSW;
-    spair[m] = (smoother && q2 < kSGroups) ? q2 : -1;
+    sbase[m] = (smoother && q2 < kSGroups) ? (GH * jp) * kRW + kk : -1;
+    smask[m] = 0u;
 #pragma unroll
     for (int h = 0; h < GH; ++h) {
       const int j = fj0 + 1 + GH * jp + h, k = fk0 + 1 + kk;
-      sin_[GH * m + h] = q2 < kSGroups && j >= 1 && k >= 1 && j <= N - 2 && k <= N - 2;
+      if (q2 < kSGroups && j >= 1 && k >= 1 && j <= N - 2 && k <= N - 2) smask[m] |= 1u << h;
     }
   }
 #pragma unroll
@@ -313,11 +315,10 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
         const bool sok = t - 1 >= 1 && t - 1 <= N - 2;
 #pragma unroll
         for (int mp = 0; mp < kSPairs; ++mp) {
-          if (spair[mp] < 0) continue;
-          const int q2 = spair[mp];
-          const int jp = q2 / kSW, kk = q2 - jp * kSW;
+          if (sbase[mp] < 0) continue;
           // rows GH jp - 1 .. GH jp + GH, cols kk - 1 .. kk + 1 of the sm window (rho window + 1)
-          const int rb = (GH * jp) * kRW + kk;
+          const int rb = sbase[mp];
+          const unsigned mk = sok ? smask[mp] : 0u;
           double R[GH + 2][3];
 #pragma unroll
           for (int a = 0; a < GH + 2; ++a)
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
             double sc = (((SCa[m] + d0) + d1) + d2) + d3;
             double v = ((C_D8 * XA[m]) - (C_E6 * se)) - (C_C12 * sc);
             v = v * A.scale;
-            Sb[(GH * jp + h) * kRW + kk] = (sok && sin_[m]) ? v : 0.0;
+            Sb[rb + h * kRW] = ((mk >> h) & 1u) ? v : 0.0;
             SEa[m] = (((SEb[m] + d0) + d1) + d2) + d3;
             SCa[m] = SCb[m];
             XA[m] = xc;
