@@ -279,6 +279,7 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
   // integer division in the step): rsl / rph = ring slot and barrier parity of rho(t), m3c / oc =
   // floor(s / 3) and s mod 3 of s = t - 2 (p0 is a multiple of 3)
   int rsl = 0, m3c = Ia - 2, oc = 1;
+  int k3c = 1, k6c = 4;  // (m3c - Ia) mod 3 / mod kRNT: the row set / table slot of plane m3c
   unsigned rph = 0u;
   for (int t = p0; t <= pEnd + 1; ++t) {
     if (t > p0) {
@@ -289,6 +290,8 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
       if (++oc == 3) {
         oc = 0;
         ++m3c;
+        k3c = k3c == 2 ? 0 : k3c + 1;
+        k6c = k6c == kRNT - 1 ? 0 : k6c + 1;
       }
       __syncthreads();  // step t-1 done: rho(t-3)'s slot and P(t-3)'s set are free, sm(t-2) is written
       if (lt == 0) {
@@ -364,10 +367,13 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
             const double* wn = nullptr;
             int ws;
             if (DICT) {
-              if (c) wc = rows_of(m3) + tab_of(m3)[kRTabLoc + w] * kRRowS + (o + 2) * 25;
+              const double* rows = sr + oRRows;
+              const uint8_t* tabs = reinterpret_cast<const uint8_t*>(sr + oRTab) + kRTabLoc + w;
+              if (c) wc = rows + k3c * kRRowSet + tabs[k6c * kRTabBytes] * kRRowS + (o + 2) * 25;
               if (nx) {
                 if (o == 1) wait_plane(m3 + 1);
-                wn = rows_of(m3 + 1) + tab_of(m3 + 1)[kRTabLoc + w] * kRRowS + (o - 1) * 25;
+                const int k3n = k3c == 2 ? 0 : k3c + 1, k6n = k6c == kRNT - 1 ? 0 : k6c + 1;
+                wn = rows + k3n * kRRowSet + tabs[k6n * kRTabBytes] * kRRowS + (o - 1) * 25;
               }
               ws = 1;
             } else {
