@@ -532,6 +532,13 @@ static int smr_rv() {
   return s ? atoi(s) : 1;
 }
 
+// the decoupled smoothing / restriction schedule (named barriers per sm buffer; dictionary P
+// only): default, TMG_SMR_DEC=0 keeps the one-barrier-per-step schedule (config 5 L6: 2.80-2.83
+// vs 2.85-2.92 ms, cycle 9.02-9.05 vs 9.11-9.12 ms)
+static int smr_dec() {
+  const char* s = getenv("TMG_SMR_DEC");
+  return s ? atoi(s) : 1;
+}
 static int smr_gh() {
   const char* s = getenv("TMG_SMR_GH");
   return s ? atoi(s) : 7;
@@ -580,7 +587,9 @@ int launch_smr(Engine3* e, int l, bool smooth, int clo = -1, int chi = -1) {
   const dim3 grid(tiles, (n + A.chunk - 1) / A.chunk);
   cudaEvent_t e0_ = nullptr;
   TRY3(begin_k(e, &e0_));
-  if (smr_rv() == 1 && smr_gh() == 7) {
+  if (cc.Pd && smr_dec() && smr_rv() == 1 && smr_gh() == 7) {
+    k3_smr<true, 1, 7, true><<<grid, kRTasks + kRK * kRJ, kSmrSmemDB, e->s>>>(A);
+  } else if (smr_rv() == 1 && smr_gh() == 7) {
     if (cc.Pd) k3_smr<true, 1, 7><<<grid, kRTasks + kRK * kRJ, kSmrSmemD, e->s>>>(A);
     else k3_smr<false, 1, 7><<<grid, kRTasks + kRK * kRJ, kSmrSmem, e->s>>>(A);
   } else if (smr_rv() == 1) {
@@ -1265,6 +1274,7 @@ int build(Engine3* e, const tmg_tree3* t) {
       CK3(cudaFuncSetAttribute(k3_smr<true, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmemD));
       CK3(cudaFuncSetAttribute(k3_smr<false, 1, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmem));
       CK3(cudaFuncSetAttribute(k3_smr<true, 1, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmemD));
+      CK3(cudaFuncSetAttribute(k3_smr<true, 1, 7, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmemDB));
       for (int l = e->smr_lo - 1; l < l1; ++l) {
         Lvl3& cc = e->L[l];
         if (!cc.bR) TRY3(alloc3(e, &cc.bR, cc.nv));

@@ -80,6 +80,18 @@ constexpr int oRRows = oRTab + kRNT * kRTabBytes / 8;
 constexpr int kRRowSet = kRRows * kRRowS;
 constexpr int oRSd = oRRows + 3 * kRRowSet;
 constexpr size_t kSmrSmemD = sizeof(double) * (oRSd + 2 * kSBuf);
+// decoupled schedule (DEC): six rho slots and three sm buffers, so the restriction may lag the
+// smoothing by up to three fine planes
+constexpr int kRStagesB = 6;
+constexpr size_t kSmrSmemDB =
+    sizeof(double) * (kRStagesB * kRSlot + kRNT * kRTabBytes / 8 + 3 * kRRowSet + 3 * kSBuf);
+static_assert(kSmrSmemDB + 256 <= 227 * 1024, "DEC layout exceeds shared memory");
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 constexpr unsigned kRRowBytes = 126 * 8;  // 125 weights, rounded to 16 bytes (rows are 1 KB)
 
 // tables of the dictionary variant: one thread per (coarse plane m, tile); *over = 1 when a tile
@@ -165,11 +177,16 @@ __device__ __forceinline__ void terms2(const double* wc, const double* wn, int w
   }
 }
 
-template <bool DICT, int RV, int GH>
+template <bool DICT, int RV, int GH, bool DEC = false>
 __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_smr(const __grid_constant__ Smr A) {
+  static_assert(!DEC || (DICT && RV == 1), "the decoupled schedule needs the dictionary and RV 1");
   constexpr int kSPairs = kSPer<GH>, kSCols = GH * kSPairs, kSGroups = kSW * (kSH / GH);
+  constexpr int kRStages = DEC ? kRStagesB : t3::kRStages;  // rho slots
+  constexpr int oRTab = kRStages * kRSlot;
+  constexpr int oRRows = oRTab + kRNT * kRTabBytes / 8;
+  constexpr int oRSd = oRRows + 3 * kRRowSet;
   extern __shared__ __align__(128) double sr[];
-  __shared__ __align__(8) uint64_t bar[kRStages], pbar[kPStages], tbar[kRNT], rbar[3];
+  __shared__ __align__(8) uint64_t bar[kRStagesB], pbar[kPStages], tbar[kRNT], rbar[3];
   const int N = A.N, Nc = A.Nc, n = Nc - 2;
   const int tk = blockIdx.x % A.tilesK, tj = blockIdx.x / A.tilesK;
   const int K0 = 1 + tk * kRK, J0 = 1 + tj * kRJ;
@@ -275,47 +292,8 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
     issue_tab(p0 / 3 + 2);
   }
 
-  // step t: C completes sm(t-1) from rho(t); D restricts fine plane t-2.  Running counters (no
-  // integer division in the step): rsl / rph = ring slot and barrier parity of rho(t), m3c / oc =
-  // floor(s / 3) and s mod 3 of s = t - 2 (p0 is a multiple of 3)
-  int rsl = 0, m3c = Ia - 2, oc = 1;
-  int k3c = 1, k6c = 4;  // (m3c - Ia) mod 3 / mod kRNT: the row set / table slot of plane m3c
-  unsigned rph = 0u;
-  for (int t = p0; t <= pEnd + 1; ++t) {
-    if (t > p0) {
-      if (++rsl == kRStages) {
-        rsl = 0;
-        rph ^= 1u;
-      }
-      if (++oc == 3) {
-        oc = 0;
-        ++m3c;
-        k3c = k3c == 2 ? 0 : k3c + 1;
-        k6c = k6c == kRNT - 1 ? 0 : k6c + 1;
-      }
-      __syncthreads();  // step t-1 done: rho(t-3)'s slot and P(t-3)'s set are free, sm(t-2) is written
-      if (lt == 0) {
-        fence_proxy_async();
-        if (t + 2 <= pEnd) issue_r(t + 2);                              // into the slot of plane t - 3
-        if (t - 1 >= s0 + kPStages && t - 1 <= pEnd - 1) issue_p(t - 1);  // into the set of plane t - 3
-      }
-    }
-    // table slot of plane t/3 + 3 last held plane t/3 - 3 (last read at step t - 5); row set of
-    // plane t/3 + 1 last held plane t/3 - 2 (last read at step t - 2)
-    if (DICT && oc == 1 && lt >= kRTasks && lt < kRTasks + 32) {  // t % 3 == 0, t / 3 == m3c + 1
-      fence_proxy_async();
-      if (lt == kRTasks) issue_tab(m3c + 4);
-      issue_rows(m3c + 2, lt - kRTasks);
-    }
-    if (smoother) {
-      // ---- C: sm(t - 1) completes; sm(t), sm(t + 1) advance ------------------------
-      // every rho plane's TMA is waited for here (also without smoothing): a slot is re-armed only
-      // after its previous load completed, and no load is in flight when the CTA exits
-      if (t <= pEnd) mbar_wait(&bar[rsl], rph);
-      if (A.jac && t <= pEnd) {
-        const double* Rp = sr + rsl * kRSlot;
-        double* Sb = sr + oS + ((t - 1) & 1) * kSBuf;
-        const bool sok = t - 1 >= 1 && t - 1 <= N - 2;
+  // C: sm of the plane below rho's slot Rp completes into Sb (pending partial sums advance)
+  auto smooth_body = [&](const double* Rp, double* Sb, bool sok) {
 #pragma unroll
         for (int mp = 0; mp < kSPairs; ++mp) {
           if (sbase[mp] < 0) continue;
@@ -345,24 +323,13 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
             SCb[m] = ((d0 + d1) + d2) + d3;
           }
         }
-      }
-    } else {
-      // ---- D: restriction of fine plane s = t - 2 (rho from its slot, sm(s) from its buffer) ----
-      const int s = t - 2;
-      if (s >= s0) {
-        const int ps = s - s0, rs_ = s - p0;
-        const int ssl = rsl >= 2 ? rsl - 2 : rsl + kRStages - 2;  // slot / parity of rho(s)
-        const unsigned sph = rsl >= 2 ? rph : rph ^ 1u;
-        if (!DICT) mbar_wait(&pbar[ps % kPStages], (unsigned)(ps / kPStages) & 1u);
-        mbar_wait(&bar[ssl], sph);  // rho(s): visibility of the TMA write
-        // fine plane s feeds coarse plane m3 (offset o) and, for o >= 1, m3 + 1 (offset o - 3);
-        // this role's plane among them (warp-uniform)
-        const int m3 = m3c, o = oc;
-        if constexpr (RV == 1) {
+  };
+  // D (RV 1): restriction of fine plane s (rho in slot ssl, sm in smb) into coarse planes m3 / m3+1
+  auto restrict_body = [&](int s, int ssl, int m3, int o, int k3c, int k6c, const double* smb, int ps) {
           const bool c = m3 >= Ia && m3 < Ib, nx = o >= 1 && m3 + 1 >= Ia && m3 + 1 < Ib;
           if (rtask) {
             const double* xr = sr + ssl * kRSlot + (3 * wj + 3) * kRW + 3 * wk + 3;
-            const double* xs = sr + oS + (s & 1) * kSBuf + (3 * wj + 2) * kRW + 3 * wk + 2;
+            const double* xs = smb + (3 * wj + 2) * kRW + 3 * wk + 2;
             const double* wc = nullptr;
             const double* wn = nullptr;
             int ws;
@@ -403,6 +370,122 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
               accNR = accNS = 0.0;
             }
           }
+  };
+  if constexpr (DEC) {
+    // Decoupled: the smoothing threads (barrier 7 among themselves) and the restriction threads
+    // meet only through named barriers per sm buffer b (plane x in buffer (x - p0) % 3):
+    //   FULL 1 + b   smoothing arrives when sm(x) is complete, the restriction syncs before x;
+    //   EMPTY 4 + b  the restriction arrives when done with plane x (sm(x), rho(x)), the
+    //                smoothing syncs before writing sm(x + 3) and re-arming rho(x)'s slot.
+    // The restriction may lag by three planes; every arrive has exactly one matching sync.
+    constexpr int kAll = kRTasks + kRK * kRJ;
+    auto sbuf = [&](int x) { return (x - p0 + 3) % 3; };  // x >= p0 - 1
+    if (smoother) {
+      int rsl = 0;
+      unsigned rph = 0u;
+      for (int t = p0; t <= pEnd; ++t) {
+        if (t > p0 && ++rsl == kRStages) {
+          rsl = 0;
+          rph ^= 1u;
+        }
+        named_sync(7, kRTasks);  // the group left step t - 1 (rho(t - 4)'s slot is free for it)
+        // buffer of t - 1 last held t - 4 and rho(t + 2)'s slot rho(t - 4): the restriction is done
+        if (t - 1 >= s0 + 3) named_sync(4 + sbuf(t - 1), kAll);
+        if (lt == 0 && t > p0 && t + 2 <= pEnd) {
+          fence_proxy_async();
+          issue_r(t + 2);
+        }
+        mbar_wait(&bar[rsl], rph);
+        if (A.jac) smooth_body(sr + rsl * kRSlot, sr + oS + sbuf(t - 1) * kSBuf, t - 1 >= 1 && t - 1 <= N - 2);
+        if (t - 1 >= s0) named_arrive(1 + sbuf(t - 1), kAll);
+      }
+    } else {
+      if (lt < kRTasks + 32) {  // the first planes' table and rows (step t = p0 of the coupled loop)
+        fence_proxy_async();
+        if (lt == kRTasks) issue_tab(Ia + 2);
+        issue_rows(Ia, lt - kRTasks);
+      }
+      int ssl = 1, m3c = Ia - 1, oc = 1, k3c = 2, k6c = kRNT - 1;  // s = s0 = p0 + 1
+      unsigned sph = 0u;
+      for (int s = s0; s <= pEnd - 1; ++s) {
+        if (s > s0) {
+          if (++ssl == kRStages) {
+            ssl = 0;
+            sph ^= 1u;
+          }
+          if (++oc == 3) {
+            oc = 0;
+            ++m3c;
+            k3c = k3c == 2 ? 0 : k3c + 1;
+            k6c = k6c == kRNT - 1 ? 0 : k6c + 1;
+          }
+        }
+        named_sync(1 + sbuf(s), kAll);  // sm(s) complete; every restriction thread left s - 1
+        if (oc == 1 && lt < kRTasks + 32) {
+          fence_proxy_async();
+          if (lt == kRTasks) issue_tab(m3c + 4);
+          issue_rows(m3c + 2, lt - kRTasks);
+        }
+        mbar_wait(&bar[ssl], sph);
+        restrict_body(s, ssl, m3c, oc, k3c, k6c, sr + oS + sbuf(s) * kSBuf, s - s0);
+        if (s + 3 <= pEnd - 1) named_arrive(4 + sbuf(s), kAll);
+      }
+    }
+    return;
+  }
+
+  // step t: C completes sm(t-1) from rho(t); D restricts fine plane t-2.  Running counters (no
+  // integer division in the step): rsl / rph = ring slot and barrier parity of rho(t), m3c / oc =
+  // floor(s / 3) and s mod 3 of s = t - 2 (p0 is a multiple of 3)
+  int rsl = 0, m3c = Ia - 2, oc = 1;
+  int k3c = 1, k6c = 4;  // (m3c - Ia) mod 3 / mod kRNT: the row set / table slot of plane m3c
+  unsigned rph = 0u;
+  for (int t = p0; t <= pEnd + 1; ++t) {
+    if (t > p0) {
+      if (++rsl == kRStages) {
+        rsl = 0;
+        rph ^= 1u;
+      }
+      if (++oc == 3) {
+        oc = 0;
+        ++m3c;
+        k3c = k3c == 2 ? 0 : k3c + 1;
+        k6c = k6c == kRNT - 1 ? 0 : k6c + 1;
+      }
+      __syncthreads();  // step t-1 done: rho(t-3)'s slot and P(t-3)'s set are free, sm(t-2) is written
+      if (lt == 0) {
+        fence_proxy_async();
+        if (t + 2 <= pEnd) issue_r(t + 2);                              // into the slot of plane t - 3
+        if (t - 1 >= s0 + kPStages && t - 1 <= pEnd - 1) issue_p(t - 1);  // into the set of plane t - 3
+      }
+    }
+    // table slot of plane t/3 + 3 last held plane t/3 - 3 (last read at step t - 5); row set of
+    // plane t/3 + 1 last held plane t/3 - 2 (last read at step t - 2)
+    if (DICT && oc == 1 && lt >= kRTasks && lt < kRTasks + 32) {  // t % 3 == 0, t / 3 == m3c + 1
+      fence_proxy_async();
+      if (lt == kRTasks) issue_tab(m3c + 4);
+      issue_rows(m3c + 2, lt - kRTasks);
+    }
+    if (smoother) {
+      // ---- C: sm(t - 1) completes; sm(t), sm(t + 1) advance ------------------------
+      // every rho plane's TMA is waited for here (also without smoothing): a slot is re-armed only
+      // after its previous load completed, and no load is in flight when the CTA exits
+      if (t <= pEnd) mbar_wait(&bar[rsl], rph);
+      if (A.jac && t <= pEnd) smooth_body(sr + rsl * kRSlot, sr + oS + ((t - 1) & 1) * kSBuf, t - 1 >= 1 && t - 1 <= N - 2);
+    } else {
+      // ---- D: restriction of fine plane s = t - 2 (rho from its slot, sm(s) from its buffer) ----
+      const int s = t - 2;
+      if (s >= s0) {
+        const int ps = s - s0, rs_ = s - p0;
+        const int ssl = rsl >= 2 ? rsl - 2 : rsl + kRStages - 2;  // slot / parity of rho(s)
+        const unsigned sph = rsl >= 2 ? rph : rph ^ 1u;
+        if (!DICT) mbar_wait(&pbar[ps % kPStages], (unsigned)(ps / kPStages) & 1u);
+        mbar_wait(&bar[ssl], sph);  // rho(s): visibility of the TMA write
+        // fine plane s feeds coarse plane m3 (offset o) and, for o >= 1, m3 + 1 (offset o - 3);
+        // this role's plane among them (warp-uniform)
+        const int m3 = m3c, o = oc;
+        if constexpr (RV == 1) {
+          restrict_body(s, ssl, m3, o, k3c, k6c, sr + oS + (s & 1) * kSBuf, ps);
           continue;
         }
         int m = -1, off = 0;

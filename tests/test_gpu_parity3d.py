@@ -256,13 +256,15 @@ def test_3d_weight_dictionary_equals_dense(variant, wname, monkeypatch):
         assert np.array_equal(wl1.tree.u[l], wl2.tree.u[l]), f"level {l}"
 
 
-@pytest.mark.parametrize("layout", [("0", "2"), ("1", "2")])
+@pytest.mark.parametrize("layout", [("0", "2", "0"), ("1", "2", "0"), ("1", "7", "0")])
 @pytest.mark.parametrize("wname", ["config5-L5", "random-L5"])
 def test_3d_smr_layouts_equal(layout, wname, monkeypatch):
     """k3_smr's thread layouts -- the default (restriction thread per coarse vertex over both
-    planes and fields, 7-column smoothing groups) and the earlier ones (TMG_SMR_RV=0: two roles
-    owning alternate planes; TMG_SMR_GH=2: column pairs) -- give the same iterate bit for bit,
-    on the dictionary (blockwise eps) and the dense (per-cell eps) weight paths."""
+    planes and fields, 7-column smoothing groups, smoothing and restriction decoupled by named
+    barriers) and the earlier ones (TMG_SMR_RV=0: two roles owning alternate planes;
+    TMG_SMR_GH=2: column pairs; TMG_SMR_DEC=0: one CTA barrier per fine plane) -- give the same
+    iterate bit for bit, on the dictionary (blockwise eps) and the dense (per-cell eps) weight
+    paths."""
     def make():
         if wname == "config5-L5":
             return workloads.config5(levels=5, block=27)
@@ -276,6 +278,7 @@ def test_3d_smr_layouts_equal(layout, wname, monkeypatch):
     e1, h1 = gpu_run(wl1, n, "adafac-jac")
     monkeypatch.setenv("TMG_SMR_RV", layout[0])
     monkeypatch.setenv("TMG_SMR_GH", layout[1])
+    monkeypatch.setenv("TMG_SMR_DEC", layout[2])
     wl2 = make()
     e2, h2 = gpu_run(wl2, n, "adafac-jac")
     assert [s.l2h for s in h1] == [s.l2h for s in h2]
