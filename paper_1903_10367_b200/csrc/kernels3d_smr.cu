@@ -25,7 +25,12 @@
 //           stores them when the plane completes.
 // One weight load feeds both fields' products.  Same per-element DAGs as
 // k3_smooth2r and k3_down_c: b_R, b_T and everything after them are bitwise
-// unchanged.  Default layout (engine3.cu: smr_rv / smr_gh): 256 smoothing threads
+// unchanged.  Default schedule (engine3.cu: smr_dec; dictionary P): smoothing and
+// restriction threads are decoupled -- they meet only through named barriers per
+// sm buffer (full / empty pairs over three sm buffers, six rho slots), so the
+// restriction lags the smoothing by up to three fine planes and its 25 | 50 | 50
+// terms per step average out (2.80 vs 2.85-2.92 ms with one CTA barrier per
+// step).  Default layout (engine3.cu: smr_rv / smr_gh): 256 smoothing threads
 // owning groups of 7 sm columns (27 shared loads per 7 columns), 128 restriction
 // threads, one per coarse vertex, carrying both coarse planes a fine plane feeds
 // and both fields (the 5 x 5 x 2 window is read once for both planes) --
