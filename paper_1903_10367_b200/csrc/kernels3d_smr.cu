@@ -393,9 +393,11 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
           rsl = 0;
           rph ^= 1u;
         }
-        named_sync(7, kRTasks);  // the group left step t - 1 (rho(t - 4)'s slot is free for it)
         // buffer of t - 1 last held t - 4 and rho(t + 2)'s slot rho(t - 4): the restriction is done
+        // with them, and (a sync of every thread) the smoothing group left step t - 1; before the
+        // first such step the group syncs alone (rho(t - 4)'s slot)
         if (t - 1 >= s0 + 3) named_sync(4 + sbuf(t - 1), kAll);
+        else named_sync(7, kRTasks);
         if (lt == 0 && t > p0 && t + 2 <= pEnd) {
           fence_proxy_async();
           issue_r(t + 2);
