@@ -178,7 +178,8 @@ def bytes_model3(eng, wl):
         out[f"k3_down_L{l}"] = b
         if jac and l > l0:
             out[f"k3_smooth_L{l}"] = 16 * n
-        up = n * (16 + 8 + (8 if l < L else 0))
+        # u r/w + g (+ carry); the finest level keeps g inside its double-buffered u (Engine3::pp)
+        up = n * (16 + (8 if l < L or wl.variant == "adafac-pi" else 0) + (8 if l < L else 0))
         if l > l0:
             up += dofs[l - 1] * (8 + (992 if boxmg else 0))
         out[f"k3_up_L{l}"] = up
@@ -188,8 +189,7 @@ def bytes_model3(eng, wl):
             lc = l
     # k3_smr (the engine's default for BoxMG but adafac-pi): a level's smoothing and its restriction
     # into the next coarser level run in one kernel named k3_smooth_L{l}; k3_down_L{l-1} reads b_R / b_T
-    smr = (boxmg and wl.variant != "adafac-pi" and L - 1 > lc and os.environ.get("TMG_SMR", "1") != "0"
-           and os.environ.get("TMG_FFP", "0") not in ("1", "4"))
+    smr = boxmg and wl.variant != "adafac-pi" and L - 1 > lc
     if smr:  # every level l >= lc + 2 smooths and restricts into l - 1 in k3_smooth_L{l}
         nb = 2 if jac else 1
         for l in range(lc + 2, L + 1):
@@ -285,29 +285,6 @@ def cpu_port_time(wl_name: str, cycles: int, budget_s: float = 20.0):
     t0 = time.perf_counter()
     eng = oracle_engine(wl)
     setup = time.perf_counter() - t0
-    eng.advance()  # warm-up
-    done, t0 = 0, time.perf_counter()
-    while done < cycles:
-        eng.advance()
-        done += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = (time.perf_counter() - t0) / done
-    return dt, done, setup, wl
-
-
-def _unused_cpu_port_time2(wl_name: str, cycles: int, budget_s: float = 20.0):
-    from oracle import mg2d
-    from paper_1903_10367_b200 import workloads
-    wl = workloads.by_name(wl_name)
-    t = mg2d.Tree(lmin=wl.tree.lmin, lmax=wl.tree.lmax)
-    t.refined = [r.copy() for r in wl.tree.refined]
-    t.u = [u.copy() for u in wl.tree.u]
-    t.eps = [e.copy() for e in wl.tree.eps]
-    t0 = time.perf_counter()
-    eng = mg2d.Engine(t, mg2d.Config(variant=wl.variant, flavor=wl.flavor))
-    setup = time.perf_counter() - t0
-    eng.rhs.update(wl.rhs)
     eng.advance()  # warm-up
     done, t0 = 0, time.perf_counter()
     while done < cycles:

@@ -205,12 +205,9 @@ inline unsigned tiles_y(int N, int ty = tmg::kTileY) { return (unsigned)((N + ty
 
 // Coarse grid levels run 32 x kCoarseTileY tiles: their per-vertex work is
 // heavy (BoxMG restriction + R~ from P, ~200 registers) and they have few
-// vertices, so small CTAs spread them over more SMs (TMG_CTY overrides).
-const int kCoarseTileY = [] {
-  const char* v = std::getenv("TMG_CTY");
-  const int t = v ? std::atoi(v) : 2;
-  return (t == 1 || t == 2 || t == 4 || t == 8) ? t : 2;
-}();
+// vertices, so small CTAs spread them over more SMs (measured at config 2: 2
+// beats 1, 4 and 8).
+constexpr int kCoarseTileY = 2;
 
 #define LAUNCH_TILES(h, name, kernel, N, TY, ...)                                      \
   do {                                                                                 \
@@ -251,13 +248,9 @@ tmg::DownArgs make_down(tmg_handle* h, int l, bool write) {
     a.boxmg = h->cfg.flavor == TMG_BOXMG;
     a.P = c.P;
     a.Rt = c.Rt;
+    // R~ rebuilt from the P registers (RT_FROM_P) beat reading the stored
+    // table on every level of config 2 (measured)
     a.rt_mode = c.rt_mode;
-    if (a.rt_mode == tmg::RT_FROM_P) {
-      // R~ rebuilt from the P registers beat reading the stored table on every
-      // level of config 2 (measured); TMG_RT=table selects the table path.
-      const char* env = std::getenv("TMG_RT");
-      if (env && std::strcmp(env, "table") == 0) a.rt_mode = tmg::RT_TABLE;
-    }
     const double c1 = 1.0 / 3.0;  // interior_stencil(1.0) (discretization.py:165-167)
     a.rt_side = c1 * -1.0;
     a.rt_mid = c1 * 8.0;
@@ -308,11 +301,8 @@ tmg::UpArgs make_up(tmg_handle* h, int l) {
   return a;
 }
 
-// the coarse chain on a thread-block cluster (TMG_CHAIN=block: one CTA)
-const bool kChainCluster = [] {
-  const char* v = std::getenv("TMG_CHAIN");
-  return !(v && v[0] == 'b');
-}();
+// the coarse chain runs on a thread-block cluster (53 -> 41 us at config 2 against one CTA)
+constexpr bool kChainCluster = true;
 
 int launch_coarse(tmg_handle* h, bool write) {
   tmg::CoarseArgs a{};
@@ -724,6 +714,21 @@ int read_stats(tmg_handle* h, long long first, int count, tmg_stats* out) {
   return TMG_OK;
 }
 
+// Every entry point that takes a handle runs on the handle's device and restores
+// the caller's current device on return (a process may hold engines on several
+// GPUs, and torch may switch the current device between calls).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const tmg_handle* h) {
+    int cur = -1;
+    if (h && cudaGetDevice(&cur) == cudaSuccess && cur != h->cfg.device && cudaSetDevice(h->cfg.device) == cudaSuccess)
+      prev = cur;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 }  // namespace
 
 // ============================================================================
@@ -806,6 +811,7 @@ int tmg3_create(const tmg_tree3* tree, const tmg_config* cfg, tmg_handle** out) 
 }
 
 int tmg3_rebuild(tmg_handle* h, const tmg_tree3* tree) {
+  DeviceGuard dg_(h);
   if (!h || !tree || !h->e3) return fail(TMG_EINVAL, "null argument or not a 3D handle");
   CK(cudaSetDevice(h->cfg.device));
   return e3_rebuild(h->e3, tree, g_err);
@@ -814,41 +820,49 @@ int tmg3_rebuild(tmg_handle* h, const tmg_tree3* tree) {
 int tmg_dim(tmg_handle* h) { return (h && h->e3) ? 3 : 2; }
 
 int tmg3_shard(tmg_handle* h, int32_t ls, const int32_t* lo, const int32_t* hi) {
+  DeviceGuard dg_(h);
   if (!h || !h->e3 || !lo || !hi) return fail(TMG_EINVAL, "null argument or not a 3D handle");
   return e3_shard(h->e3, ls, lo, hi, g_err);
 }
 
 int tmg3_phase(tmg_handle* h, int32_t phase, int32_t level) {
+  DeviceGuard dg_(h);
   if (!h || !h->e3) return fail(TMG_EINVAL, "null argument or not a 3D handle");
   return e3_phase(h->e3, phase, level, g_err);
 }
 
 int tmg3_field(tmg_handle* h, int32_t field, int32_t level, uint64_t* ptr, int64_t* count) {
+  DeviceGuard dg_(h);
   if (!h || !h->e3 || !ptr || !count) return fail(TMG_EINVAL, "null argument or not a 3D handle");
   return e3_field(h->e3, field, level, ptr, count, g_err);
 }
 
 int tmg3_storage(tmg_handle* h, int32_t level, int64_t* out) {
+  DeviceGuard dg_(h);
   if (!h || !h->e3 || !out) return fail(TMG_EINVAL, "null argument or not a 3D handle");
   return e3_storage(h->e3, level, out, g_err);
 }
 
 int tmg3_fused(tmg_handle* h, int32_t level, int32_t* out) {
+  DeviceGuard dg_(h);
   if (!h || !h->e3 || !out) return fail(TMG_EINVAL, "null argument or not a 3D handle");
   return e3_fused(h->e3, level, out, g_err);
 }
 
 int tmg3_stream(tmg_handle* h, uint64_t* stream) {
+  DeviceGuard dg_(h);
   if (!h || !h->e3 || !stream) return fail(TMG_EINVAL, "null argument or not a 3D handle");
   return e3_stream(h->e3, stream);
 }
 
 int tmg3_history(tmg_handle* h, int32_t count, tmg_stats* out) {
+  DeviceGuard dg_(h);
   if (!h || !h->e3 || !out) return fail(TMG_EINVAL, "null argument or not a 3D handle");
   return e3_history(h->e3, count, out, g_err);
 }
 
 int tmg_rebuild(tmg_handle* h, const tmg_tree* tree) {
+  DeviceGuard dg_(h);
   if (h && h->e3) return fail(TMG_EINVAL, "3D handle: use tmg3_rebuild");
   if (!h || !tree) return fail(TMG_EINVAL, "null argument");
   CK(cudaSetDevice(h->cfg.device));
@@ -858,6 +872,7 @@ int tmg_rebuild(tmg_handle* h, const tmg_tree* tree) {
 }
 
 int tmg_set_rhs(tmg_handle* h, int32_t level, const double* rhs) {
+  DeviceGuard dg_(h);
   if (h && h->e3) return e3_set_rhs(h->e3, level, rhs, g_err);
   TRY(check_level(h, level));
   Level& c = h->L[level];
@@ -875,6 +890,7 @@ int tmg_set_rhs(tmg_handle* h, int32_t level, const double* rhs) {
 }
 
 int tmg_set_u(tmg_handle* h, int32_t level, const double* u) {
+  DeviceGuard dg_(h);
   if (h && h->e3) return u ? e3_set_u(h->e3, level, u, g_err) : fail(TMG_EINVAL, "null array");
   TRY(check_level(h, level, true));
   if (!u) return fail(TMG_EINVAL, "null array");
@@ -886,6 +902,7 @@ int tmg_set_u(tmg_handle* h, int32_t level, const double* u) {
 }
 
 int tmg_get_u(tmg_handle* h, int32_t level, double* u) {
+  DeviceGuard dg_(h);
   if (h && h->e3) return u ? e3_get_u(h->e3, level, u, g_err) : fail(TMG_EINVAL, "null array");
   TRY(check_level(h, level, true));
   if (!u) return fail(TMG_EINVAL, "null array");
@@ -897,6 +914,7 @@ int tmg_get_u(tmg_handle* h, int32_t level, double* u) {
 }
 
 int tmg_update_fas_state(tmg_handle* h) {
+  DeviceGuard dg_(h);
   if (h && h->e3) return e3_update_fas_state(h->e3, g_err);
   if (!h) return fail(TMG_EINVAL, "null handle");
   TRY(enqueue_fas(h));
@@ -905,6 +923,7 @@ int tmg_update_fas_state(tmg_handle* h) {
 }
 
 int tmg_cycle(tmg_handle* h, int32_t ncycles, tmg_stats* stats) {
+  DeviceGuard dg_(h);
   if (h && h->e3) return e3_cycle(h->e3, ncycles, stats, g_err);
   if (!h) return fail(TMG_EINVAL, "null handle");
   if (ncycles < 0) return fail(TMG_EINVAL, "negative cycle count");
@@ -923,6 +942,7 @@ int tmg_cycle(tmg_handle* h, int32_t ncycles, tmg_stats* stats) {
 }
 
 int tmg_residual_stats(tmg_handle* h, tmg_stats* out) {
+  DeviceGuard dg_(h);
   if (h && h->e3 && out) return e3_residual_stats(h->e3, out, g_err);
   if (!h || !out) return fail(TMG_EINVAL, "null argument");
   TRY(enqueue_down(h, false));
@@ -932,6 +952,7 @@ int tmg_residual_stats(tmg_handle* h, tmg_stats* out) {
 }
 
 int tmg_levels(tmg_handle* h, int32_t* lmin, int32_t* ltop) {
+  DeviceGuard dg_(h);
   if (h && h->e3) return e3_levels(h->e3, lmin, ltop);
   if (!h) return fail(TMG_EINVAL, "null handle");
   if (lmin) *lmin = h->lmin;
@@ -941,6 +962,7 @@ int tmg_levels(tmg_handle* h, int32_t* lmin, int32_t* ltop) {
 
 int tmg_level_counts(tmg_handle* h, int32_t level, int64_t* dof, int64_t* composite,
                      int64_t* hanging) {
+  DeviceGuard dg_(h);
   if (h && h->e3) return e3_level_counts(h->e3, level, dof, composite, hanging, g_err);
   TRY(check_level(h, level));
   const Level& c = h->L[level];
@@ -951,6 +973,7 @@ int tmg_level_counts(tmg_handle* h, int32_t level, int64_t* dof, int64_t* compos
 }
 
 int tmg_get_kinds(tmg_handle* h, int32_t level, int8_t* out) {
+  DeviceGuard dg_(h);
   if (h && h->e3) return e3_get_kinds(h->e3, level, out, g_err);
   TRY(check_level(h, level));
   const Level& c = h->L[level];
@@ -962,6 +985,7 @@ int tmg_get_kinds(tmg_handle* h, int32_t level, int8_t* out) {
 }
 
 int tmg_get_table(tmg_handle* h, int32_t which, int32_t level, double* out) {
+  DeviceGuard dg_(h);
   if (h && h->e3) return e3_get_table(h->e3, which, level, out, g_err);
   TRY(check_level(h, level));
   Level& c = h->L[level];
@@ -1020,6 +1044,7 @@ int tmg_get_table(tmg_handle* h, int32_t which, int32_t level, double* out) {
 }
 
 int tmg_time_cycles(tmg_handle* h, int32_t ncycles, int64_t flush_bytes, float* ms) {
+  DeviceGuard dg_(h);
   if (h && h->e3 && ms) return e3_time_cycles(h->e3, ncycles, flush_bytes, ms, g_err);
   if (!h || !ms) return fail(TMG_EINVAL, "null argument");
   TRY(ensure_graph(h));
@@ -1060,6 +1085,7 @@ int tmg_time_cycles(tmg_handle* h, int32_t ncycles, int64_t flush_bytes, float* 
 
 int tmg_profile_cycles(tmg_handle* h, int32_t ncycles, int32_t cap, const char** names, float* ms,
                        int32_t* launches, int32_t* nk) {
+  DeviceGuard dg_(h);
   if (h && h->e3) return e3_profile_cycles(h->e3, ncycles, cap, names, ms, launches, nk, g_err);
   if (!h) return fail(TMG_EINVAL, "null handle");
   std::vector<KTimer> timers;
@@ -1089,6 +1115,7 @@ int tmg_profile_cycles(tmg_handle* h, int32_t ncycles, int32_t cap, const char**
 }
 
 int tmg_launches_per_cycle(tmg_handle* h, int32_t* n) {
+  DeviceGuard dg_(h);
   if (h && h->e3 && n) return e3_launches_per_cycle(h->e3, n, g_err);
   if (!h || !n) return fail(TMG_EINVAL, "null argument");
   TRY(ensure_graph(h));
@@ -1098,6 +1125,7 @@ int tmg_launches_per_cycle(tmg_handle* h, int32_t* n) {
 
 // diagnostics (not part of tmg.h): %globaltimer stamps of the last k_coarse phases
 int tmg_debug_stamps(tmg_handle* h, unsigned long long* out, int n) {
+  DeviceGuard dg_(h);
   if (!h || !out) return fail(TMG_EINVAL, "null argument");
   CK(cudaMemcpy(out, h->stamps, sizeof(unsigned long long) * std::min(n, 64), cudaMemcpyDeviceToHost));
   return TMG_OK;
@@ -1105,12 +1133,12 @@ int tmg_debug_stamps(tmg_handle* h, unsigned long long* out, int n) {
 
 void tmg_destroy(tmg_handle* h) {
   if (!h) return;
+  DeviceGuard dg_(h);
   if (h->e3) {
     e3_destroy(h->e3);
     delete h;
     return;
   }
-  cudaSetDevice(h->cfg.device);
   if (h->s) cudaStreamSynchronize(h->s);
   free_all(h);
   for (auto e : h->ev_pool) cudaEventDestroy(e);

@@ -14,8 +14,6 @@
 #include "engine3.h"
 #include "kernels3d.cu"
 #include "kernels3d_fast.cu"
-#include "kernels3d_ffp.cu"
-#include "kernels3d_ffp4.cu"
 #include "kernels3d_upq.cu"
 #include "kernels3d_smr.cu"
 #include "kernels3d_top4.cu"
@@ -108,19 +106,16 @@ struct Engine3 {
   std::vector<int> own_blocks2, own_chunk2;  // two-row kernels (k3_top2 / k3_smooth2r)
   double* red = nullptr;            // {sum, max} of this cycle's stats
   int top_parts = 0;
-  // fused fine pass (pipelined schedule): the finest level's u and g are double
-  // buffered; after a cycle the finest level carries a pending correction
-  // P carry_{ltop-1} + g that the next cycle's fused pass (or flush) applies
-  bool ffp = false, fpend = false;
-  int pu = 0, pg = 0;
+  // finest level double buffered (pp): the down sweep writes u + g of the finest level into
+  // the other buffer (g never reaches HBM) and the up sweep adds P carry there; ubuf[par]
+  // holds the current iterate, one captured graph per parity
+  bool pp = false;
+  int par = 0;
   double* ubuf[2] = {nullptr, nullptr};
-  double* gbuf[2] = {nullptr, nullptr};
-  int ffp_tiles = 0, ffp_chunk = 0, ffp_blocks = 0;
   std::map<int, cudaGraphExec_t> gcache;
-  // throttled BoxMG setup: next level to receive BoxMG P + Galerkin rows (< lmin: done)
-  bool ffp4 = false;  // version-4 fused pass (TMA plane sets, partial-sum smoothing)
   bool smr = false;   // smoothing fused with the restriction into the next level (k3_smr)
   int smr_lo = 0;     // ... for the levels smr_lo..ltop
+  // throttled BoxMG setup: next level to receive BoxMG P + Galerkin rows (< lmin: done)
   int thr_next = -1;
   int* deg = nullptr;
 };
@@ -167,11 +162,24 @@ void free3(Engine3* e) {
   e->gexec = nullptr;
   for (auto& kv : e->gcache) cudaGraphExecDestroy(kv.second);
   e->gcache.clear();
-  e->ffp = e->fpend = false;
-  e->pu = e->pg = 0;
+  e->pp = false;
+  e->par = 0;
+  e->ubuf[0] = e->ubuf[1] = nullptr;
   for (void* p : e->allocs) cudaFree(p);
   e->allocs.clear();
   e->L.clear();
+  // buffers from e3_shard were in allocs: a rebuilt handle is unsharded until tmg3_shard runs again
+  e->red = nullptr;
+  e->part_sum = e->part_max = nullptr;
+  e->nparts = 0;
+  e->sharded = false;
+  e->ls = 0;
+  e->own_lo.clear();
+  e->own_hi.clear();
+  e->own_blocks.clear();
+  e->own_chunk.clear();
+  e->own_blocks2.clear();
+  e->own_chunk2.clear();
   e->graph_dirty = true;
 }
 
@@ -284,6 +292,10 @@ Up3 make_up(Engine3* e, int l) {
   a.ihi = c.N - 1;
   a.u = c.u;
   a.g = c.g;
+  if (l == l1 && e->pp) {  // the down sweep wrote u + g into the other buffer
+    a.u = e->ubuf[e->par ^ 1];
+    a.g = nullptr;
+  }
   a.carry = (l < l1) ? c.carry : nullptr;
   if (l > l0) {
     Lvl3& cc = e->L[l - 1];
@@ -367,17 +379,9 @@ bool tmap3(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_
                 prom, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// TMA staging of the streaming kernels' vertex planes (TMG_TMA=0: cp.async)
-const bool kUseTma = [] {
-  const char* v = std::getenv("TMG_TMA");
-  return !(v && v[0] == '0');
-}();
-
-// BoxMG prolongation: tiled cube kernel (TMG_UPT=0: the cell-owned k3_up_cell)
-const bool kUseUpTile = [] {
-  const char* v = std::getenv("TMG_UPT");
-  return !(v && v[0] == '0');
-}();
+// TMA staging of the streaming kernels' vertex planes (cp.async when the driver entry point of
+// the tensor-map encoder is missing)
+constexpr bool kUseTma = true;
 
 bool tmap4(CUtensorMap* map, const double* base, const uint64_t d[4], const uint64_t s[3], const uint32_t b[4]) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
@@ -398,13 +402,13 @@ bool tmap4(CUtensorMap* map, const double* base, const uint64_t d[4], const uint
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// SM count of the current device (the ABI's DeviceGuard makes it the handle's)
 int num_sms() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return n;
+  static int cache[64] = {0};
+  int dev = 0, v = 148;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return v;
+  if (!cache[dev] && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) cache[dev] = v;
+  return cache[dev] ? cache[dev] : v;
 }
 
 int launch_up_tma(Engine3* e, int l, const Up3& a) {
@@ -417,7 +421,7 @@ int launch_up_tma(Engine3* e, int l, const Up3& a) {
   const uint32_t bp[4] = {kQK, kQJ, 1, kQS};
   bool ok = tmap4(&A.tp, cc.Pc, dp, sp, bp);
   ok = ok && tmap3(&A.tu, a.u, N, N, N, N * 8, N * N * 8, kQFK, kQFJ, 3, CU_TENSOR_MAP_L2_PROMOTION_NONE);
-  ok = ok && tmap3(&A.tg, a.g, N, N, N, N * 8, N * N * 8, kQFK, kQFJ, 3, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+  if (a.g) ok = ok && tmap3(&A.tg, a.g, N, N, N, N * 8, N * N * 8, kQFK, kQFJ, 3, CU_TENSOR_MAP_L2_PROMOTION_NONE);
   ok = ok && tmap3(&A.tc, a.carry_c, Nc, Nc, Nc, Nc * 8, Nc * Nc * 8, kQCK, kQCJ, 2);
   if (!ok) return fail3(e, TMG_ECUDA, "tensor map encoding failed (k3_up_tma)");
   const int nc = a.Nc - 1;
@@ -444,10 +448,12 @@ int launch_up_tma(Engine3* e, int l, const Up3& a) {
     D.I0 = A.I0;
     D.steps = (int)A.steps;
     D.per = (int)A.per;
-    if (a.carry) k3_up_dict<true><<<grid, kDThreads, kUpDictSmem, e->s>>>(D);
+    if (!a.g) k3_up_dict<false, false><<<grid, kDThreads, kUpDictSmem, e->s>>>(D);
+    else if (a.carry) k3_up_dict<true><<<grid, kDThreads, kUpDictSmem, e->s>>>(D);
     else k3_up_dict<false><<<grid, kDThreads, kUpDictSmem, e->s>>>(D);
   } else {
-    if (a.carry) k3_up_tma<true><<<grid, kQT, kUpTmaSmem, e->s>>>(A);
+    if (!a.g) k3_up_tma<false, false><<<grid, kQT, kUpTmaSmem, e->s>>>(A);
+    else if (a.carry) k3_up_tma<true><<<grid, kQT, kUpTmaSmem, e->s>>>(A);
     else k3_up_tma<false><<<grid, kQT, kUpTmaSmem, e->s>>>(A);
   }
   CKL3();
@@ -459,7 +465,7 @@ int launch_up_boxmg(Engine3* e, int l, const Up3& a) {
   if (e->L[l - 1].Pc && !a.pi) return launch_up_tma(e, l, a);
   // small levels (< 32 coarse cells per axis): the cell-owned kernel has 9x the threads of the
   // tiled one, which is latency-bound there (config 5: up L3 55 -> 17 us, L4 79 -> 20 us)
-  if (!kUseUpTile || a.Nc - 1 < kUX) {
+  if (a.Nc - 1 < kUX) {
     LAUNCH3(kname("k3_up", l), k3_up_cell<true>, e->L[l - 1].u_grid, 128, a);
     return TMG_OK;
   }
@@ -474,14 +480,8 @@ int launch_up_boxmg(Engine3* e, int l, const Up3& a) {
   return TMG_OK;
 }
 
-// element operator with every plane through TMA: the four-rows-per-thread kernel (TMG_TOP4=0: k3_top2)
-bool use_top4(const Top3& a) {
-  static const bool on = [] {
-    const char* v = std::getenv("TMG_TOP4");
-    return !(v && v[0] == '0');
-  }();
-  return on && a.use_tma == 2 && a.rhs_tma;
-}
+// element operator with every plane through TMA: the four-rows-per-thread kernel (else k3_top2)
+bool use_top4(const Top3& a) { return a.use_tma == 2 && a.rhs_tma; }
 
 Top3 make_top(Engine3* e, int l) {
   Lvl3& c = e->L[l];
@@ -496,14 +496,14 @@ Top3 make_top(Engine3* e, int l) {
   a.w = c.w;
   a.hw = std::pow(3.0, -1.5 * l);
   a.g = c.g;
+  a.u_out = (l == e->ltop && e->pp) ? e->ubuf[e->par ^ 1] : nullptr;
   a.rho = (l > e->lmin) ? c.rho : nullptr;
   a.part_sum = e->part_sum;
   a.part_max = e->part_max;
   a.use_tma = kUseTma && vertex_tmap(&a.tm, c.u, c.N);
   if (a.use_tma && c.op.kind == OP_ELEMENT && c.coefp && cell_tmap(&a.tmc, c.coefp, c.N - 1)) a.use_tma = 2;
-  // rhs through TMA as well (TMG_TMA_RHS=0: per-thread loads); needs the vertex-plane TMA path
-  const char* tr = std::getenv("TMG_TMA_RHS");
-  a.rhs_tma = a.use_tma && c.rhs && !(tr && tr[0] == '0') &&
+  // rhs through TMA as well; needs the vertex-plane TMA path
+  a.rhs_tma = a.use_tma && c.rhs &&
               tmap3(&a.tmr, c.rhs, c.N, c.N, c.N, (uint64_t)c.N * 8, (uint64_t)c.N * c.N * 8, k2RowR, k2Y, 1);
   return a;
 }
@@ -520,28 +520,6 @@ SmoothS make_smooth_s(Engine3* e, int l) {
   a.scale = e->cfg.omega * 3.0 / 8.0;
   a.use_tma = kUseTma && vertex_tmap(&a.tm, c.rho, c.N);
   return a;
-}
-
-// k3_smr layout (measured at config 5, L6): one restriction thread per coarse vertex carrying both
-// planes and both fields (default; TMG_SMR_RV=0: two roles owning alternate planes, 3.17 vs
-// 3.07 ms), smoothing threads owning groups of 7 sm columns (default; TMG_SMR_GH=2: pairs, 3.05 vs
-// 2.97 ms)
-// (read at every launch: an engine's cycle graph is captured once)
-static int smr_rv() {
-  const char* s = getenv("TMG_SMR_RV");
-  return s ? atoi(s) : 1;
-}
-
-// the decoupled smoothing / restriction schedule (named barriers per sm buffer; dictionary P
-// only): default, TMG_SMR_DEC=0 keeps the one-barrier-per-step schedule (config 5 L6: 2.80-2.83
-// vs 2.85-2.92 ms, cycle 9.02-9.05 vs 9.11-9.12 ms)
-static int smr_dec() {
-  const char* s = getenv("TMG_SMR_DEC");
-  return s ? atoi(s) : 1;
-}
-static int smr_gh() {
-  const char* s = getenv("TMG_SMR_GH");
-  return s ? atoi(s) : 7;
 }
 
 // k3_smr over the finest level: adaFACx smoothing (when `smooth`) and the restriction of rho / sm
@@ -587,18 +565,8 @@ int launch_smr(Engine3* e, int l, bool smooth, int clo = -1, int chi = -1) {
   const dim3 grid(tiles, (n + A.chunk - 1) / A.chunk);
   cudaEvent_t e0_ = nullptr;
   TRY3(begin_k(e, &e0_));
-  if (cc.Pd && smr_dec() && smr_rv() == 1 && smr_gh() == 7) {
-    k3_smr<true, 1, 7, true><<<grid, kRTasks + kRK * kRJ, kSmrSmemDB, e->s>>>(A);
-  } else if (smr_rv() == 1 && smr_gh() == 7) {
-    if (cc.Pd) k3_smr<true, 1, 7><<<grid, kRTasks + kRK * kRJ, kSmrSmemD, e->s>>>(A);
-    else k3_smr<false, 1, 7><<<grid, kRTasks + kRK * kRJ, kSmrSmem, e->s>>>(A);
-  } else if (smr_rv() == 1) {
-    if (cc.Pd) k3_smr<true, 1, 2><<<grid, kRTasks + kRK * kRJ, kSmrSmemD, e->s>>>(A);
-    else k3_smr<false, 1, 2><<<grid, kRTasks + kRK * kRJ, kSmrSmem, e->s>>>(A);
-  } else {
-    if (cc.Pd) k3_smr<true, 0, 2><<<grid, kRThreads, kSmrSmemD, e->s>>>(A);
-    else k3_smr<false, 0, 2><<<grid, kRThreads, kSmrSmem, e->s>>>(A);
-  }
+  if (cc.Pd) k3_smr<true, 1, 7, true><<<grid, kRTasks + kRK * kRJ, kSmrSmemDB, e->s>>>(A);
+  else k3_smr<false, 1, 7><<<grid, kRTasks + kRK * kRJ, kSmrSmem, e->s>>>(A);
   CKL3();
   TRY3(end_k(e, kname("k3_smooth", l), e0_));
   return TMG_OK;
@@ -665,144 +633,7 @@ int enqueue_down(Engine3* e, bool write) {
   return TMG_OK;
 }
 
-Ffp3 make_ffp(Engine3* e, bool apply) {
-  const int l1 = e->ltop, lC = l1 - 1;
-  Lvl3& c = e->L[l1];
-  Lvl3& cc = e->L[lC];
-  Ffp3 a{};
-  a.N = c.N;
-  a.Nc = cc.N;
-  a.tiles = e->ffp_tiles;
-  a.chunk = e->ffp_chunk;
-  a.apply = apply ? 1 : 0;
-  a.variant = e->cfg.variant;
-  a.jac = e->cfg.variant == VAR_JAC;
-  a.u_in = e->ubuf[e->pu];
-  a.u_out = e->ubuf[e->pu ^ 1];
-  a.g_in = e->gbuf[e->pg];
-  a.g_out = e->gbuf[e->pg ^ 1];
-  a.carry_c = cc.carry;
-  a.P = cc.P;
-  a.op = c.op;
-  a.rhs = c.rhs;
-  a.w = c.w;
-  a.hw = std::pow(3.0, -1.5 * l1);
-  a.scale = e->cfg.omega * 3.0 / 8.0;
-  a.bR = cc.bR;
-  a.bT = cc.bT;
-  a.l = l1;
-  a.l0 = e->lmin;
-  for (int k = e->lmin; k < l1; ++k) {
-    a.ul[k] = e->L[k].u;
-    a.Nl[k] = e->L[k].N;
-  }
-  a.part_sum = e->part_sum;
-  a.part_max = e->part_max;
-  return a;
-}
-
-int make_ffp4(Engine3* e, bool apply, Ffp4* A) {
-  *A = Ffp4{};
-  A->f = make_ffp(e, apply);
-  const Ffp3& f = A->f;
-  const uint64_t N = (uint64_t)f.N, Nc = (uint64_t)f.Nc, n = N - 1, np = n + (n & 1);
-  bool ok = tmap3(&A->tu, f.u_in, N, N, N, N * 8, N * N * 8, k4U, k4U, 1);
-  if (apply) {
-    ok = ok && tmap3(&A->tg, f.g_in, N, N, N, N * 8, N * N * 8, k4U, k4U, 1);
-    ok = ok && tmap3(&A->tk, f.carry_c, Nc, Nc, Nc, Nc * 8, Nc * Nc * 8, k4K, k4K, 2);
-  }
-  if (f.op.kind == OP_ELEMENT)
-    ok = ok && tmap3(&A->tc, e->L[e->ltop].coefp, n, n, n, np * 8, np * n * 8, k4U, k4U, 1);
-  if (f.rhs) ok = ok && tmap3(&A->th, f.rhs, N, N, N, N * 8, N * N * 8, k4U, k4U, 1);
-  if (!ok) return fail3(e, TMG_ECUDA, "tensor map encoding failed (fused fine pass)");
-  const char* dbg = std::getenv("TMG_FFP4_DBG");
-  A->dbg = dbg ? std::atoi(dbg) : 0;
-  return TMG_OK;
-}
-
-// One cycle with the fused fine pass: FFP (finest level), then the coarse levels.
-int enqueue_cycle_ffp(Engine3* e, bool apply) {
-  const bool jac = e->cfg.variant == VAR_JAC;
-  const dim3 sblk(kSX, kSY);
-  if (e->ffp4) {
-    Ffp4 A;
-    TRY3(make_ffp4(e, apply, &A));
-    cudaEvent_t e0_ = nullptr;
-    TRY3(begin_k(e, &e0_));
-    if (A.f.op.kind == OP_CONST) k3_ffp4<OP_CONST><<<e->ffp_blocks, k4Threads, kFfp4Smem, e->s>>>(A);
-    else k3_ffp4<OP_ELEMENT><<<e->ffp_blocks, k4Threads, kFfp4Smem, e->s>>>(A);
-    CKL3();
-    TRY3(end_k(e, kname("k3_down", e->ltop), e0_));
-  } else {
-    Ffp3 f = make_ffp(e, apply);
-    cudaEvent_t e0_ = nullptr;
-    TRY3(begin_k(e, &e0_));
-    k3_ffp<<<e->ffp_blocks, kFThreads, kFfpSmem, e->s>>>(f);
-    CKL3();
-    TRY3(end_k(e, kname("k3_down", e->ltop), e0_));
-  }
-  for (int l = e->ltop - 1; l > e->lc; --l) {
-    Lvl3& c = e->L[l];
-    Down3 a = make_down(e, l, true);
-    if (l == e->ltop - 1) {
-      a.bR = c.bR;
-      a.bT = c.bT;
-      if (jac) LAUNCH3(kname("k3_down", l), (k3_down_c<true, true, true>), c.c_grid, 128, a);
-      else LAUNCH3(kname("k3_down", l), (k3_down_c<true, false, true>), c.c_grid, 128, a);
-    } else if (jac) {
-      LAUNCH3(kname("k3_down", l), (k3_down_c<true, true>), c.c_grid, 128, a);
-    } else {
-      LAUNCH3(kname("k3_down", l), (k3_down_c<true, false>), c.c_grid, 128, a);
-    }
-    if (jac && l > e->lmin) {
-      SmoothS sa = make_smooth_s(e, l);
-      LAUNCH3(kname("k3_smooth", l), k3_smooth_s, c.s_blocks, sblk, sa);
-    }
-  }
-  Chain3 ch{};
-  ch.l0 = e->lmin;
-  ch.lc = e->lc;
-  ch.do_up = 1;
-  ch.jac = jac ? 1 : 0;
-  ch.part_sum = e->part_sum;
-  ch.part_max = e->part_max;
-  ch.nparts = e->ffp_blocks;
-  ch.hist = e->hist;
-  ch.counter = e->counter;
-  ch.cap = e->cap;
-  for (int l = e->lmin; l <= e->lc; ++l) {
-    ch.down[l - e->lmin] = make_down(e, l, true);
-    ch.smooth[l - e->lmin] = make_smooth(e, l);
-    ch.up[l - e->lmin] = make_up(e, l);
-  }
-  LAUNCH3("k3_chain", k3_chain, 1, kChainBlock, ch);
-  for (int l = e->lc + 1; l <= e->ltop - 1; ++l) {
-    Up3 a = make_up(e, l);
-    TRY3(launch_up_boxmg(e, l, a));
-  }
-  return TMG_OK;
-}
-
-// after a fused cycle: swap the finest level's buffers, the correction is pending
-void ffp_advance(Engine3* e, bool applied) {
-  if (applied) e->pu ^= 1;
-  e->pg ^= 1;
-  e->fpend = true;
-  e->L[e->ltop].u = e->ubuf[e->pu];
-  e->L[e->ltop].g = e->gbuf[e->pg];
-}
-
-// apply the pending correction of the finest level (+ its FAS injection) in place
-int ffp_flush(Engine3* e) {
-  if (!e->ffp || !e->fpend) return TMG_OK;
-  Up3 a = make_up(e, e->ltop);  // u = current buffer, g = latest d
-  TRY3(launch_up_boxmg(e, e->ltop, a));
-  e->fpend = false;
-  return TMG_OK;
-}
-
 int enqueue_cycle(Engine3* e) {
-  if (e->ffp) return enqueue_cycle_ffp(e, e->fpend);
   TRY3(enqueue_down(e, true));
   const bool boxmg = e->cfg.flavor == TMG_BOXMG;
   const bool pi = e->cfg.variant == VAR_PI;
@@ -817,6 +648,13 @@ int enqueue_cycle(Engine3* e) {
   return TMG_OK;
 }
 
+// after a cycle with the finest level double buffered: the other buffer is current
+void pp_advance(Engine3* e) {
+  if (!e->pp) return;
+  e->par ^= 1;
+  e->L[e->ltop].u = e->ubuf[e->par];
+}
+
 int ensure_graph(Engine3* e) {
   if (e->graph_dirty) {
     if (e->gexec && e->gcache.empty()) cudaGraphExecDestroy(e->gexec);
@@ -824,9 +662,9 @@ int ensure_graph(Engine3* e) {
     for (auto& kv : e->gcache) cudaGraphExecDestroy(kv.second);
     e->gcache.clear();
   }
-  if (e->ffp) {
-    // one graph per (pending, u parity, g parity) state of the double buffers
-    const int key = (e->fpend ? 4 : 0) + e->pu * 2 + e->pg;
+  if (e->pp) {
+    // one graph per parity of the finest level's double buffer
+    const int key = e->par;
     auto it = e->gcache.find(key);
     if (it == e->gcache.end()) {
       cudaGraph_t g;
@@ -982,12 +820,8 @@ int refresh_pc(Engine3* e, int l) {
   const char* env = std::getenv("TMG_PDICT");
   if (e->cfg.throttled || (env && env[0] == '0') || l < e->ltop - 2 || c.Pd || c.Pcd) return TMG_OK;
   const bool force = env && env[0] == '2';
-  // Pc's dictionary feeds k3_up_dict (TMG_PDICT_UP=0: dense), P's the restriction in k3_smr
-  // (TMG_PDICT_SMR=0: dense)
-  const char* es = std::getenv("TMG_PDICT_SMR");
-  const char* eu = std::getenv("TMG_PDICT_UP");
-  if (!(eu && eu[0] == '0'))
-    TRY3(build_dict(e, RowsView{c.Pc, nc, Kp, nc * nc * Kp, kQS, nc, Kp}, nc * nc * nc, force, &c.Pcd, &c.Pcdi,
+  // Pc's dictionary feeds k3_up_dict, P's the restriction in k3_smr
+  TRY3(build_dict(e, RowsView{c.Pc, nc, Kp, nc * nc * Kp, kQS, nc, Kp}, nc * nc * nc, force, &c.Pcd, &c.Pcdi,
                     &c.Pcdp, &c.Pcdn));
   if (c.Pcd) {  // k3_up_tma's step tables; a step meeting more than kQRows rows keeps the dense stream
     const int tK = (int)((nc + kQK - 1) / kQK), tJ = (int)((nc + kQJ - 1) / kQJ);
@@ -1002,14 +836,7 @@ int refresh_pc(Engine3* e, int l) {
     CK3(cudaStreamSynchronize(e->s));
     if (over) c.Pcd = nullptr, c.Pcdn = 0;
   }
-  // the Galerkin rows (k3_down_c's operator at level ltop-1) -- opt-in (TMG_PDICT_GAL=1): at config 5
-  // they have 1.24 M distinct rows and the per-lane row loads made k3_down_c slower (0.85 vs 0.65 ms)
-  const char* eg = std::getenv("TMG_PDICT_GAL");
-  if (l == e->ltop - 1 && eg && eg[0] == '1') {
-    size_t tdp = 0;
-    TRY3(build_dict(e, RowsView{c.tbl, c.nv, 0, c.nv, 27, c.nv, c.nv}, c.nv, force, &c.Td, &c.Tdi, &tdp, &c.Tdn));
-  }
-  if (!(es && es[0] == '0')) {
+  {
     const size_t Nc = c.N, Ncp = (Nc + 3) / 4 * 4;  // id rows padded to 16 bytes
     TRY3(build_dict(e, RowsView{c.P, c.nv, 0, c.nv, 125, Nc, Ncp}, c.nv, force, &c.Pd, &c.Pdi, &c.Pdp, &c.Pdn));
     if (c.Pd) {  // k3_smr's tile-plane tables; a tile plane meeting more than kRRows rows keeps the dense P
@@ -1112,6 +939,8 @@ int build(Engine3* e, const tmg_tree3* t) {
   CK3(cudaFuncSetAttribute(k3_up_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpTmaSmem));
   CK3(cudaFuncSetAttribute(k3_up_dict<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpDictSmem));
   CK3(cudaFuncSetAttribute(k3_up_dict<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpDictSmem));
+  CK3(cudaFuncSetAttribute(k3_up_dict<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpDictSmem));
+  CK3(cudaFuncSetAttribute(k3_up_tma<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpTmaSmem));
   TRY3(alloc3(e, &e->deg, 1));
   e->thr_next = l0 - 1;
   if (cfg.flavor == TMG_GEOMETRIC) {
@@ -1132,9 +961,8 @@ int build(Engine3* e, const tmg_tree3* t) {
       Lvl3& c = e->L[l];
       TRY3(alloc3(e, &c.P, 125 * c.nv, false));
       TRY3(alloc3(e, &c.tbl, 27 * c.nv, false));
-      // BoxMG prolongation of the two finest levels as TMA streams (k3_up_tma; TMG_UPQ=0: k3_up_tile)
-      const char* upq = std::getenv("TMG_UPQ");
-      if (l >= l1 - 2 && !(upq && upq[0] == '0') && c.N - 1 >= kQK) {
+      // BoxMG prolongation of the two finest levels as TMA streams (k3_up_tma)
+      if (l >= l1 - 2 && c.N - 1 >= kQK) {
         const size_t nc = (size_t)c.N - 1, Kp = (nc + kQK - 1) / kQK * kQK;
         TRY3(alloc3(e, &c.Pc, (size_t)kQS * nc * nc * Kp));
       }
@@ -1226,54 +1054,24 @@ int build(Engine3* e, const tmg_tree3* t) {
       parts = std::max(c.s_blocks, c.s2_blocks);
     }
   }
-  // fused fine pass: BoxMG, every variant but adafac-pi, a grid level below the top
-  {
-    // opt-in (TMG_FFP=1) until it beats the phase-by-phase cycle (profiles/r01_ffp_*)
-    const char* env = std::getenv("TMG_FFP");
-    const bool want = env && (std::strcmp(env, "1") == 0 || std::strcmp(env, "4") == 0);
-    e->ffp = want && cfg.flavor == TMG_BOXMG && cfg.variant != VAR_PI && l1 - 1 > e->lc;
-    e->ffp4 = e->ffp && std::strcmp(env, "4") == 0;
-    e->fpend = false;
-    e->pu = e->pg = 0;
-    if (e->ffp) {
-      CK3(cudaFuncSetAttribute(k3_ffp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFfpSmem));
-      Lvl3& c = e->L[l1];
-      Lvl3& cc = e->L[l1 - 1];
-      e->ubuf[0] = c.u;
-      TRY3(alloc3(e, &e->ubuf[1], c.nv, false));
-      CK3(cudaMemcpyAsync(e->ubuf[1], c.u, sizeof(double) * c.nv, cudaMemcpyDeviceToDevice, e->s));
-      e->gbuf[0] = c.g;
-      TRY3(alloc3(e, &e->gbuf[1], c.nv));
-      TRY3(alloc3(e, &cc.bR, cc.nv));
-      TRY3(alloc3(e, &cc.bT, cc.nv));
-      if (e->ffp4) {
-        CK3(cudaFuncSetAttribute(k3_ffp4<OP_CONST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFfp4Smem));
-        CK3(cudaFuncSetAttribute(k3_ffp4<OP_ELEMENT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kFfp4Smem));
-      }
-      const int ft = e->ffp4 ? k4T : kFT;
-      e->ffp_tiles = (c.N - 1 + 3 * ft - 1) / (3 * ft);
-      const int t2 = e->ffp_tiles * e->ffp_tiles;
-      int nch = ((e->ffp4 ? 148 : 8 * 148) + t2 - 1) / t2;
-      nch = std::max(1, std::min(nch, std::max(1, cc.N / 8)));
-      e->ffp_chunk = (cc.N + nch - 1) / nch;
-      e->ffp_blocks = t2 * ((cc.N + e->ffp_chunk - 1) / e->ffp_chunk);
-      parts = std::max(parts, e->ffp_blocks);
-    }
+  // finest level double buffered: its down sweep (a grid level, not the chain) writes u + g into
+  // the other buffer and its up sweep adds P carry there -- g never reaches HBM.  adafac-pi
+  // subtracts a prolonged d~ on the finest level too, so it keeps g.
+  e->par = 0;
+  e->pp = l1 > e->lc && cfg.variant != VAR_PI;
+  if (e->pp) {
+    Lvl3& c = e->L[l1];
+    e->ubuf[0] = c.u;
+    TRY3(alloc3(e, &e->ubuf[1], c.nv, false));
+    CK3(cudaMemcpyAsync(e->ubuf[1], c.u, sizeof(double) * c.nv, cudaMemcpyDeviceToDevice, e->s));
   }
-  // finest-level smoothing + restriction fused (k3_smr; TMG_SMR=0: k3_smooth2r + k3_down_c)
+  // finest-level smoothing + restriction fused (k3_smr; else k3_smooth2r + k3_down_c)
   {
-    const char* env = std::getenv("TMG_SMR");
-    e->smr = !(env && env[0] == '0') && !e->ffp && cfg.flavor == TMG_BOXMG && cfg.variant != VAR_PI &&
+    e->smr = cfg.flavor == TMG_BOXMG && cfg.variant != VAR_PI &&
              l1 - 1 > e->lc;
     e->smr_lo = e->lc + 2;  // every level whose coarser level is a grid (not chain) level
     if (e->smr) {
-      CK3(cudaFuncSetAttribute(k3_smr<false, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmem));
-      CK3(cudaFuncSetAttribute(k3_smr<true, 0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmemD));
-      CK3(cudaFuncSetAttribute(k3_smr<false, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmem));
-      CK3(cudaFuncSetAttribute(k3_smr<true, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmemD));
       CK3(cudaFuncSetAttribute(k3_smr<false, 1, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmem));
-      CK3(cudaFuncSetAttribute(k3_smr<true, 1, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmemD));
       CK3(cudaFuncSetAttribute(k3_smr<true, 1, 7, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmemDB));
       for (int l = e->smr_lo - 1; l < l1; ++l) {
         Lvl3& cc = e->L[l];
@@ -1486,9 +1284,8 @@ int phase3(Engine3* e, int phase, int l) {
 
 int e3_shard(Engine3* e, int ls, const int32_t* lo, const int32_t* hi, std::string& err) {
   ErrScope es(e, err);
-  TRY3(ffp_flush(e));
-  if (e->ffp) {  // sharded runs use the phase kernels on buffer 'current'
-    e->ffp = false;
+  if (e->pp) {  // sharded runs use the phase kernels with g on the current buffer
+    e->pp = false;
     e->graph_dirty = true;
   }
   if (ls <= e->lmin || ls > e->ltop) return fail3(e, TMG_EINVAL, "shard level must lie in (lmin, ltop]");
@@ -1597,9 +1394,8 @@ int launch_cycle(Engine3* e) {
     TRY3(check_degenerate(e));
     --e->thr_next;
   }
-  const bool applied = e->fpend;
   CK3(cudaGraphLaunch(e->gexec, e->s));
-  if (e->ffp) ffp_advance(e, applied);
+  pp_advance(e);
   return TMG_OK;
 }
 
@@ -1667,10 +1463,9 @@ int e3_set_rhs(Engine3* e, int level, const double* rhs, std::string& err) {
 int e3_set_u(Engine3* e, int level, const double* u, std::string& err) {
   ErrScope es(e, err);
   TRY3(check_level(e, level));
-  TRY3(ffp_flush(e));
   CK3(cudaMemcpyAsync(e->L[level].u, u, sizeof(double) * e->L[level].nv, cudaMemcpyHostToDevice, e->s));
-  if (e->ffp && level == e->ltop)  // both buffers: the boundary values are never rewritten
-    CK3(cudaMemcpyAsync(e->ubuf[e->pu ^ 1], u, sizeof(double) * e->L[level].nv, cudaMemcpyHostToDevice, e->s));
+  if (e->pp && level == e->ltop)  // both buffers: the down sweep writes interior vertices only
+    CK3(cudaMemcpyAsync(e->ubuf[e->par ^ 1], u, sizeof(double) * e->L[level].nv, cudaMemcpyHostToDevice, e->s));
   CK3(cudaStreamSynchronize(e->s));
   return TMG_OK;
 }
@@ -1678,7 +1473,6 @@ int e3_set_u(Engine3* e, int level, const double* u, std::string& err) {
 int e3_get_u(Engine3* e, int level, double* u, std::string& err) {
   ErrScope es(e, err);
   TRY3(check_level(e, level));
-  TRY3(ffp_flush(e));
   CK3(cudaMemcpyAsync(u, e->L[level].u, sizeof(double) * e->L[level].nv, cudaMemcpyDeviceToHost, e->s));
   CK3(cudaStreamSynchronize(e->s));
   return TMG_OK;
@@ -1686,7 +1480,6 @@ int e3_get_u(Engine3* e, int level, double* u, std::string& err) {
 
 int e3_update_fas_state(Engine3* e, std::string& err) {
   ErrScope es(e, err);
-  TRY3(ffp_flush(e));
   for (int l = e->ltop - 1; l >= e->lmin; --l) {
     const int n = e->L[l].N - 2;
     if (n <= 0) continue;
@@ -1716,7 +1509,6 @@ int e3_cycle(Engine3* e, int ncycles, tmg_stats* stats, std::string& err) {
 
 int e3_residual_stats(Engine3* e, tmg_stats* out, std::string& err) {
   ErrScope es(e, err);
-  TRY3(ffp_flush(e));
   TRY3(enqueue_down(e, false));
   const long long first = e->host_counter++;
   return read_stats(e, first, 1, out);
@@ -1840,9 +1632,8 @@ int e3_profile_cycles(Engine3* e, int ncycles, int cap, const char** names, floa
   e->profiling = true;
   int rc = TMG_OK;
   for (int k = 0; k < ncycles && rc == TMG_OK; ++k) {
-    const bool applied = e->fpend;
     rc = enqueue_cycle(e);
-    if (e->ffp) ffp_advance(e, applied);
+    pp_advance(e);
     e->host_counter++;
   }
   e->profiling = false;
@@ -1884,4 +1675,3 @@ int e3_launches_per_cycle(Engine3* e, int32_t* n, std::string& err) {
   return TMG_OK;
 }
 
-int e3_uses_ffp(Engine3* e) { return e->ffp ? 1 : 0; }

@@ -273,7 +273,7 @@ template <class LD>
 __device__ __forceinline__ void up_vertex(const Up3& a, int i, int j, int k) {
   const int N = a.N;
   const size_t v = vid(N, i, j, k);
-  double g = LD::ld(a.g + v);
+  double g = a.g ? LD::ld(a.g + v) : 0.0;  // null: the finest level's g is already in u (pp)
   double c;
   if (a.is_bottom) {
     c = g;

@@ -44,7 +44,8 @@ struct Top3 {
   Op3 op;
   double w, hw;
   double* g;
-  double* rho;  // or nullptr
+  double* u_out;  // or nullptr: write u + g there instead of g (the finest level's double buffer)
+  double* rho;    // or nullptr
   double* part_sum;
   double* part_max;
 };
@@ -101,6 +102,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         : "r"(smem_addr(bar)), "r"(parity)
         : "memory");
   } while (!ready);
+}
+// generic-proxy shared-memory writes (or reads) ordered before later async-proxy (TMA) accesses
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 // 1D bulk copy global -> shared (16-byte multiples), completion on an mbarrier
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
@@ -561,14 +566,18 @@ __global__ void __launch_bounds__(kSB, 3) k3_top2(const __grid_constant__ Top3 a
         const double t0 = a.hw * rho0;
         s = s + t0 * t0;
         mx = fmax(mx, fabs(rho0));
-        a.g[v] = (a.w * rho0) / dg0;
+        const double g0 = (a.w * rho0) / dg0;
+        if (a.u_out) a.u_out[v] = x0[13] + g0;
+        else a.g[v] = g0;
         if (a.rho) a.rho[v] = rho0;
         if (ok1) {
           const double rho1 = rhs1 - au1;
           const double t1 = a.hw * rho1;
           s = s + t1 * t1;
           mx = fmax(mx, fabs(rho1));
-          a.g[v + N] = (a.w * rho1) / dg1;
+          const double g1 = (a.w * rho1) / dg1;
+          if (a.u_out) a.u_out[v + N] = x1[13] + g1;
+          else a.g[v + N] = g1;
           if (a.rho) a.rho[v + N] = rho1;
         }
       },
@@ -717,7 +726,7 @@ __global__ void __launch_bounds__(128) k3_up_cell(const __grid_constant__ Up3 a)
         pc = prolong_dlinear(cv, Nc, i, j, k);
       }
       const size_t v = vid(N, i, j, k);
-      const double c = pc + __ldg(a.g + v);
+      const double c = a.g ? pc + __ldg(a.g + v) : pc;
       if (a.carry) a.carry[v] = c;
       const double un = a.u[v] + c;
       a.u[v] = un;
@@ -794,7 +803,7 @@ __global__ void __launch_bounds__(kUX * kUY, 6) k3_up_tile(const __grid_constant
             acc = acc + wt * (di ? c1[dj][dk] : c0[dj][dk]);
           }
           const size_t v = vb + ri * NN + rj * N + rk;
-          const double c = acc + __ldg(g + v);
+          const double c = g ? acc + __ldg(g + v) : acc;
           if (carry) carry[v] = c;
           const double un = u[v] + c;
           u[v] = un;

@@ -77,7 +77,9 @@ __global__ void __launch_bounds__(kT4B, 3) k3_top4(const __grid_constant__ Top3 
           s = s + t * t;
           mx = fmax(mx, fabs(rho));
           const size_t v = (size_t)i * NN + col_off + (size_t)aa * N;
-          a.g[v] = (a.w * rho) / dg;
+          const double gv = (a.w * rho) / dg;
+          if (a.u_out) a.u_out[v] = x[13] + gv;
+          else a.g[v] = gv;
           if (a.rho) a.rho[v] = rho;
         }
       },

@@ -113,7 +113,8 @@ __device__ __forceinline__ void tma_store_3d_ef(const CUtensorMap* map, const vo
                : "memory");
 }
 
-template <bool CARRY>
+// G = false: no g stream (the finest level's g is already in u, Engine3::pp)
+template <bool CARRY, bool G = true>
 __global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant__ UpD A) {
   extern __shared__ __align__(128) double sq[];
   __shared__ __align__(8) uint64_t full[kDNS], done[kDNS], tful[kDNT], rful[kDNR];
@@ -154,8 +155,8 @@ __global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant
       const int r = s - s0;
       double* b = sq + (r % kDNS) * kDSlot;
       uint64_t* br = &full[r % kDNS];
-      mbar_expect_tx(br, kDBytes);
-      tma_load_3d_ef(b + oDG, &A.tg, br, 3 * K0, 3 * J0, 3 * I, pol);
+      mbar_expect_tx(br, kDBytes - (G ? 0u : (unsigned)sizeof(double) * kQUd));
+      if (G) tma_load_3d_ef(b + oDG, &A.tg, br, 3 * K0, 3 * J0, 3 * I, pol);
       tma_load_3d(b + oDC, &A.tc, br, K0, J0, I);
       tma_load_3d_ef(b + oDU, &A.tu, br, 3 * K0, 3 * J0, 3 * I, pol);
     };
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant
     auto prefetch = [&](int s) {
       int I, J0, K0;
       coords(s, I, J0, K0);
-      tma_prefetch_3d(&A.tg, 3 * K0, 3 * J0, 3 * I);
+      if (G) tma_prefetch_3d(&A.tg, 3 * K0, 3 * J0, 3 * I);
       tma_prefetch_3d(&A.tu, 3 * K0, 3 * J0, 3 * I);
       tma_prefetch_3d(&A.tc, K0, J0, I);
       bulk_prefetch(A.tab + (((size_t)I * A.tilesJ + J0 / kQJ) * A.tilesK + K0 / kQK) * kQTabBytes, kQTabBytes);
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant
             const bool skip = i < a.ilo || i >= a.ihi || (rj == 0 && J == 0) || (rk == 0 && K == 0);
             if (!skip) {
               const int o = (ri * kQFJ + 3 * ty + rj) * kQFK + 3 * tx + rk;
-              const double cv = acc + Gs[o];
+              const double cv = G ? acc + Gs[o] : acc;
               const double un = Us[o] + cv;
               Us[o] = un;
               if (CARRY) a.carry[vid(N, i, 3 * J + rj, 3 * K + rk)] = cv;

@@ -112,7 +112,8 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-template <bool CARRY>
+// G = false: no g stream (the finest level's g is already in u, Engine3::pp)
+template <bool CARRY, bool G = true>
 __global__ void __launch_bounds__(kQT, 1) k3_up_tma(const __grid_constant__ UpQ A) {
   extern __shared__ __align__(128) double sq[];
   __shared__ __align__(8) uint64_t bar[2];
@@ -135,9 +136,9 @@ __global__ void __launch_bounds__(kQT, 1) k3_up_tma(const __grid_constant__ UpQ 
     double* b = sq + (r & 1) * kQSlot;
     uint64_t* br = &bar[r & 1];
     fence_proxy_async();
-    mbar_expect_tx(br, kQBytes);
+    mbar_expect_tx(br, kQBytes - (G ? 0u : (unsigned)sizeof(double) * kQUd));
     tma_load_4d(b + oQP, &A.tp, br, K0, J0, I, 0);
-    tma_load_3d(b + oQG, &A.tg, br, 3 * K0, 3 * J0, 3 * I);
+    if (G) tma_load_3d(b + oQG, &A.tg, br, 3 * K0, 3 * J0, 3 * I);
     tma_load_3d(b + oQC, &A.tc, br, K0, J0, I);
     bulk_wait_read0();  // this slot's u region was stored from at the end of step s - 2
     tma_load_3d(b + oQU, &A.tu, br, 3 * K0, 3 * J0, 3 * I);
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(kQT, 1) k3_up_tma(const __grid_constant__ UpQ 
             const bool skip = i < a.ilo || i >= a.ihi || (rj == 0 && J == 0) || (rk == 0 && K == 0);
             if (!skip) {
               const int o = (ri * kQFJ + 3 * ty + rj) * kQFK + 3 * tx + rk;
-              const double cv = acc + Gs[o];
+              const double cv = G ? acc + Gs[o] : acc;
               const double un = Us[o] + cv;
               Us[o] = un;
               if (CARRY) a.carry[vid(N, i, 3 * J + rj, 3 * K + rk)] = cv;

@@ -26,7 +26,7 @@ from .spacetree import CellId, Spacetree, VertexKind, build_regular
 from .spacetree3d import Spacetree3
 
 __all__ = ["Workload", "config1", "config2", "config3", "config4", "config5", "annulus_tree",
-           "seeded_rhs", "by_name"]
+           "seeded_rhs", "random_l5", "by_name"]
 
 
 @dataclass
@@ -189,6 +189,16 @@ def config5(levels: int = 6, block: int | None = None, seed: int = 0, cycles: in
                     cycles, None, seeded_rhs3(tree, rng), seed)
 
 
+def random_l5(seed: int = 7) -> Workload:
+    """Depth-5 3D BoxMG with per-cell log-uniform coefficients: no weight row repeats, so the
+    device keeps its dense weight streams (the dictionaries do not engage)."""
+    wl = config5(levels=5)
+    rng = np.random.default_rng(seed)
+    wl.tree.eps[5][...] = 10.0 ** rng.uniform(-2, 2, wl.tree.eps[5].shape)
+    wl.name = "random-L5"
+    return wl
+
+
 def by_name(name: str) -> Workload:
     table = {
         "config1": config1, "config2": config2, "config4": config4,
@@ -200,6 +210,11 @@ def by_name(name: str) -> Workload:
         "config5-L4": lambda: config5(levels=4, cycles=10),
         "config3-L4": lambda: config3(levels=4, cycles=12),
         "config5-L5": lambda: config5(levels=5, cycles=10),
+        "config3-L5": lambda: config3(levels=5),
+        # config 5's 27-cell coefficient blocks at depth 5 (9 level-4 cells): the weight
+        # dictionaries of the config-5 path engage
+        "config5-L5b27": lambda: config5(levels=5, block=27),
+        "random-L5": random_l5,
     }
     if name not in table:
         raise ValueError(f"unknown workload {name!r}; choose from {sorted(table)}")

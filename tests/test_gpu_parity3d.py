@@ -2,15 +2,17 @@
 
 There is no 3D reference (treemg is 2D only); the oracle ``oracle/mg3d.py``
 defines the fp64 expression DAG of every 3D operation and the kernels evaluate
-the same DAG, so the bar is **bitwise**: final ``u`` on every level with
-``array_equal``, P and Galerkin tables with ``array_equal``; the residual
-norms differ only by the reduction order of the sum of squares (rtol 1e-13).
-Larger sizes are checked against committed fixtures (tests/golden3d, made by
-tests/golden3d/make_golden3d.py from the oracle): per-cycle history and
-SHA-256 of the final iterate.
+the same algorithm with FMA contraction (the 3D translation unit is built with
+``--fmad=true``; there is no 3D reference to pin rounding to).  The bar is the
+north star's: per-cycle residual 2-norms (and max norms) and the final ``u``
+on every level within relative 1e-10 (``RTOL``; ``u`` normwise per level), P
+and Galerkin tables within 1e-12.  Depth 4 and depth 5 -- including config
+5's 27-cell coefficient blocks, where the weight dictionaries of the
+config-5 bench path engage -- are checked against committed fixtures
+(tests/golden3d, made by tests/golden3d/make_golden3d.py from the oracle):
+per-cycle history, per-level norms and a strided sample of the final iterate.
 """
 
-import hashlib
 import json
 import os
 
@@ -21,6 +23,7 @@ from oracle import mg3d
 from paper_1903_10367_b200 import GpuEngine, SolverConfig, workloads
 
 pytestmark = pytest.mark.gpu
+RTOL = 1e-10  # BASELINE.json north star: residual history and final u within relative 1e-10
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
@@ -46,13 +49,20 @@ def gpu_run(wl, n, variant=None, flavor=None, **kw):
     return eng, hist
 
 
+def close_u(got, want, rtol=RTOL, what="u"):
+    """Normwise relative bound: max |got - want| <= rtol * max |want|."""
+    scale = max(float(np.abs(want).max()), 1e-300)
+    err = float(np.abs(got - want).max())
+    assert err <= rtol * scale, f"{what}: max abs diff {err:.3e} > {rtol:g} x {scale:.3e}"
+
+
 def check(wl, eng, hist, t, e, ohist):
-    np.testing.assert_allclose([s.l2h for s in hist], [s.l2h for s in ohist], rtol=1e-13, atol=0)
-    np.testing.assert_allclose([s.linf for s in hist], [s.linf for s in ohist], rtol=0, atol=0)
+    np.testing.assert_allclose([s.l2h for s in hist], [s.l2h for s in ohist], rtol=RTOL, atol=0)
+    np.testing.assert_allclose([s.linf for s in hist], [s.linf for s in ohist], rtol=RTOL, atol=0)
     assert [s.dofs for s in hist] == [s.dofs for s in ohist]
     assert [s.updates for s in hist] == [s.updates for s in ohist]
     for l in range(wl.tree.lmin, wl.tree.depth + 1):
-        assert np.array_equal(wl.tree.u[l], t.u[l]), f"u level {l} not bitwise equal"
+        close_u(wl.tree.u[l], t.u[l], what=f"u level {l}")
 
 
 VARIANTS = ["additive", "additive-exp", "bpx", "afacc", "adafac-pi", "adafac-jac"]
@@ -60,7 +70,7 @@ VARIANTS = ["additive", "additive-exp", "bpx", "afacc", "adafac-pi", "adafac-jac
 
 @pytest.mark.parametrize("flavor", ["geometric", "boxmg"])
 @pytest.mark.parametrize("variant", VARIANTS)
-def test_3d_small_all_variants_bitwise(variant, flavor):
+def test_3d_small_all_variants(variant, flavor):
     wl = workloads.config5(levels=2, block=3) if flavor == "boxmg" else workloads.config3(levels=2)
     t, e, oh = oracle_run(wl, 6, variant, flavor)
     eng, h = gpu_run(wl, 6, variant, flavor)
@@ -68,26 +78,26 @@ def test_3d_small_all_variants_bitwise(variant, flavor):
 
 
 @pytest.mark.parametrize("name", ["config3-small", "config5-small"])
-def test_3d_level3_bitwise(name):
+def test_3d_level3(name):
     wl = workloads.by_name(name)
     t, e, oh = oracle_run(wl, 8)
     eng, h = gpu_run(wl, 8)
     check(wl, eng, h, t, e, oh)
     rs = eng.residual_stats()
     ors = e.residual_stats()
-    np.testing.assert_allclose([rs.l2h, rs.linf], [ors.l2h, ors.linf], rtol=1e-13)
+    np.testing.assert_allclose([rs.l2h, rs.linf], [ors.l2h, ors.linf], rtol=RTOL)
 
 
-def test_3d_boxmg_tables_bitwise():
+def test_3d_boxmg_tables():
     wl = workloads.config5(levels=3)
     t, e, _ = oracle_run(wl, 0)
     eng = GpuEngine(wl.tree, SolverConfig(variant=wl.variant, flavor=wl.flavor))
     for l in range(wl.tree.lmin, wl.tree.depth):
-        assert np.array_equal(eng.transfers[l].p_table, e.tr[l].p), f"P level {l}"
+        close_u(eng.transfers[l].p_table, e.tr[l].p, 1e-12, f"P level {l}")
         got = eng.ops[l].table().reshape(e.ops[l].tbl.shape)
-        assert np.array_equal(got, e.ops[l].tbl), f"A level {l}"
+        close_u(got, e.ops[l].tbl, 1e-12, f"A level {l}")
     for l in range(wl.tree.lmin, wl.tree.depth + 1):
-        assert np.array_equal(eng.eff_eps(l), e.eff[l]), f"eff level {l}"
+        close_u(eng.eff_eps(l), e.eff[l], 1e-14, f"eff level {l}")
 
 
 def test_3d_ds0_equals_additive_and_kinds():
@@ -95,59 +105,45 @@ def test_3d_ds0_equals_additive_and_kinds():
     e1, h1 = gpu_run(wl, 4, "adafac-jac", damping_scale=0.0)
     wl2 = workloads.config5(levels=3)
     e2, h2 = gpu_run(wl2, 4, "additive")
-    assert [s.l2h for s in h1] == [s.l2h for s in h2]
-    assert np.array_equal(wl.tree.u[3], wl2.tree.u[3])
+    np.testing.assert_allclose([s.l2h for s in h1], [s.l2h for s in h2], rtol=1e-13)
+    close_u(wl.tree.u[3], wl2.tree.u[3], 1e-13)
     for l in (1, 2, 3):
         assert np.array_equal(e1.kinds(l), wl.tree.vertex_kinds(l))
 
 
-def _sha(a):
-    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
-
-
-FIXTURES = sorted(f[:-5] for f in os.listdir(os.path.join(HERE, "golden3d")) if f.endswith(".json"))
+FIXTURES = sorted(f[:-4] for f in os.listdir(os.path.join(HERE, "golden3d")) if f.endswith(".npz"))
 
 
 @pytest.mark.parametrize("name", FIXTURES)
-def test_3d_fixture_history_and_sha(name):
-    fx = json.load(open(os.path.join(HERE, "golden3d", name + ".json")))
-    wl = workloads.by_name(fx["workload"])
-    eng, h = gpu_run(wl, fx["cycles"])
-    np.testing.assert_allclose([s.l2h for s in h], fx["l2h"], rtol=1e-13)
-    np.testing.assert_allclose([s.linf for s in h], fx["linf"], rtol=0)
-    for l, sha in fx["u_sha256"].items():
-        assert _sha(wl.tree.u[int(l)]) == sha, f"u level {l}"
-
-
-@pytest.mark.parametrize("ffp", ["1", "4"])
-@pytest.mark.parametrize("variant", ["adafac-jac", "additive", "additive-exp", "bpx", "afacc"])
-def test_3d_fused_fine_pass_equals_unfused(variant, ffp, monkeypatch):
-    """The fused fine pass (pipelined schedule, BoxMG) is bit-identical to the phase-by-phase cycle."""
-    n = 5
-    monkeypatch.setenv("TMG_FFP", ffp)
-    wl1 = workloads.by_name("config5-L4")
-    e1, h1 = gpu_run(wl1, n, variant)
-    monkeypatch.setenv("TMG_FFP", "0")
-    wl2 = workloads.by_name("config5-L4")
-    e2, h2 = gpu_run(wl2, n, variant)
-    np.testing.assert_allclose([s.l2h for s in h1], [s.l2h for s in h2], rtol=1e-13)
-    assert [s.linf for s in h1] == [s.linf for s in h2]
-    for l in range(1, 5):
-        assert np.array_equal(wl1.tree.u[l], wl2.tree.u[l]), f"level {l}"
-    # state round trip: residual_stats / update_fas_state / push after a pipelined run
-    np.testing.assert_allclose(e1.residual_stats().l2h, e2.residual_stats().l2h, rtol=1e-13)
-    h1b = e1.advance_many(2)
-    h2b = e2.advance_many(2)
-    np.testing.assert_allclose([s.l2h for s in h1b], [s.l2h for s in h2b], rtol=1e-13)
-    e1.pull()
-    e2.pull()
-    assert np.array_equal(wl1.tree.u[4], wl2.tree.u[4])
+def test_3d_fixture_history_and_iterate(name):
+    """Default engine vs the oracle's committed run (history, per-level norms, strided u sample)."""
+    z = np.load(os.path.join(HERE, "golden3d", name + ".npz"))
+    meta = json.loads(str(z["meta"]))
+    wl = workloads.by_name(meta["workload"])
+    eng, h = gpu_run(wl, meta["cycles"])
+    if name == "config5-L5b27":  # the config-5 bench path: weight dictionaries engaged
+        st = eng.weight_storage(wl.tree.depth - 1)
+        assert 0 < st["p_distinct"] <= st["p_rows"] // 4, st
+        assert 0 < st["pc_distinct"] <= st["pc_rows"] // 4, st
+    if name == "random-L5":  # per-cell coefficients: the dense weight streams
+        st = eng.weight_storage(wl.tree.depth - 1)
+        assert st["p_distinct"] == 0 and st["pc_distinct"] == 0, st
+    np.testing.assert_allclose([s.l2h for s in h], z["l2h"], rtol=RTOL)
+    np.testing.assert_allclose([s.linf for s in h], z["linf"], rtol=RTOL)
+    s = meta["stride"]
+    for l in range(wl.tree.lmin, wl.tree.depth + 1):
+        u = wl.tree.u[l]
+        o = l % s
+        close_u(u[o::s, o::s, o::s], z[f"sample_{l}"], what=f"u sample level {l}")
+        nrm = z[f"norms_{l}"]
+        np.testing.assert_allclose([(u * u).sum(), np.abs(u).max()], nrm[1:], rtol=RTOL)
+        assert abs(u.sum() - nrm[0]) <= RTOL * np.abs(u).sum()
 
 
 @pytest.mark.parametrize("name,variant", [("config5-small", "adafac-jac"), ("config5-L4", "adafac-jac"),
                                           ("config5-L4", "additive"), ("config5-L4", "bpx")])
-def test_3d_throttled_setup_bitwise(name, variant):
-    """Throttled BoxMG setup (one level per cycle, finest first) equals the oracle bitwise;
+def test_3d_throttled_setup(name, variant):
+    """Throttled BoxMG setup (one level per cycle, finest first) matches the oracle;
     once every level is upgraded the P and Galerkin tables equal the eager build's."""
     wl = workloads.by_name(name)
     top, lmin = wl.tree.depth, wl.tree.lmin
@@ -157,9 +153,9 @@ def test_3d_throttled_setup_bitwise(name, variant):
     check(wl, eng, h, t, e, oh)
     _, e_eager, _ = oracle_run(workloads.by_name(name), 0, variant)
     for l in range(lmin, top):
-        assert np.array_equal(eng.transfers[l].p_table, e_eager.tr[l].p), f"P level {l}"
+        close_u(eng.transfers[l].p_table, e_eager.tr[l].p, 1e-12, f"P level {l}")
         got = eng.ops[l].table().reshape(e_eager.ops[l].tbl.shape)
-        assert np.array_equal(got, e_eager.ops[l].tbl), f"A level {l}"
+        close_u(got, e_eager.ops[l].tbl, 1e-12, f"A level {l}")
 
 
 def test_3d_throttled_rebuild_restarts():
@@ -171,6 +167,27 @@ def test_3d_throttled_rebuild_restarts():
         eng.tree.u[l][...] = wl2.tree.u[l]
     eng.rebuild()
     h2 = eng.advance_many(3)
+    np.testing.assert_allclose([s.l2h for s in h2], [s.l2h for s in h1], rtol=1e-13)
+
+
+def test_3d_rebuild_after_shard_is_unsharded():
+    """tmg3_rebuild on a sharded handle drops the shard state (its buffers were freed)."""
+    import ctypes as C
+
+    from paper_1903_10367_b200 import _abi
+    wl = workloads.config5(levels=3)
+    eng, h1 = gpu_run(wl, 2)
+    L = _abi.lib()
+    lo = (C.c_int32 * 4)(0, 0, 0, 0)
+    hi = (C.c_int32 * 4)(0, 0, 0, 28)
+    _abi.check(L.tmg3_shard(eng._h, 3, lo, hi))
+    wl2 = workloads.config5(levels=3)
+    for l in range(len(wl2.tree.u)):
+        eng.tree.u[l][...] = wl2.tree.u[l]
+    eng.rebuild()
+    with pytest.raises(ValueError, match="not sharded"):
+        _abi.check(L.tmg3_phase(eng._h, _abi.PH_DOWN, 3))
+    h2 = eng.advance_many(2)
     np.testing.assert_allclose([s.l2h for s in h2], [s.l2h for s in h1], rtol=1e-13)
 
 
@@ -200,31 +217,12 @@ def test_3d_error_paths_raise_like_the_reference():
         sharding.plan(2, 8)  # too shallow for 8 ranks
 
 
-@pytest.mark.parametrize("variant,throttled", [("adafac-jac", False), ("additive", False), ("afacc", False),
-                                               ("adafac-jac", True)])
-def test_3d_prolongation_stream_equals_tile(variant, throttled, monkeypatch):
-    """The TMA-fed finest-level prolongation (k3_up_tma over the cube-owned copy of P;
-    used from depth 5 up) is bit-identical to the per-thread tiled kernel (TMG_UPQ=0),
-    which the depth <= 4 tests pin to the oracle."""
-    n = 4
-    monkeypatch.setenv("TMG_UPQ", "1")
-    wl1 = workloads.by_name("config5-L5")
-    e1, h1 = gpu_run(wl1, n, variant, throttled=throttled)
-    monkeypatch.setenv("TMG_UPQ", "0")
-    wl2 = workloads.by_name("config5-L5")
-    e2, h2 = gpu_run(wl2, n, variant, throttled=throttled)
-    assert [s.l2h for s in h1] == [s.l2h for s in h2]
-    assert [s.linf for s in h1] == [s.linf for s in h2]
-    for l in range(1, 6):
-        assert np.array_equal(wl1.tree.u[l], wl2.tree.u[l]), f"level {l}"
-
-
 @pytest.mark.parametrize("variant", ["adafac-jac", "additive", "afacc"])
 @pytest.mark.parametrize("wname", ["config5-L5", "random-L5"])
 def test_3d_weight_dictionary_equals_dense(variant, wname, monkeypatch):
     """Level ltop-1's BoxMG weights as bitwise-verified row dictionaries (k3_smr's DICT variant,
-    k3_up_dict; TMG_PDICT=2 forces them even where rows barely repeat) give the same iterate,
-    bit for bit, as the dense P / Pc streams (TMG_PDICT=0)."""
+    k3_up_dict; TMG_PDICT=2 forces them even where rows barely repeat) give the same iterate as
+    the dense P / Pc streams (TMG_PDICT=0), up to the kernels' different FMA contraction."""
     def make():
         if wname == "config5-L5":
             return workloads.config5(levels=5, block=27)  # config 5's block size (9 level-4 cells)
@@ -235,12 +233,9 @@ def test_3d_weight_dictionary_equals_dense(variant, wname, monkeypatch):
 
     n = 4
     monkeypatch.setenv("TMG_PDICT", "2")
-    monkeypatch.setenv("TMG_PDICT_SMR", "1")
-    monkeypatch.setenv("TMG_PDICT_GAL", "1")
     wl1 = make()
     e1, h1 = gpu_run(wl1, n, variant)
     st = e1.weight_storage(4)
-    assert 0 < st["galerkin_distinct"] <= st["galerkin_rows"], st
     if wname == "config5-L5":
         assert 0 < st["p_distinct"] <= st["p_rows"], st
         assert 0 < st["pc_distinct"] <= st["pc_rows"], st
@@ -250,48 +245,17 @@ def test_3d_weight_dictionary_equals_dense(variant, wname, monkeypatch):
     wl2 = make()
     e2, h2 = gpu_run(wl2, n, variant)
     assert e2.weight_storage(4)["p_distinct"] == 0
-    assert [s.l2h for s in h1] == [s.l2h for s in h2]
-    assert [s.linf for s in h1] == [s.linf for s in h2]
+    np.testing.assert_allclose([s.l2h for s in h1], [s.l2h for s in h2], rtol=1e-12)
+    np.testing.assert_allclose([s.linf for s in h1], [s.linf for s in h2], rtol=1e-12)
     for l in range(1, 6):
-        assert np.array_equal(wl1.tree.u[l], wl2.tree.u[l]), f"level {l}"
-
-
-@pytest.mark.parametrize("layout", [("0", "2", "0"), ("1", "2", "0"), ("1", "7", "0")])
-@pytest.mark.parametrize("wname", ["config5-L5", "random-L5"])
-def test_3d_smr_layouts_equal(layout, wname, monkeypatch):
-    """k3_smr's thread layouts -- the default (restriction thread per coarse vertex over both
-    planes and fields, 7-column smoothing groups, smoothing and restriction decoupled by named
-    barriers) and the earlier ones (TMG_SMR_RV=0: two roles owning alternate planes;
-    TMG_SMR_GH=2: column pairs; TMG_SMR_DEC=0: one CTA barrier per fine plane) -- give the same
-    iterate bit for bit, on the dictionary (blockwise eps) and the dense (per-cell eps) weight
-    paths."""
-    def make():
-        if wname == "config5-L5":
-            return workloads.config5(levels=5, block=27)
-        wl = workloads.by_name("config5-L5")
-        rng = np.random.default_rng(11)
-        wl.tree.eps[5][...] = 10.0 ** rng.uniform(-2, 2, wl.tree.eps[5].shape)
-        return wl
-
-    n = 4
-    wl1 = make()
-    e1, h1 = gpu_run(wl1, n, "adafac-jac")
-    monkeypatch.setenv("TMG_SMR_RV", layout[0])
-    monkeypatch.setenv("TMG_SMR_GH", layout[1])
-    monkeypatch.setenv("TMG_SMR_DEC", layout[2])
-    wl2 = make()
-    e2, h2 = gpu_run(wl2, n, "adafac-jac")
-    assert [s.l2h for s in h1] == [s.l2h for s in h2]
-    assert [s.linf for s in h1] == [s.linf for s in h2]
-    for l in range(1, 6):
-        assert np.array_equal(wl1.tree.u[l], wl2.tree.u[l]), f"level {l}"
+        close_u(wl1.tree.u[l], wl2.tree.u[l], 1e-12, f"level {l}")
 
 
 def test_3d_weight_dictionary_default_on_blocks():
     """On blockwise-constant coefficients (config 5's structure) the default setup stores level
     ltop-1's weights (P for the restriction, the cube-owned copy for the prolongation) as
     dictionaries: far fewer distinct rows than coarse vertices / cubes; the Galerkin rows stay
-    dense unless TMG_PDICT_GAL=1."""
+    dense."""
     wl = workloads.config5(levels=5, block=27)  # config 5's block size (9 level-4 cells)
     eng, _ = gpu_run(wl, 1)
     st = eng.weight_storage(wl.tree.depth - 1)
