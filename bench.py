@@ -19,12 +19,16 @@ fine DoFs, L2-resident and latency-bound) is ``--workload config2``.
 * roofline   -- dominant kernel: algorithmic bytes per launch / mean launch
                 time (events around each launch, tmg_profile_cycles); also the
                 whole-cycle B_alg / t_cycle.
-* cpu_baseline -- the CPU oracle port on 1 core on a bounded sample (2D:
-                oracle/mg2d.py on the workload itself; 3D: oracle/mg3d.py on
-                the same structure at depth 4 -- there is no 3D reference).
+* cpu_baseline -- the CPU oracle port on 1 pinned core on a bounded sample (2D:
+                oracle/mg2d.py on the workload itself; config 3: the workload
+                itself; config 5: oracle/mg3d.py on the same structure at
+                depth 5, 14.2 M fine DoFs -- depth 6 needs ~270 GB in numpy;
+                see CPU_SAMPLES_3D).  The line names the sample, the CPU model
+                and the host's core count.
 * --impl reference -- the reference's CPU algorithm (the oracle port; the
-                reference is pure Python and cannot travel to the box) on the
-                same workload (3D: the depth-4 sample); rank 0 only.
+                reference is pure Python and cannot travel to the box), the
+                same samples, K + W cycles; `config` is the GPU arm's, the
+                sample is named in `cpu_baseline`; rank 0 only.
 
 Multi-GPU (torchrun, one process per GPU): 3D workloads are slab-sharded
 over the ranks with NCCL (paper_1903_10367_b200/sharding.py; strong
@@ -254,16 +258,60 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sms)}
 
 
-CPU_SAMPLE_3D = {"config3": "config3-L4", "config5": "config5-L4"}
+# 3D CPU samples, largest first: (sample workload, frozen d-linear setup?).  The oracle's eager
+# BoxMG setup at depth 5 takes ~7 min on one core, so the depth-5 BoxMG sample starts the oracle in
+# its throttled mode (d-linear weights in the same dense 125-weight P tables, rediscretised rows in
+# the same 27-point tables) and freezes it there: every cycle runs the same array operations over
+# the same bytes as the eager build's cycle; only the weights' values differ.  Depth 6 itself needs
+# ~270 GB of host memory in numpy (476 MB at depth 4, x27 per level) and is not runnable.
+CPU_SAMPLES_3D = {
+    "config3": [("config3-L5", False), ("config3-L4", False)],
+    "config5": [("config5-L5b27", True), ("config5-L4", False)],
+}
 
 
-def oracle_engine(wl):
+def host_info() -> dict:
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+class PinOneCore:
+    """taskset -c <first allowed core> for the CPU legs (1 core, pinned)."""
+
+    def __enter__(self):
+        self.prev = None
+        try:
+            self.prev = os.sched_getaffinity(0)
+            self.core = min(self.prev)
+            os.sched_setaffinity(0, {self.core})
+        except (AttributeError, OSError):
+            self.core = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.prev is not None:
+            try:
+                os.sched_setaffinity(0, self.prev)
+            except OSError:
+                pass
+
+
+def oracle_engine(wl, frozen_dlinear: bool = False):
     """The CPU oracle engine on the workload's inputs (checker / CPU baseline only)."""
     if wl.dim == 3:
         from oracle import mg3d
         t = mg3d.Tree(wl.tree.depth, wl.tree.lmin)
         t.eps[wl.tree.depth] = wl.tree.eps[wl.tree.depth].copy()
-        eng = mg3d.Engine(t, mg3d.Config(variant=wl.variant, flavor=wl.flavor))
+        eng = mg3d.Engine(t, mg3d.Config(variant=wl.variant, flavor=wl.flavor, throttled=frozen_dlinear))
+        if frozen_dlinear:
+            eng.thr_next = t.lmin - 1  # never upgrade: the BoxMG setup is not part of a cycle
         eng.rhs.update({l: b.copy() for l, b in wl.rhs.items()})
         return eng
     from oracle import mg2d
@@ -276,24 +324,33 @@ def oracle_engine(wl):
     return eng
 
 
-def cpu_port_time(wl_name: str, cycles: int, budget_s: float = 20.0):
-    """Oracle (numpy restatement of the reference; 3D: the d-generic restatement) on
-    1 core, on a bounded sample: seconds per cycle of the sample workload."""
+def cpu_sample(wl_name: str, cycles: int, budget_s: float):
+    """The oracle on the largest sample of the workload whose `cycles` cycles fit `budget_s`
+    (estimated from one warm-up cycle): (engine, sample workload, seconds of the warm-up cycle,
+    setup seconds, description).  2D workloads run at their real size."""
     from paper_1903_10367_b200 import workloads
-    wl_name = CPU_SAMPLE_3D.get(wl_name, wl_name)
-    wl = workloads.by_name(wl_name)
-    t0 = time.perf_counter()
-    eng = oracle_engine(wl)
-    setup = time.perf_counter() - t0
-    eng.advance()  # warm-up
-    done, t0 = 0, time.perf_counter()
-    while done < cycles:
-        eng.advance()
-        done += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = (time.perf_counter() - t0) / done
-    return dt, done, setup, wl
+    base = wl_name.split("-")[0]
+    cands = CPU_SAMPLES_3D.get(wl_name) or ([(wl_name, False)] if base not in CPU_SAMPLES_3D or "-" in wl_name
+                                            else CPU_SAMPLES_3D[base])
+    for k, (name, frozen) in enumerate(cands):
+        wl = workloads.by_name(name)
+        t0 = time.perf_counter()
+        eng = oracle_engine(wl, frozen)
+        setup = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        eng.advance()  # warm-up (numpy has no JIT; one cycle faults the work arrays in)
+        first = time.perf_counter() - t0
+        if first * cycles <= budget_s or k == len(cands) - 1:
+            if wl.dim == 3:
+                what = ("oracle/mg3d.py (3D restatement of the reference's numpy cycle; no 3D reference exists)"
+                        + ("; BoxMG tables frozen at their throttled start (d-linear / rediscretised values in "
+                           "the same dense P and 27-point tables: same operations and bytes per cycle, no "
+                           "7-minute eager setup)" if frozen else ""))
+            else:
+                what = "oracle/mg2d.py (numpy restatement of treemg, bit-identical iterates)"
+            return eng, wl, first, setup, what
+        del eng
+    raise AssertionError
 
 
 def run_reference(args, dist: Dist):
@@ -301,35 +358,49 @@ def run_reference(args, dist: Dist):
         return
     from paper_1903_10367_b200 import workloads
     full = workloads.by_name(args.workload)
-    sample = CPU_SAMPLE_3D.get(args.workload)
-    wl = workloads.by_name(sample) if sample else full
+    ws = dist_env()[0]
+    hi = host_info()
+    with PinOneCore() as pin:
+        # K steps + W warm-up on one engine; a step = one cycle of the port on the sample
+        eng, wl, first, setup, what = cpu_sample(args.workload, args.steps + args.warmup, args.ref_budget)
+        for _ in range(args.warmup - 1):  # (cpu_sample ran the first warm-up cycle)
+            eng.advance()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            eng.advance()
+        total = time.perf_counter() - t0
     n_fine = wl.fine_dofs()
-    # time K steps on one engine (each step = one cycle of the port; 3D: one cycle
-    # of the bounded sample, the same structure at depth 4)
-    eng = oracle_engine(wl)
-    for _ in range(args.warmup):
-        eng.advance()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        eng.advance()
-    total = time.perf_counter() - t0
     v = n_fine * args.steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, SURVEY.md §8(d))",
-        "config": {"workload": full.name, "levels": f"{full.tree.lmin}..{full.ltop}",
-                   "variant": full.variant, "flavor": full.flavor, "n_fine": full.fine_dofs()},
+        "config": config_of(full, ws, sharded=full.dim == 3 and (ws > 1 or args.force_shard)),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": f"{args.steps} cycles of {wl.name} after {args.warmup} warm-up; "
-                                   + ("oracle/mg3d.py (3D restatement, no 3D reference exists; "
-                                      "same structure at depth 4, DoF/s of the sample)"
-                                      if sample else "oracle/mg2d.py (numpy restatement of treemg, "
-                                      "bit-identical iterates)") + ", single thread"},
+                         "sample": f"{args.steps} cycles of {wl.name} ({n_fine} fine DoFs; value = fine DoFs "
+                                   f"of the sample / s) after {args.warmup} warm-up; {what}; 1 thread pinned "
+                                   f"to core {pin.core} of {hi['cpu_model']} ({hi['nproc']} cores); "
+                                   f"setup {setup:.1f} s",
+                         "sample_workload": wl.name, "sample_n_fine": n_fine, **hi},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def config_of(wl, ws: int, sharded: bool = False) -> dict:
+    """The `config` object both arms print (identical for the same workload and N)."""
+    if sharded:
+        from paper_1903_10367_b200 import sharding
+        pl = sharding.plan(wl.tree.depth, ws)
+        par = (f"slab{ws} (levels {pl.ls}..{wl.ltop} sharded on axis 0, "
+               f"levels {wl.tree.lmin}..{pl.ls - 1} replicated)")
+        l2 = "inputs larger than L2 (no flush)"
+    else:
+        par = "replicas" if ws > 1 else "single"
+        l2 = f"flushed ({FLUSH_BYTES >> 20} MiB write) before every timed cycle"
+    return {"workload": wl.name, "levels": f"{wl.tree.lmin}..{wl.ltop}", "variant": wl.variant,
+            "flavor": wl.flavor, "n_fine": wl.fine_dofs(), "parallelism": par, "l2": l2}
 
 
 def run_ours(args, dist: Dist):
@@ -473,13 +544,22 @@ def run_ours(args, dist: Dist):
     # ---- CPU baseline (rank 0 at N=1 only) ---------------------------------------
     cpu = None
     if dist.rank == 0 and dist.ws == 1 and not args.no_cpu:
-        dt, done, setup, swl = cpu_port_time(args.workload, 400, budget_s=args.cpu_budget)
+        hi = host_info()
+        with PinOneCore() as pin:
+            ceng, swl, first, setup, what = cpu_sample(args.workload, 2, 2 * args.cpu_budget)
+            done, t0 = 0, time.perf_counter()
+            while done < 400:
+                ceng.advance()
+                done += 1
+                if time.perf_counter() - t0 + first > args.cpu_budget:
+                    break
+            dt = (time.perf_counter() - t0) / done
         cpu = {"value": swl.fine_dofs() / dt, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"{done} cycles of {swl.name} (after 1 warm-up) in "
-                         f"{dt * done:.1f} s; "
-                         + ("oracle/mg3d.py 3D restatement (no 3D reference), same structure at "
-                            "depth 4" if swl.dim == 3 else "oracle/mg2d.py numpy restatement")
-                         + f", 1 thread; setup {setup:.2f} s"}
+               "sample": f"{done} cycles of {swl.name} ({swl.fine_dofs()} fine DoFs; value = fine DoFs of the "
+                         f"sample / s) after 1 warm-up, {dt * done:.1f} s; {what}; 1 thread pinned to core "
+                         f"{pin.core} of {hi['cpu_model']} ({hi['nproc']} cores); setup {setup:.1f} s",
+               "sample_workload": swl.name, "sample_n_fine": swl.fine_dofs(), **hi}
+        del ceng
 
     if dist.rank == 0:
         line = {
@@ -487,11 +567,8 @@ def run_ours(args, dist: Dist):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, SURVEY.md §8(d))",
-            "config": {"workload": wl.name, "levels": f"{wl.tree.lmin}..{wl.ltop}",
-                       "variant": wl.variant, "flavor": wl.flavor, "n_fine": n_fine,
-                       "parallelism": "replicas" if dist.ws > 1 else "single",
-                       "l2": f"flushed ({FLUSH_BYTES >> 20} MiB write) before every timed cycle",
-                       "ms_per_step_l2_warm": ms_warm / args.steps,
+            "config": config_of(wl, dist.ws),
+            "detail": {"ms_per_step_l2_warm": ms_warm / args.steps,
                        "total_updates_per_s": dist.ws * updates / (ms_step * 1e-3),
                        "weight_storage": storage},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
@@ -580,12 +657,8 @@ def run_sharded(args, dist: Dist):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, SURVEY.md §8(d))",
-            "config": {"workload": wl.name, "levels": f"{wl.tree.lmin}..{wl.ltop}",
-                       "variant": wl.variant, "flavor": wl.flavor, "n_fine": n_fine,
-                       "parallelism": f"slab{dist.ws} (levels {pl.ls}..{wl.ltop} sharded on axis 0, "
-                                      f"levels {wl.tree.lmin}..{pl.ls - 1} replicated)",
-                       "l2": "inputs larger than L2 (no flush)",
-                       "l2h_last": hist[0].l2h},
+            "config": config_of(wl, dist.ws, sharded=True),
+            "detail": {"l2h_last": hist[0].l2h},
             "roofline": {"bound": "hbm", "kernel": "cycle (per GPU)", "achieved": per_gpu, "peak": peak,
                          "unit": "GB/s", "frac": per_gpu / peak, "traffic": None,
                          "cycle_B_alg": bm["cycle"]},
@@ -611,7 +684,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--workload", default="config5")
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-budget", type=float, default=25.0,
+                    help="seconds of timed CPU work in the cpu_baseline leg")
+    ap.add_argument("--ref-budget", type=float, default=480.0,
+                    help="--impl reference: largest sample whose K + W cycles fit this many seconds")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-1e-8 run")
     ap.add_argument("--ttt-cap", type=int, default=200, help="cycle cap of the time-to-1e-8 run")

@@ -565,7 +565,7 @@ int launch_smr(Engine3* e, int l, bool smooth, int clo = -1, int chi = -1) {
   const dim3 grid(tiles, (n + A.chunk - 1) / A.chunk);
   cudaEvent_t e0_ = nullptr;
   TRY3(begin_k(e, &e0_));
-  if (cc.Pd) k3_smr<true, 1, 7, true><<<grid, kRTasks + kRK * kRJ, kSmrSmemDB, e->s>>>(A);
+  if (cc.Pd) k3_smr<true, 1, 7, true><<<grid, kRThreads, kSmrSmemDB, e->s>>>(A);
   else k3_smr<false, 1, 7><<<grid, kRTasks + kRK * kRJ, kSmrSmem, e->s>>>(A);
   CKL3();
   TRY3(end_k(e, kname("k3_smooth", l), e0_));

@@ -46,6 +46,8 @@
 // three sm buffers; bitwise) measured slower, 3.29-3.44 vs 3.0 ms.
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "kernels3d.cuh"
 
 namespace t3 {
@@ -158,13 +160,13 @@ __device__ __forceinline__ int floor3s(int x) { return x >= 0 ? x / 3 : -((2 - x
 // warp's vertices have neighbouring ids), the same doubles in the same order.
 // RV = 1 (TMG_SMR_RV=1): one restriction thread per coarse vertex carrying both coarse planes and
 // both fields (x loaded once for both planes), 128 restriction threads (384 per CTA)
-template <bool C, bool NX, bool JAC>
+template <bool C, bool NX, bool JAC, int Q0 = 0, int Q1 = 25>
 __device__ __forceinline__ void terms2(const double* wc, const double* wn, int ws, const double* xr,
                                        const double* xs, bool ctr0, bool zc, double& cR, double& cS,
                                        double& nR, double& nS) {
   constexpr int ld = kRW;
 #pragma unroll
-  for (int q = 0; q < 25; ++q) {
+  for (int q = Q0; q < Q1; ++q) {
     const int oj = q / 5 - 2, ok = q % 5 - 2;
     const double x = xr[oj * ld + ok];
     const double y = JAC ? xs[oj * ld + ok] : 0.0;
@@ -182,8 +184,14 @@ __device__ __forceinline__ void terms2(const double* wc, const double* wn, int w
   }
 }
 
+// DEC: 256 restriction threads -- the 25 in-plane terms of a step are split between two threads of
+// a coarse vertex (q < 13 | q >= 13, in different warps), whose partial sums meet through `comb`
+// when a coarse plane completes: the restriction group was the critical path with one thread per
+// vertex (ncu: the smoothing warps waited on its EMPTY barriers 42 % of their time).
+constexpr int kRSplit = 13;
 template <bool DICT, int RV, int GH, bool DEC = false>
-__global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_smr(const __grid_constant__ Smr A) {
+__global__ void __launch_bounds__(DEC ? kRThreads : (RV ? kRTasks + kRK * kRJ : kRThreads), 1)
+    k3_smr(const __grid_constant__ Smr A) {
   static_assert(!DEC || (DICT && RV == 1), "the decoupled schedule needs the dictionary and RV 1");
   constexpr int kSPairs = kSPer<GH>, kSCols = GH * kSPairs, kSGroups = kSW * (kSH / GH);
   constexpr int kRStages = DEC ? kRStagesB : t3::kRStages;  // rho slots
@@ -192,6 +200,7 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
   constexpr int oRSd = oRRows + 3 * kRRowSet;
   extern __shared__ __align__(128) double sr[];
   __shared__ __align__(8) uint64_t bar[kRStagesB], pbar[kPStages], tbar[kRNT], rbar[3];
+  __shared__ double comb[DEC ? 2 * kRK * kRJ : 2];  // DEC: the upper half's partial sums of a completed plane
   const int N = A.N, Nc = A.Nc, n = Nc - 2;
   const int tk = blockIdx.x % A.tilesK, tj = blockIdx.x / A.tilesK;
   const int K0 = 1 + tk * kRK, J0 = 1 + tj * kRJ;
@@ -230,11 +239,22 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
   // 12-15: r = 1), so a thread keeps its plane's two sums over all five fine planes it meets
   const int task = lt - kRTasks;
   const int role = RV ? 0 : (task >> 7) & 1, w = task & (kRK * kRJ - 1);
+  const int half = DEC ? (task >> 7) & 1 : 0;  // DEC: which part of a step's 25 terms (warp-uniform)
   static_assert(kRK * kRJ == 128, "two restriction roles of 128 vertices");
   const int wj = w / kRK, wk = w % kRK;
   const int rJ = J0 + wj, rK = K0 + wk;
   const bool rtask = !smoother && rJ <= n && rK <= n;
   double accR = 0.0, accS = 0.0, accNR = 0.0, accNS = 0.0;
+  // DEC, lower half: the completed plane's partial sums, stored once the upper half's are in `comb`
+  double pendR = 0.0, pendS = 0.0;
+  size_t pend_ix = 0;
+  bool pending = false;
+  auto flush_pending = [&]() {
+    if (!pending) return;
+    A.bR[pend_ix] = pendR + comb[2 * w];
+    if (A.jac) A.bT[pend_ix] = pendS + comb[2 * w + 1];
+    pending = false;
+  };
 
   auto issue_r = [&](int p) {  // rho plane p into its slot
     const int sl = (p - p0) % kRStages;
@@ -297,7 +317,14 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
     issue_tab(p0 / 3 + 2);
   }
 
-  // C: sm of the plane below rho's slot Rp completes into Sb (pending partial sums advance)
+  // C: sm of the plane below rho's slot Rp completes into Sb (pending partial sums advance).
+  // Per column and plane: F = the 4 in-plane edge neighbours' sum, D = the 4 in-plane diagonals'
+  // sum (the stencil has no face taps); sm(t-1) = scale (8/3 x(t-1) - 1/6 (F(t-2) + D(t-1) + F(t))
+  // - 1/12 (D(t-2) + D(t))).  The rows' outer sums a_r = x[r][k-1] + x[r][k+1] are shared by the
+  // group's columns (about 10 fp64 operations per column and plane; summation order differs from
+  // the oracle's plane-major chain, within the 3D tolerance).  State per column: SEa = F(t-2) +
+  // D(t-1), SCa = D(t-2), XA = x(t-1), SEb = F(t-1), SCb = D(t-1).
+  const double kD8s = C_D8 * A.scale, kE6s = C_E6 * A.scale, kC12s = C_C12 * A.scale;
   auto smooth_body = [&](const double* Rp, double* Sb, bool sok) {
 #pragma unroll
         for (int mp = 0; mp < kSPairs; ++mp) {
@@ -305,27 +332,25 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
           // rows GH jp - 1 .. GH jp + GH, cols kk - 1 .. kk + 1 of the sm window (rho window + 1)
           const int rb = sbase[mp];
           const unsigned mk = sok ? smask[mp] : 0u;
-          double R[GH + 2][3];
+          double Rc[GH + 2], Ra[GH + 2];
 #pragma unroll
-          for (int a = 0; a < GH + 2; ++a)
-#pragma unroll
-            for (int b = 0; b < 3; ++b) R[a][b] = Rp[rb + a * kRW + b];
+          for (int a = 0; a < GH + 2; ++a) {
+            Rc[a] = Rp[rb + a * kRW + 1];
+            Ra[a] = Rp[rb + a * kRW] + Rp[rb + a * kRW + 2];
+          }
 #pragma unroll
           for (int h = 0; h < GH; ++h) {
             const int m = GH * mp + h;
-            const double f0 = R[h][1], f1 = R[h + 1][0], f2 = R[h + 1][2], f3 = R[h + 2][1];
-            const double d0 = R[h][0], d1 = R[h][2], d2 = R[h + 2][0], d3 = R[h + 2][2];
-            const double xc = R[h + 1][1];
-            double se = (((SEa[m] + f0) + f1) + f2) + f3;
-            double sc = (((SCa[m] + d0) + d1) + d2) + d3;
-            double v = ((C_D8 * XA[m]) - (C_E6 * se)) - (C_C12 * sc);
-            v = v * A.scale;
+            const double Dt = Ra[h] + Ra[h + 2];
+            const double Ft = (Rc[h] + Rc[h + 2]) + Ra[h + 1];
+            const double se = SEa[m] + Ft, sc = SCa[m] + Dt;
+            const double v = (kD8s * XA[m] - kE6s * se) - kC12s * sc;
             Sb[rb + h * kRW] = ((mk >> h) & 1u) ? v : 0.0;
-            SEa[m] = (((SEb[m] + d0) + d1) + d2) + d3;
+            SEa[m] = SEb[m] + Dt;
             SCa[m] = SCb[m];
-            XA[m] = xc;
-            SEb[m] = ((f0 + f1) + f2) + f3;
-            SCb[m] = ((d0 + d1) + d2) + d3;
+            XA[m] = Rc[h + 1];
+            SEb[m] = Ft;
+            SCb[m] = Dt;
           }
         }
   };
@@ -354,21 +379,38 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
               ws = kRJ * kPW;
             }
             const bool c0 = o == 0, zc = A.zc != 0;
-            if (c && nx) {
-              if (A.jac) terms2<true, true, true>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
-              else terms2<true, true, false>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
-            } else if (c) {
-              if (A.jac) terms2<true, false, true>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
-              else terms2<true, false, false>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
-            } else if (nx) {
-              if (A.jac) terms2<false, true, true>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
-              else terms2<false, true, false>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
-            }
+            auto run = [&](auto Q0, auto Q1) {
+              constexpr int q0 = decltype(Q0)::value, q1 = decltype(Q1)::value;
+              if (c && nx) {
+                if (A.jac) terms2<true, true, true, q0, q1>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
+                else terms2<true, true, false, q0, q1>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
+              } else if (c) {
+                if (A.jac) terms2<true, false, true, q0, q1>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
+                else terms2<true, false, false, q0, q1>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
+              } else if (nx) {
+                if (A.jac) terms2<false, true, true, q0, q1>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
+                else terms2<false, true, false, q0, q1>(wc, wn, ws, xr, xs, c0, zc, accR, accS, accNR, accNS);
+              }
+            };
+            using std::integral_constant;
+            if (!DEC) run(integral_constant<int, 0>{}, integral_constant<int, 25>{});
+            else if (half == 0) run(integral_constant<int, 0>{}, integral_constant<int, kRSplit>{});
+            else run(integral_constant<int, kRSplit>{}, integral_constant<int, 25>{});
             if (o == 2) {
               if (c) {
                 const size_t ix = ((size_t)m3 * Nc + rJ) * Nc + rK;
-                A.bR[ix] = accR;
-                if (A.jac) A.bT[ix] = accS;
+                if (!DEC) {
+                  A.bR[ix] = accR;
+                  if (A.jac) A.bT[ix] = accS;
+                } else if (half) {  // read by the lower half after the next step's barrier
+                  comb[2 * w] = accR;
+                  comb[2 * w + 1] = accS;
+                } else {
+                  pend_ix = ix;
+                  pendR = accR;
+                  pendS = accS;
+                  pending = true;
+                }
               }
               accR = accNR;
               accS = accNS;
@@ -383,7 +425,7 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
     //   EMPTY 4 + b  the restriction arrives when done with plane x (sm(x), rho(x)), the
     //                smoothing syncs before writing sm(x + 3) and re-arming rho(x)'s slot.
     // The restriction may lag by three planes; every arrive has exactly one matching sync.
-    constexpr int kAll = kRTasks + kRK * kRJ;
+    constexpr int kAll = kRThreads, kRest = kRThreads - kRTasks;
     auto sbuf = [&](int x) { return (x - p0 + 3) % 3; };  // x >= p0 - 1
     if (smoother) {
       int rsl = 0;
@@ -428,6 +470,7 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
           }
         }
         named_sync(1 + sbuf(s), kAll);  // sm(s) complete; every restriction thread left s - 1
+        flush_pending();
         if (oc == 1 && lt < kRTasks + 32) {
           fence_proxy_async();
           if (lt == kRTasks) issue_tab(m3c + 4);
@@ -437,6 +480,8 @@ __global__ void __launch_bounds__(RV ? kRTasks + kRK * kRJ : kRThreads, 1) k3_sm
         restrict_body(s, ssl, m3c, oc, k3c, k6c, sr + oS + sbuf(s) * kSBuf, s - s0);
         if (s + 3 <= pEnd - 1) named_arrive(4 + sbuf(s), kAll);
       }
+      named_sync(8, kRest);  // the last plane's upper-half sums
+      flush_pending();
     }
     return;
   }

@@ -31,6 +31,7 @@ constexpr int kQTabBytes = 256;           // {n, ids[kQRows]} uint32, local[64] 
 constexpr int oDU = 0, oDG = qal16(kQUd), oDC = oDG + qal16(kQUd);
 constexpr int kDSlot = oDC + qal16(kQCd);
 constexpr int kDNS = 3, kDNT = 8, kDTD = 6, kDNR = 4, kDRD = 3, kDPF = 4;
+static_assert(kDNR == kDRD + 1, "row sets: one per step in flight plus the one being staged");
 constexpr int kDCons = 6 * 32, kDThreads = kDCons + 64;  // consumers + two producer warps
 constexpr int oDTab = kDNS * kDSlot, oDRows = oDTab + kDNT * kQTabBytes / 8, kDRowSlot = kQRows * kQRowS;
 constexpr size_t kUpDictSmem = sizeof(double) * (oDRows + kDNR * kDRowSlot);
@@ -118,6 +119,7 @@ template <bool CARRY, bool G = true>
 __global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant__ UpD A) {
   extern __shared__ __align__(128) double sq[];
   __shared__ __align__(8) uint64_t full[kDNS], done[kDNS], tful[kDNT], rful[kDNR];
+  __shared__ int rsl[kDNR];  // row slot of the step whose barrier is rful[same index]
   const Up3& a = A.a;
   const int Nc = a.Nc, nc = Nc - 1, N = a.N;
   const int lt = threadIdx.x;
@@ -178,17 +180,35 @@ __global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant
                 A.tab + (((size_t)I * A.tilesJ + J0 / kQJ) * A.tilesK + K0 / kQK) * kQTabBytes, kQTabBytes,
                 &tful[r % kDNT]);
     };
+    // the row set of step s: a tile's consecutive layers inside an eps block meet the same rows
+    // (same ids in the same order), so the set staged last is kept while the ids repeat -- the
+    // step's barrier then gets a plain arrival and rsl[] names the slot that holds its rows.  A
+    // new set goes to slot (set counter) % kDNR: the steps in flight (k + 1 .. k + kDRD, at most
+    // one set each) and the new one use at most kDNR = kDRD + 1 sets.
+    int held_n = -1, held_set = -1;
+    uint32_t held_id = 0u;
     auto rows = [&](int s) {  // the table of step s is in (waited here)
       const int r = s - s0;
       mbar_wait(&tful[r % kDNT], (unsigned)(r / kDNT) & 1u);
       const uint32_t* T = reinterpret_cast<const uint32_t*>(tab_of(r));
       const int n = (int)T[0];
+      const uint32_t id = lane < n ? T[1 + lane] : 0u;
       uint64_t* rb = &rful[r % kDNR];
-      if (l0) mbar_expect_tx(rb, kDRowBytes * (unsigned)n);
+      const bool same = __all_sync(0xffffffffu, n == held_n && (lane >= n || id == held_id));
+      if (!same) {
+        ++held_set;
+        held_n = n;
+        held_id = id;
+      }
+      const int slot = held_set % kDNR;
+      if (l0) {
+        rsl[r % kDNR] = slot;
+        if (same) mbar_arrive(rb);
+        else mbar_expect_tx(rb, kDRowBytes * (unsigned)n);
+      }
       __syncwarp();
-      if (lane < n)
-        bulk_load(sq + oDRows + (r % kDNR) * kDRowSlot + lane * kQRowS, A.dict + (size_t)T[1 + lane] * kDictW,
-                  kDRowBytes, rb);
+      if (!same && lane < n)
+        bulk_load(sq + oDRows + slot * kDRowSlot + lane * kQRowS, A.dict + (size_t)id * kDictW, kDRowBytes, rb);
     };
     if (streamer) {
       if (!l0) return;
@@ -245,7 +265,7 @@ __global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant
     mbar_wait(&rful[r % kDNR], (unsigned)(r / kDNR) & 1u);
     const int J = J0 + ty, K = K0 + tx;
     if (J < nc && K < nc) {
-      const double* Wd = sq + oDRows + (r % kDNR) * kDRowSlot + kQRowS * tab_of(r)[132 + cl];
+      const double* Wd = sq + oDRows + rsl[r % kDNR] * kDRowSlot + kQRowS * tab_of(r)[132 + cl];
       const double* Gs = b + oDG;
       const double* Cs = b + oDC;
       double* Us = b + oDU;
