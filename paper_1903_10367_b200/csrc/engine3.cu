@@ -19,6 +19,7 @@
 #include "kernels3d_top4.cu"
 #include "kernels3d_updict.cu"
 #include "kernels3d_dict.cu"
+#include "kernels3d_rap.cu"
 
 namespace {
 
@@ -856,6 +857,39 @@ int refresh_pc(Engine3* e, int l) {
   return TMG_OK;
 }
 
+// Galerkin rows of level l's interior vertices (k3_rap_y + k3_rap_out over slabs of coarse planes;
+// the scratch Y holds 343 doubles per slab vertex, at most about 2 GB)
+int galerkin_rows(Engine3* e, int l, const Rows& raw) {
+  Lvl3& c = e->L[l];
+  const size_t plane = (size_t)c.N * c.N;
+  const int interior = c.N - 2;
+  const int per = (int)std::max<size_t>(1, std::min<size_t>(interior, ((size_t)2 << 30) / (plane * 343 * 8)));
+  double* Y = nullptr;
+  CK3(cudaMalloc(&Y, sizeof(double) * plane * 343 * per));
+  int rc = TMG_OK;
+  for (int I0 = 1; I0 <= interior && rc == TMG_OK; I0 += per) {
+    RapArgs A{};
+    A.Nc = c.N;
+    A.Nf = raw.N;
+    A.I0 = I0;
+    A.planes = std::min(per, interior - I0 + 1);
+    A.P = c.P;
+    A.tbl = raw.tbl;
+    A.e = raw.e;
+    A.Y = Y;
+    A.out = c.tbl;
+    const size_t sv = plane * A.planes;
+    const unsigned gb = (unsigned)std::min<size_t>((sv + 31) / 32, (size_t)num_sms() * 32);
+    if (raw.tbl) k3_rap_y<false><<<gb, dim3(32, kRapYW), 0, e->s>>>(A);
+    else k3_rap_y<true><<<gb, dim3(32, kRapYW), 0, e->s>>>(A);
+    k3_rap_out<<<gb, dim3(32, 27), 0, e->s>>>(A);
+    if (cudaGetLastError() != cudaSuccess) rc = fail3(e, TMG_ECUDA, "kernel launch: k3_rap_y / k3_rap_out");
+  }
+  cudaStreamSynchronize(e->s);
+  cudaFree(Y);
+  return rc;
+}
+
 // BoxMG P and Galerkin rows of level l from level l+1's operator (solvers.py:227-250):
 // P[l] and tbl[l] are rewritten in place, so captured graphs stay valid
 int boxmg_level(Engine3* e, int l) {
@@ -877,11 +911,7 @@ int boxmg_level(Engine3* e, int l) {
   CKL3();
   k3_assemble<<<nblk(c.nv), 256, 0, e->s>>>(c.tbl, Rows{c.N, nullptr, c.coef});
   CKL3();
-  if (c.N > 2) {
-    const size_t ni = (size_t)(c.N - 2) * (c.N - 2) * (c.N - 2);
-    k3_rap<<<nblk(ni, 128), 128, 0, e->s>>>(c.tbl, nc, c.P, raw);
-    CKL3();
-  }
+  if (c.N > 2) TRY3(galerkin_rows(e, l, raw));
   return refresh_pc(e, l);
 }
 

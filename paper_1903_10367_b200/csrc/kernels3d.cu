@@ -761,40 +761,4 @@ __global__ void __launch_bounds__(128) k3_cells(double* P, int nc, Rows R) {
   }
 }
 
-// Galerkin rows at interior (overlapped) coarse vertices (mg3d.galerkin):
-// loops fine offset o (125) > stencil tap s (27) > coarse neighbour dw (27),
-// fine rows masked to interior (equation) vertices.
-__global__ void __launch_bounds__(128) k3_rap(double* tbl, int nc, const double* P, Rows R) {
-  const int Nc = nc + 1, Nf = 3 * nc + 1;
-  const int n = Nc - 2;
-  const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= (size_t)n * n * n) return;
-  const int K = 1 + (int)(q % n), rr = (int)(q / n), J = 1 + rr % n, I = 1 + rr / n;
-  const size_t nvc = (size_t)Nc * Nc * Nc, vc = vid(Nc, I, J, K);
-  double out[27];
-  for (int d = 0; d < 27; ++d) out[d] = 0.0;
-  for (int o = 0; o < 125; ++o) {
-    const int oi = o / 25 - 2, oj = (o / 5) % 5 - 2, ok = o % 5 - 2;
-    const double rw = P[(size_t)o * nvc + vc];
-    if (rw == 0.0) continue;
-    const int fi = 3 * I + oi, fj = 3 * J + oj, fk = 3 * K + ok;
-    if (fi < 1 || fj < 1 || fk < 1 || fi > Nf - 2 || fj > Nf - 2 || fk > Nf - 2) continue;
-    double t[27];
-    row27(R, fi, fj, fk, t);
-    for (int s = 0; s < 27; ++s) {
-      const double ac = t[s];
-      const int ti = oi + s / 9 - 1, tj = oj + (s / 3) % 3 - 1, tk = ok + s % 3 - 1;
-      const double ra = rw * ac;
-      for (int d = 0; d < 27; ++d) {
-        const int di = d / 9 - 1, dj = (d / 3) % 3 - 1, dk = d % 3 - 1;
-        const int pi = ti - 3 * di, pj = tj - 3 * dj, pk = tk - 3 * dk;
-        if (pi < -2 || pi > 2 || pj < -2 || pj > 2 || pk < -2 || pk > 2) continue;
-        const double pw = P[(size_t)pslot(pi, pj, pk) * nvc + vid(Nc, I + di, J + dj, K + dk)];
-        out[d] = out[d] + ra * pw;
-      }
-    }
-  }
-  for (int d = 0; d < 27; ++d) tbl[(size_t)d * nvc + vc] = out[d];
-}
-
 }  // namespace t3
