@@ -30,6 +30,13 @@ CASES = {
                                 target=1e-30, engine="pipelined"),
     "pipe_skew_boxmg_additive_L3": dict(setup="skew", k=3, variant="additive", flavor="boxmg", lmax=3,
                                         max_cycles=10, target=1e-30, engine="pipelined"),
+    # dynamic refinement between cycles (amr.py, bench.py:206-219), SURVEY.md §8(f) item 3
+    "amr_poisson_jac_L4": dict(setup="poisson", variant="adafac-jac", lmax=4, amr=True, max_cycles=30,
+                               target=1e-30),
+    "amr_needle_boxmg_L5": dict(setup="needle", k=2, variant="adafac-jac", flavor="boxmg", lmax=5, amr=True,
+                                max_cycles=24, target=1e-30),
+    "amr_halfjump_additive_L4_c3": dict(setup="half-jump", k=1, variant="additive", lmax=4, amr=True,
+                                        boundary_cadence=3, decile=0.2, max_cycles=20, target=1e-30),
 }
 
 

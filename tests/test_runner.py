@@ -36,8 +36,11 @@ def test_config_validation_messages():
     runner.ExperimentConfig(engine="pipelined", variant="adafac-pi").validate()
     with pytest.raises(runner.ConfigError, match="omega"):
         runner.ExperimentConfig(omega=1.5).validate()
-    with pytest.raises(runner.ConfigError, match="amr"):
-        runner.ExperimentConfig(amr=True).validate()
+    with pytest.raises(runner.ConfigError, match="decile"):
+        runner.ExperimentConfig(amr=True, decile=1.5).validate()
+    with pytest.raises(runner.ConfigError, match="boundary_cadence"):
+        runner.ExperimentConfig(amr=True, boundary_cadence=0).validate()
+    runner.ExperimentConfig(amr=True).validate()
     assert runner.normalized_residuals(2.0, 3.0, (2.0, 3.0)) == (1.0, 1.0)
     assert runner.normalized_residuals(0.0, 0.0, (0.0, 0.0)) == (0.0, 0.0)
 
