@@ -20,6 +20,7 @@
 #include "kernels3d_updict.cu"
 #include "kernels3d_dict.cu"
 #include "kernels3d_rap.cu"
+#include "kernels3d_uplin.cu"
 
 namespace {
 
@@ -41,6 +42,7 @@ struct Lvl3 {
   size_t Tdn = 0;
   size_t Pdp = 0, Pdn = 0, Pcdp = 0, Pcdn = 0;
   double* coefp = nullptr;  // finest level: coef with rows padded to even length (TMA)
+  int crun = 1;             // ... storing one plane per run of crun equal cell planes (blockwise materials)
   double *bR = nullptr, *bT = nullptr;  // level ltop-1: restrictions from the fused fine pass
   Op3 op{};
   double w = 0.0;
@@ -337,7 +339,7 @@ bool vertex_tmap(CUtensorMap* map, const double* base, int N) {
 
 // The same for the finest level's cell coefficients, stored with rows padded
 // to an even length (coefp) so that TMA can stride them.
-bool cell_tmap(CUtensorMap* map, const double* base, int n) {
+bool cell_tmap(CUtensorMap* map, const double* base, int n, int planes) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -348,7 +350,7 @@ bool cell_tmap(CUtensorMap* map, const double* base, int n) {
   }();
   if (!encode || !base) return false;
   const cuuint64_t np = (cuuint64_t)(n + (n & 1));  // padded row length
-  const cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)n};
+  const cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)planes};
   const cuuint64_t strides[2] = {np * 8, np * n * 8};
   const cuuint32_t box[3] = {(cuuint32_t)k2RowC, (cuuint32_t)k2ColC, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
@@ -449,9 +451,9 @@ int launch_up_tma(Engine3* e, int l, const Up3& a) {
     D.I0 = A.I0;
     D.steps = (int)A.steps;
     D.per = (int)A.per;
-    if (!a.g) k3_up_dict<false, false><<<grid, kDThreads, kUpDictSmem, e->s>>>(D);
-    else if (a.carry) k3_up_dict<true><<<grid, kDThreads, kUpDictSmem, e->s>>>(D);
-    else k3_up_dict<false><<<grid, kDThreads, kUpDictSmem, e->s>>>(D);
+    if (!a.g) k3_up_dict<false, false><<<grid, kDThreads, DLay<false>::smem, e->s>>>(D);
+    else if (a.carry) k3_up_dict<true><<<grid, kDThreads, DLay<true>::smem, e->s>>>(D);
+    else k3_up_dict<false><<<grid, kDThreads, DLay<true>::smem, e->s>>>(D);
   } else {
     if (!a.g) k3_up_tma<false, false><<<grid, kQT, kUpTmaSmem, e->s>>>(A);
     else if (a.carry) k3_up_tma<true><<<grid, kQT, kUpTmaSmem, e->s>>>(A);
@@ -481,6 +483,21 @@ int launch_up_boxmg(Engine3* e, int l, const Up3& a) {
   return TMG_OK;
 }
 
+// d-linear prolongation into level l (k3_up_lin): units = (cube layer, cube row, 32-cube K tile)
+int launch_up_lin(Engine3* e, int l, const Up3& a) {
+  UpL A{};
+  A.a = a;
+  const int nc = a.Nc - 1;
+  A.tilesK = (nc + 31) / 32;
+  A.I0 = a.ilo / 3;
+  A.nI = std::max(0, std::min(nc, (a.ihi + 2) / 3) - A.I0);
+  if (A.nI == 0) return TMG_OK;
+  A.units = (long long)A.nI * nc * A.tilesK;
+  const int grid = (int)std::min<long long>(A.units, (long long)num_sms() * 7 * 8);
+  LAUNCH3(kname("k3_up", l), k3_up_lin, grid, kLThreads, A);
+  return TMG_OK;
+}
+
 // element operator with every plane through TMA: the four-rows-per-thread kernel (else k3_top2)
 bool use_top4(const Top3& a) { return a.use_tma == 2 && a.rhs_tma; }
 
@@ -502,7 +519,10 @@ Top3 make_top(Engine3* e, int l) {
   a.part_sum = e->part_sum;
   a.part_max = e->part_max;
   a.use_tma = kUseTma && vertex_tmap(&a.tm, c.u, c.N);
-  if (a.use_tma && c.op.kind == OP_ELEMENT && c.coefp && cell_tmap(&a.tmc, c.coefp, c.N - 1)) a.use_tma = 2;
+  a.crun = c.crun;
+  if (a.use_tma && c.op.kind == OP_ELEMENT && c.coefp &&
+      cell_tmap(&a.tmc, c.coefp, c.N - 1, (c.N - 1 + c.crun - 1) / c.crun))
+    a.use_tma = 2;
   // rhs through TMA as well; needs the vertex-plane TMA path
   a.rhs_tma = a.use_tma && c.rhs &&
               tmap3(&a.tmr, c.rhs, c.N, c.N, c.N, (uint64_t)c.N * 8, (uint64_t)c.N * c.N * 8, k2RowR, k2Y, 1);
@@ -558,7 +578,7 @@ int launch_smr(Engine3* e, int l, bool smooth, int clo = -1, int chi = -1) {
   const uint64_t N = (uint64_t)c.N, Nc = (uint64_t)cc.N;
   const uint64_t dp[4] = {Nc, Nc, Nc, 125}, sp[3] = {Nc * 8, Nc * Nc * 8, Nc * Nc * Nc * 8};
   const uint32_t bp[4] = {kPW, kRJ, 1, 25};
-  if (!tmap3(&A.tr, c.rho, N, N, N, N * 8, N * N * 8, kRW, kRH, 1) || !tmap4(&A.tp, cc.P, dp, sp, bp))
+  if (!tmap3(&A.tr, c.rho, N, N, N, N * 8, N * N * 8, kRW, kRH, 1) || (!cc.Pd && !tmap4(&A.tp, cc.P, dp, sp, bp)))
     return fail3(e, TMG_ECUDA, "tensor map encoding failed (k3_smr)");
   A.pd = cc.Pd;
   A.ptab = cc.Pstab;
@@ -644,7 +664,7 @@ int enqueue_cycle(Engine3* e) {
     const int g = e->L[l - 1].u_grid;
     if (pi) LAUNCH3(kname("k3_up", l), k3_up, e->L[l].grid, blk, a);
     else if (boxmg) TRY3(launch_up_boxmg(e, l, a));
-    else LAUNCH3(kname("k3_up", l), k3_up_cell<false>, g, 128, a);
+    else TRY3(launch_up_lin(e, l, a));
   }
   return TMG_OK;
 }
@@ -967,9 +987,9 @@ int build(Engine3* e, const tmg_tree3* t) {
   CK3(cudaFuncSetAttribute(k3_smooth2r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2RSmemV));
   CK3(cudaFuncSetAttribute(k3_up_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpTmaSmem));
   CK3(cudaFuncSetAttribute(k3_up_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpTmaSmem));
-  CK3(cudaFuncSetAttribute(k3_up_dict<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpDictSmem));
-  CK3(cudaFuncSetAttribute(k3_up_dict<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpDictSmem));
-  CK3(cudaFuncSetAttribute(k3_up_dict<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpDictSmem));
+  CK3(cudaFuncSetAttribute(k3_up_dict<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DLay<true>::smem));
+  CK3(cudaFuncSetAttribute(k3_up_dict<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DLay<true>::smem));
+  CK3(cudaFuncSetAttribute(k3_up_dict<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DLay<false>::smem));
   CK3(cudaFuncSetAttribute(k3_up_tma<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpTmaSmem));
   TRY3(alloc3(e, &e->deg, 1));
   e->thr_next = l0 - 1;
@@ -1017,9 +1037,35 @@ int build(Engine3* e, const tmg_tree3* t) {
     Lvl3& top = e->L[l1];
     if (top.op.kind == OP_ELEMENT) {
       const int n = top.N - 1, np = n + (n & 1);
-      TRY3(alloc3(e, &top.coefp, (size_t)n * n * np));
-      CK3(cudaMemcpy2DAsync(top.coefp, sizeof(double) * np, top.coef, sizeof(double) * n,
-                            sizeof(double) * n, (size_t)n * n, cudaMemcpyDeviceToDevice, e->s));
+      // blockwise-constant materials: the cell planes repeat along axis 0 in runs of 3^k planes
+      // (bitwise check); the top kernel then streams one stored plane per run -- at config 5 the
+      // 3.1 GB coefficient stream of every cycle becomes 27 L2-resident planes
+      top.crun = 1;
+      {
+        int* flag;
+        TRY3(alloc3(e, &flag, 1, false));
+        for (int run = 27; run >= 3 && top.crun == 1; run /= 3) {
+          if (n % run) continue;
+          const int one = 1;
+          int hf = 0;
+          CK3(cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, e->s));
+          k3_plane_run_check<<<nblk(top.ncell), 256, 0, e->s>>>(top.coef, n, run, flag);
+          CKL3();
+          CK3(cudaMemcpyAsync(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost, e->s));
+          CK3(cudaStreamSynchronize(e->s));
+          if (hf) top.crun = run;
+        }
+      }
+      const int planes = n / top.crun;
+      TRY3(alloc3(e, &top.coefp, (size_t)planes * n * np));
+      if (top.crun == 1)
+        CK3(cudaMemcpy2DAsync(top.coefp, sizeof(double) * np, top.coef, sizeof(double) * n, sizeof(double) * n,
+                              (size_t)n * n, cudaMemcpyDeviceToDevice, e->s));
+      else
+        for (int pl = 0; pl < planes; ++pl)
+          CK3(cudaMemcpy2DAsync(top.coefp + (size_t)pl * n * np, sizeof(double) * np,
+                                top.coef + (size_t)pl * top.crun * n * n, sizeof(double) * n, sizeof(double) * n,
+                                (size_t)n, cudaMemcpyDeviceToDevice, e->s));
     }
   }
   TRY3(check_degenerate(e));
@@ -1097,9 +1143,32 @@ int build(Engine3* e, const tmg_tree3* t) {
   }
   // finest-level smoothing + restriction fused (k3_smr; else k3_smooth2r + k3_down_c)
   {
-    e->smr = cfg.flavor == TMG_BOXMG && cfg.variant != VAR_PI &&
-             l1 - 1 > e->lc;
+    e->smr = cfg.variant != VAR_PI && l1 - 1 > e->lc;
     e->smr_lo = e->lc + 2;  // every level whose coarser level is a grid (not chain) level
+    if (e->smr && cfg.flavor == TMG_GEOMETRIC) {
+      // d-linear transfer: one constant weight row for every interior coarse vertex (its fine
+      // offsets +-2 never leave the grid), so k3_smr's dictionary variant runs on a one-row
+      // dictionary and tile-plane tables that all name row 0
+      double row[kDictW] = {0.0};
+      for (int a = -2; a <= 2; ++a)
+        for (int b = -2; b <= 2; ++b)
+          for (int c2 = -2; c2 <= 2; ++c2) {
+            const double wa = 1.0 - std::abs(a) / 3.0, wb = 1.0 - std::abs(b) / 3.0, wc = 1.0 - std::abs(c2) / 3.0;
+            row[pslot(a, b, c2)] = (wa * wb) * wc;  // k3_p_dlinear / mg3d.dlinear_p_table
+          }
+      for (int l = e->smr_lo - 1; l < l1; ++l) {
+        Lvl3& cc = e->L[l];
+        TRY3(alloc3(e, &cc.Pd, kDictW, false));
+        CK3(cudaMemcpyAsync(cc.Pd, row, sizeof(row), cudaMemcpyHostToDevice, e->s));
+        CK3(cudaStreamSynchronize(e->s));
+        cc.Pdn = 1;
+        const int n = cc.N - 2, tK = (n + kRK - 1) / kRK, tJ = (n + kRJ - 1) / kRJ;
+        const size_t cnt = (size_t)n * tJ * tK;
+        TRY3(alloc3(e, &cc.Pstab, cnt * kRTabBytes, false));
+        k3_smr_tables_one<<<nblk(cnt, 128), 128, 0, e->s>>>(cc.Pstab, cnt);
+        CKL3();
+      }
+    }
     if (e->smr) {
       CK3(cudaFuncSetAttribute(k3_smr<false, 1, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmem));
       CK3(cudaFuncSetAttribute(k3_smr<true, 1, 7, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmemDB));
@@ -1292,7 +1361,7 @@ int phase3(Engine3* e, int phase, int l) {
         const dim3 blk(kTX, kTY, kTZ);
         LAUNCH3(kname("k3_up", l), k3_up, e->L[l].grid, blk, a);
       } else if (boxmg) TRY3(launch_up_boxmg(e, l, a));
-      else LAUNCH3(kname("k3_up", l), k3_up_cell<false>, g, 128, a);
+      else TRY3(launch_up_lin(e, l, a));
       return TMG_OK;
     }
     case TMG_PH_INJECT: {

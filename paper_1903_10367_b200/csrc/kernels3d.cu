@@ -475,6 +475,19 @@ __global__ void k3_const_check(const double* arr, size_t n, int* flag) {
   if (__ballot_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicAnd(flag, 0);
 }
 
+// flag stays 1 iff every cell plane ci equals plane ci - ci % run bit for bit (coefficients constant
+// along axis 0 in runs of `run` planes: blockwise-constant materials)
+__global__ void k3_plane_run_check(const double* arr, int n, int run, int* flag) {
+  const size_t plane = (size_t)n * n, cnt = plane * n;
+  const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool bad = false;
+  if (c < cnt) {
+    const size_t ci = c / plane, base = ci - ci % run;
+    bad = ci != base && __double_as_longlong(arr[c]) != __double_as_longlong(arr[base * plane + (c - ci * plane)]);
+  }
+  if (__ballot_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicAnd(flag, 0);
+}
+
 // Source of fine 27-point rows: a stored table, or assembled on the fly from
 // the per-cell coefficients (mg3d.assemble_table order: corner a outer, b inner).
 struct Rows {

@@ -38,6 +38,7 @@ struct Top3 {
   CUtensorMap tmr;         // 3D map of rhs (box 34 x 16 x 1 from k0 - 1: the column's rows), used when rhs_tma
   int rhs_tma;
   int use_tma;
+  int crun;                // cell plane ci is stored as plane ci / crun of tmc's array (1: every plane stored)
   int N, ilo, ihi, chunk;  // planes [ilo, ihi) split in chunks
   const double* u;
   const double* rhs;
@@ -321,7 +322,7 @@ __device__ __forceinline__ void stream25x2(const Column2& col, const double* x, 
                                            double (*us)[k2SlotU], double (*cs)[k2SlotC],
                                            const CUtensorMap* tm, uint64_t* bars, Body&& body,
                                            const CUtensorMap* tmc = nullptr, const CUtensorMap* tmr = nullptr,
-                                           double (*rs)[k2SlotR] = nullptr) {
+                                           double (*rs)[k2SlotR] = nullptr, int crun = 1) {
   const int ia = col.ia, ib = col.ib;
   if (tm && col.lt == 0) {
     for (int q = 0; q < S; ++q) mbar_init(&bars[q], 1);
@@ -334,7 +335,8 @@ __device__ __forceinline__ void stream25x2(const Column2& col, const double* x, 
       if (col.lt == 0) {
         mbar_expect_tx(&bars[slot], k2BoxBytes + (ctma ? k2BoxBytesC : 0u) + (tmr ? 8u * k2SlotR : 0u));
         tma_load_3d(us[slot], tm, &bars[slot], col.k0 - 1, col.j0 - 1, ia - 1 + g);
-        if (ctma) tma_load_3d(cs[slot], tmc, &bars[slot], col.k0 - 1, col.j0 - 1, ia - 1 + g);
+        // (ia - 1 + g >= 0; the plane past the last one stays out of bounds after the division)
+        if (ctma) tma_load_3d(cs[slot], tmc, &bars[slot], col.k0 - 1, col.j0 - 1, (ia - 1 + g) / crun);
         if (tmr) tma_load_3d(rs[slot], tmr, &bars[slot], col.k0 - 1, col.j0, ia - 1 + g);
       }
     } else {
@@ -581,7 +583,7 @@ __global__ void __launch_bounds__(kSB, 3) k3_top2(const __grid_constant__ Top3 a
           if (a.rho) a.rho[v + N] = rho1;
         }
       },
-      tmc, a.rhs_tma ? &a.tmr : nullptr, rs);
+      tmc, a.rhs_tma ? &a.tmr : nullptr, rs, a.crun);
   __shared__ double red_s[kSB / 32], red_m[kSB / 32];
   for (int o = 16; o > 0; o >>= 1) {
     s += __shfl_down_sync(0xffffffffu, s, o);

@@ -135,6 +135,17 @@ __global__ void k3_smr_tables(const uint32_t* __restrict__ ids, int Nc, int Ncp,
   }
 }
 
+// the same tables when every vertex uses dictionary row 0 (the d-linear flavour: one constant row)
+__global__ void k3_smr_tables_one(uint8_t* __restrict__ tab, size_t cnt) {
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += (size_t)gridDim.x * blockDim.x) {
+    uint32_t* T = reinterpret_cast<uint32_t*>(tab + t * kRTabBytes);
+    T[0] = 1u;
+    for (int q = 0; q < kRRows; ++q) T[1 + q] = 0u;
+    for (int c = 0; c < kRK * kRJ; ++c) tab[t * kRTabBytes + kRTabLoc + c] = 0;
+    for (int c = kRTabLoc + kRK * kRJ; c < kRTabBytes; ++c) tab[t * kRTabBytes + c] = 0;
+  }
+}
+
 struct Smr {
   CUtensorMap tr;  // rho of the finest level, box {100, 16, 1}
   CUtensorMap tp;  // P of level ltop-1 as {Nc, Nc, Nc, 125}, box {34, 4, 1, 25}

@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kT4B, 3) k3_top4(const __grid_constant__ Top3 
           if (a.rho) a.rho[v] = rho;
         }
       },
-      &a.tmc, &a.tmr, rs);
+      &a.tmc, &a.tmr, rs, a.crun);
   __shared__ double red_s[kT4B / 32], red_m[kT4B / 32];
   for (int o = 16; o > 0; o >>= 1) {
     s += __shfl_down_sync(0xffffffffu, s, o);

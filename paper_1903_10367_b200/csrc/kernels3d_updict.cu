@@ -28,14 +28,43 @@ namespace t3 {
 
 constexpr int kQRows = 32, kQRowS = 130;  // rows per step (cap), row stride in doubles (1040 B)
 constexpr int kQTabBytes = 256;           // {n, ids[kQRows]} uint32, local[64] uint8 at byte 132
-constexpr int oDU = 0, oDG = qal16(kQUd), oDC = oDG + qal16(kQUd);
-constexpr int kDSlot = oDC + qal16(kQCd);
-constexpr int kDNS = 3, kDNT = 8, kDTD = 6, kDNR = 4, kDRD = 3, kDPF = 4;
+constexpr int kDNT = 8, kDTD = 6, kDNR = 4, kDRD = 3, kDPF = 4;
 static_assert(kDNR == kDRD + 1, "row sets: one per step in flight plus the one being staged");
-constexpr int kDCons = 6 * 32, kDThreads = kDCons + 64;  // consumers + two producer warps
-constexpr int oDTab = kDNS * kDSlot, oDRows = oDTab + kDNT * kQTabBytes / 8, kDRowSlot = kQRows * kQRowS;
-constexpr size_t kUpDictSmem = sizeof(double) * (oDRows + kDNR * kDRowSlot);
-constexpr unsigned kDBytes = (unsigned)sizeof(double) * (2 * kQUd + kQCd);
+// consumers: 18 warps = the nine fine rows (ri, rj) of a cube on two warps each (64 cubes), three
+// fine vertices per thread -- with 6 warps (a cube's fine plane per thread) the consumers were busy
+// two thirds of the time and set the step rate
+constexpr int kDCons = 18 * 32, kDThreads = kDCons + 64;  // consumers + two producer warps
+// index of the first stored term of fine row (ri, rj) in a cube's row (cube_terms order)
+__host__ __device__ constexpr int cube_row_q0(int ri, int rj) {
+  int q = 0;
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      if (a == ri && b == rj) return q;
+      for (int c = 0; c < 3; ++c)
+        for (int d = 7; d >= 0; --d) {
+          const int di = (d >> 2) & 1, dj = (d >> 1) & 1, dk = d & 1;
+          if ((di && !a) || (dj && !b) || (dk && !c)) continue;
+          if (pslot(a - 3 * di, b - 3 * dj, c - 3 * dk) == 62) continue;
+          ++q;
+        }
+    }
+  return q;
+}
+constexpr int kDRowSlot = kQRows * kQRowS;
+// shared-memory layout: NS slots {u, (g,) carry}, the table ring, the row-set ring.  Without the g
+// stream (the finest level's g lives in its double-buffered u) a slot is half the size (five slots
+// in flight instead of three measured no faster: the consumers, not the loads, set the pace).
+template <bool G>
+struct DLay {
+  static constexpr int oU = 0, oG = qal16(kQUd), oC = G ? 2 * qal16(kQUd) : qal16(kQUd);
+  static constexpr int slot = oC + qal16(kQCd);
+  static constexpr int NS = 3;
+  static constexpr int oTab = NS * slot, oRows = oTab + kDNT * kQTabBytes / 8;
+  static constexpr size_t smem = sizeof(double) * (oRows + kDNR * kDRowSlot);
+  static constexpr unsigned bytes = (unsigned)sizeof(double) * ((G ? 2 : 1) * kQUd + kQCd);
+  static_assert(smem + 1024 <= 227 * 1024, "k3_up_dict exceeds shared memory");
+};
+constexpr int kDNSMax = 5;
 constexpr unsigned kDRowBytes = (unsigned)sizeof(double) * kQS;  // 992 of a row's 1 KB
 
 struct UpD {
@@ -117,8 +146,12 @@ __device__ __forceinline__ void tma_store_3d_ef(const CUtensorMap* map, const vo
 // G = false: no g stream (the finest level's g is already in u, Engine3::pp)
 template <bool CARRY, bool G = true>
 __global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant__ UpD A) {
+  using LY = DLay<G>;
+  constexpr int kDNS = LY::NS, kDSlot = LY::slot, oDU = LY::oU, oDG = LY::oG, oDC = LY::oC, oDTab = LY::oTab,
+                oDRows = LY::oRows;
+  constexpr unsigned kDBytes = LY::bytes;
   extern __shared__ __align__(128) double sq[];
-  __shared__ __align__(8) uint64_t full[kDNS], done[kDNS], tful[kDNT], rful[kDNR];
+  __shared__ __align__(8) uint64_t full[kDNSMax], done[kDNSMax], tful[kDNT], rful[kDNR];
   __shared__ int rsl[kDNR];  // row slot of the step whose barrier is rful[same index]
   const Up3& a = A.a;
   const int Nc = a.Nc, nc = Nc - 1, N = a.N;
@@ -157,7 +190,7 @@ __global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant
       const int r = s - s0;
       double* b = sq + (r % kDNS) * kDSlot;
       uint64_t* br = &full[r % kDNS];
-      mbar_expect_tx(br, kDBytes - (G ? 0u : (unsigned)sizeof(double) * kQUd));
+      mbar_expect_tx(br, kDBytes);
       if (G) tma_load_3d_ef(b + oDG, &A.tg, br, 3 * K0, 3 * J0, 3 * I, pol);
       tma_load_3d(b + oDC, &A.tc, br, K0, J0, I);
       tma_load_3d_ef(b + oDU, &A.tu, br, 3 * K0, 3 * J0, 3 * I, pol);
@@ -245,7 +278,7 @@ __global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant
     return;
   }
 
-  // ---------------- consumers: warps 0-5, cube plane ri = warp / 2 ----------------
+  // ---------------- consumers: warps 0-17, fine row (ri, rj) = warp / 2 ----------------
   const int rg = lt >> 6, cl = lt & 63, tx = cl & 31, ty = cl >> 5;
   int I, J0, K0;  // coordinates of step s, advanced incrementally
   coords(s0, I, J0, K0);
@@ -269,57 +302,68 @@ __global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant
       const double* Gs = b + oDG;
       const double* Cs = b + oDC;
       double* Us = b + oDU;
-      double c[2][2][2];
+      auto run = [&](auto R0, auto R1) {  // fine row (ri, rj) of the cube
+        constexpr int ri = decltype(R0)::value, rj = decltype(R1)::value;
+        double c[2][2][2];
 #pragma unroll
-      for (int di = 0; di < 2; ++di)
+        for (int di = 0; di < 2; ++di)
 #pragma unroll
-        for (int dj = 0; dj < 2; ++dj)
+          for (int dj = 0; dj < 2; ++dj)
 #pragma unroll
-          for (int dk = 0; dk < 2; ++dk) c[di][dj][dk] = Cs[(di * kQCJ + ty + dj) * kQCK + tx + dk];
-      auto run = [&](auto R0) {  // fine plane ri of the cube; q = its first stored term
-        constexpr int ri = decltype(R0)::value;
-        int q = ri == 0 ? 0 : ri == 1 ? 24 : 74;
-#pragma unroll
-        for (int rj = 0; rj < 3; ++rj)
-#pragma unroll
-          for (int rk = 0; rk < 3; ++rk) {
-            double acc = 0.0;
-#pragma unroll
-            for (int d = 7; d >= 0; --d) {
-              const int di = (d >> 2) & 1, dj = (d >> 1) & 1, dk = d & 1;
-              if ((di && !ri) || (dj && !rj) || (dk && !rk)) continue;
-              const int sl = pslot(ri - 3 * di, rj - 3 * dj, rk - 3 * dk);
-              double wt = 1.0;
-              if (sl != 62) {
-                wt = Wd[q];
-                ++q;
-              }
-              acc = acc + wt * c[di][dj][dk];
+            for (int dk = 0; dk < 2; ++dk) {
+              c[di][dj][dk] = 0.0;
+              if ((di && !ri) || (dj && !rj)) continue;
+              c[di][dj][dk] = Cs[(di * kQCJ + ty + dj) * kQCK + tx + dk];
             }
-            const int i = 3 * I + ri;  // fine planes outside [ilo, ihi) stay as loaded
-            const bool skip = i < a.ilo || i >= a.ihi || (rj == 0 && J == 0) || (rk == 0 && K == 0);
-            if (!skip) {
-              const int o = (ri * kQFJ + 3 * ty + rj) * kQFK + 3 * tx + rk;
-              const double cv = G ? acc + Gs[o] : acc;
-              const double un = Us[o] + cv;
-              Us[o] = un;
-              if (CARRY) a.carry[vid(N, i, 3 * J + rj, 3 * K + rk)] = cv;
-              if (ri == 0 && rj == 0 && rk == 0) {  // FAS walk-down injection
-                int ii = I, jj = J, kk = K;
-                for (int lc = a.l - 1; lc >= a.l0; --lc) {
-                  a.ul[lc][vid(a.Nl[lc], ii, jj, kk)] = un;
-                  if (ii % 3 || jj % 3 || kk % 3) break;
-                  ii /= 3;
-                  jj /= 3;
-                  kk /= 3;
-                }
+        int q = cube_row_q0(ri, rj);
+#pragma unroll
+        for (int rk = 0; rk < 3; ++rk) {
+          double acc = 0.0;
+#pragma unroll
+          for (int d = 7; d >= 0; --d) {
+            const int di = (d >> 2) & 1, dj = (d >> 1) & 1, dk = d & 1;
+            if ((di && !ri) || (dj && !rj) || (dk && !rk)) continue;
+            const int sl = pslot(ri - 3 * di, rj - 3 * dj, rk - 3 * dk);
+            double wt = 1.0;
+            if (sl != 62) {
+              wt = Wd[q];
+              ++q;
+            }
+            acc = acc + wt * c[di][dj][dk];
+          }
+          const int i = 3 * I + ri;  // fine planes outside [ilo, ihi) stay as loaded
+          const bool skip = i < a.ilo || i >= a.ihi || (rj == 0 && J == 0) || (rk == 0 && K == 0);
+          if (!skip) {
+            const int o = (ri * kQFJ + 3 * ty + rj) * kQFK + 3 * tx + rk;
+            const double cv = G ? acc + Gs[o] : acc;
+            const double un = Us[o] + cv;
+            Us[o] = un;
+            if (CARRY) a.carry[vid(N, i, 3 * J + rj, 3 * K + rk)] = cv;
+            if (ri == 0 && rj == 0 && rk == 0) {  // FAS walk-down injection
+              int ii = I, jj = J, kk = K;
+              for (int lc = a.l - 1; lc >= a.l0; --lc) {
+                a.ul[lc][vid(a.Nl[lc], ii, jj, kk)] = un;
+                if (ii % 3 || jj % 3 || kk % 3) break;
+                ii /= 3;
+                jj /= 3;
+                kk /= 3;
               }
             }
           }
+        }
       };
-      if (rg == 0) run(std::integral_constant<int, 0>{});
-      else if (rg == 1) run(std::integral_constant<int, 1>{});
-      else run(std::integral_constant<int, 2>{});
+      using std::integral_constant;
+      switch (rg) {
+        case 0: run(integral_constant<int, 0>{}, integral_constant<int, 0>{}); break;
+        case 1: run(integral_constant<int, 0>{}, integral_constant<int, 1>{}); break;
+        case 2: run(integral_constant<int, 0>{}, integral_constant<int, 2>{}); break;
+        case 3: run(integral_constant<int, 1>{}, integral_constant<int, 0>{}); break;
+        case 4: run(integral_constant<int, 1>{}, integral_constant<int, 1>{}); break;
+        case 5: run(integral_constant<int, 1>{}, integral_constant<int, 2>{}); break;
+        case 6: run(integral_constant<int, 2>{}, integral_constant<int, 0>{}); break;
+        case 7: run(integral_constant<int, 2>{}, integral_constant<int, 1>{}); break;
+        default: run(integral_constant<int, 2>{}, integral_constant<int, 2>{}); break;
+      }
     }
     fence_proxy_async();  // this thread's generic-proxy writes of u, before the async-proxy store
     __syncwarp();
