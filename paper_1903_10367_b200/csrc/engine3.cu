@@ -16,7 +16,7 @@
 #include "kernels3d_fast.cu"
 #include "kernels3d_upq.cu"
 #include "kernels3d_smr.cu"
-#include "kernels3d_top4.cu"
+#include "kernels3d_top4r.cu"
 #include "kernels3d_updict.cu"
 #include "kernels3d_dict.cu"
 #include "kernels3d_rap.cu"
@@ -498,9 +498,8 @@ int launch_up_lin(Engine3* e, int l, const Up3& a) {
   return TMG_OK;
 }
 
-// element operator with every plane through TMA: the four-rows-per-thread kernel (else k3_top2)
+// element operator with every plane through TMA: the register-window kernel k3_top4r (else k3_top2)
 bool use_top4(const Top3& a) { return a.use_tma == 2 && a.rhs_tma; }
-
 Top3 make_top(Engine3* e, int l) {
   Lvl3& c = e->L[l];
   Top3 a{};
@@ -605,7 +604,7 @@ int enqueue_down(Engine3* e, bool write) {
       cudaEvent_t e0_ = nullptr;
       TRY3(begin_k(e, &e0_));
       if (c.op.kind == OP_CONST) k3_top2<OP_CONST><<<c.s2_blocks, dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
-      else if (use_top4(a)) k3_top4<<<c.s2_blocks, dim3(kT4X, kT4Y), k2TopSmem, e->s>>>(a);
+      else if (use_top4(a)) k3_top4r<<<c.s2_blocks, dim3(kSX, k2Y / kT4R), kTop4rSmem, e->s>>>(a);
       else k3_top2<OP_ELEMENT><<<c.s2_blocks, dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
       CKL3();
       TRY3(end_k(e, kname("k3_down", l), e0_));
@@ -983,7 +982,7 @@ int build(Engine3* e, const tmg_tree3* t) {
   }
   CK3(cudaFuncSetAttribute(k3_top2<OP_CONST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2TopSmem));
   CK3(cudaFuncSetAttribute(k3_top2<OP_ELEMENT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2TopSmem));
-  CK3(cudaFuncSetAttribute(k3_top4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2TopSmem));
+  CK3(cudaFuncSetAttribute(k3_top4r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTop4rSmem));
   CK3(cudaFuncSetAttribute(k3_smooth2r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2RSmemV));
   CK3(cudaFuncSetAttribute(k3_up_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpTmaSmem));
   CK3(cudaFuncSetAttribute(k3_up_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpTmaSmem));
@@ -1108,11 +1107,13 @@ int build(Engine3* e, const tmg_tree3* t) {
         const int t2 = ((c.N - 2 + kSX - 1) / kSX) * ((c.N - 2 + k2Y - 1) / k2Y);
         int n2 = (148 * 12 + t2 - 1) / t2;
         n2 = std::max(1, std::min(n2, std::max(1, (c.N - 2) / 4)));
-        if (t2 >= 148 * 3) {  // tiles fill a wave of 3 CTAs per SM: chunks by wave efficiency x halo
+        // CTAs per SM of the level's streaming kernel: k3_top4r (element operator) 2, k3_top2 3
+        const int slots = num_sms() * ((l == l1 && c.op.kind == OP_ELEMENT) ? 2 : 3);
+        if (t2 >= slots) {  // tiles fill a wave: chunks by wave efficiency x halo
           double best_eff = 0.0;
           for (int nch = 1; nch <= 8; ++nch) {
             const int ch = (c.N - 2 + nch - 1) / nch, nb = t2 * ((c.N - 2 + ch - 1) / ch);
-            const double waves = (double)nb / (148 * 3);
+            const double waves = (double)nb / slots;
             const double eff = waves / std::ceil(waves) * (double)ch / (ch + 2.0);
             if (eff > best_eff + 1e-9) { best_eff = eff; n2 = nch; }
           }
@@ -1260,7 +1261,7 @@ int phase3(Engine3* e, int phase, int l) {
         if (c.op.kind == OP_CONST)
           k3_top2<OP_CONST><<<e->own_blocks2[l], dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
         else if (use_top4(a))
-          k3_top4<<<e->own_blocks2[l], dim3(kT4X, kT4Y), k2TopSmem, e->s>>>(a);
+          k3_top4r<<<e->own_blocks2[l], dim3(kSX, k2Y / kT4R), kTop4rSmem, e->s>>>(a);
         else
           k3_top2<OP_ELEMENT><<<e->own_blocks2[l], dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
         CKL3();
