@@ -602,8 +602,12 @@ def run_sharded(args, dist: Dist):
     se = sharding.ShardedEngine3([sh], sharding.DistTransport(pl, dist.rank), wl.variant)
     st = sh.stream
     with torch.cuda.stream(st):
+        se.cycle()  # eager once (NCCL channels, lazily allocated buffers), then the captured graphs
+        torch.cuda.synchronize()
+        graphed = (not args.no_shard_graph) and se.capture()
+        step = se.replay if graphed else se.cycle
         for _ in range(max(args.warmup, 3)):
-            se.cycle()
+            step()
         torch.cuda.synchronize()
         clk = ClockSampler(dev)
         clk.start()
@@ -613,7 +617,7 @@ def run_sharded(args, dist: Dist):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(st)
         for _ in range(args.steps):
-            se.cycle()
+            step()
         e1.record(st)
         torch.cuda.synchronize()
         dist.barrier()
@@ -622,20 +626,21 @@ def run_sharded(args, dist: Dist):
         hist = sh.history(1)
         # e2e: every step uploads this rank's owned u planes (all sharded levels) from
         # pinned host memory, runs one cycle and reads them back with the stats
-        views = {l: sh.view(0, l) for l in range(pl.ls, wl.ltop + 1)}
-        host = {l: torch.empty_like(views[l][slice(*pl.rng(l, dist.rank))], device="cpu").pin_memory()
-                for l in views}
-        for l in views:
-            host[l].copy_(views[l][slice(*pl.rng(l, dist.rank))])
+        # (the finest level's u is double buffered: ask for its current view every time)
+        levels = range(pl.ls, wl.ltop + 1)
+        own = {l: slice(*pl.rng(l, dist.rank)) for l in levels}
+        host = {l: torch.empty_like(sh.view(0, l)[own[l]], device="cpu").pin_memory() for l in levels}
+        for l in levels:
+            host[l].copy_(sh.view(0, l)[own[l]])
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            for l in views:
-                views[l][slice(*pl.rng(l, dist.rank))].copy_(host[l], non_blocking=True)
-            se.cycle()
-            for l in views:
-                host[l].copy_(views[l][slice(*pl.rng(l, dist.rank))], non_blocking=True)
+            for l in levels:
+                sh.view(0, l)[own[l]].copy_(host[l], non_blocking=True)
+            step()
+            for l in levels:
+                host[l].copy_(sh.view(0, l)[own[l]], non_blocking=True)
             sh.history(1)
         torch.cuda.synchronize()
         t_e2e = dist.max(time.perf_counter() - t0)
@@ -658,7 +663,7 @@ def run_sharded(args, dist: Dist):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, SURVEY.md §8(d))",
             "config": config_of(wl, dist.ws, sharded=True),
-            "detail": {"l2h_last": hist[0].l2h},
+            "detail": {"l2h_last": hist[0].l2h, "cuda_graph": bool(graphed)},
             "roofline": {"bound": "hbm", "kernel": "cycle (per GPU)", "achieved": per_gpu, "peak": peak,
                          "unit": "GB/s", "frac": per_gpu / peak, "traffic": None,
                          "cycle_B_alg": bm["cycle"]},
@@ -671,7 +676,8 @@ def run_sharded(args, dist: Dist):
         print(json.dumps(line), flush=True)
     # release every torch object tied to the engine's stream before the engine (and its
     # stream) goes away: pinned blocks record events on the streams that used them
-    del host, views
+    del host
+    se._graphs = None
     sh.close()
     torch.cuda.synchronize()
     eng.close()
@@ -691,6 +697,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-1e-8 run")
     ap.add_argument("--ttt-cap", type=int, default=200, help="cycle cap of the time-to-1e-8 run")
+    ap.add_argument("--no-shard-graph", action="store_true",
+                    help="sharded path: enqueue every phase and exchange from the host instead of replaying "
+                         "the captured CUDA graphs")
     ap.add_argument("--force-shard", action="store_true",
                     help="3D: run the sharded (NCCL) path even on one rank (testing)")
     args = ap.parse_args()

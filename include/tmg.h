@@ -120,6 +120,8 @@ int tmg_dim(tmg_handle* h);
 
 /* ---- multi-GPU slab sharding of a 3D handle ----
  * Every rank builds the full hierarchy (setup is redundant, cycles are not);
+ * the finest level stays double buffered (TMG_F_U of the finest level names the
+ * current buffer, which alternates every cycle: query it after TMG_PH_UP);
  * tmg3_shard restricts the cycle of levels >= ls to the vertex planes
  * [lo[l], hi[l]) (axis 0, the slowest) this rank owns; levels < ls are
  * replicated.  The host (paper_1903_10367_b200/sharding.py) runs the cycle
@@ -160,6 +162,13 @@ int tmg3_storage(tmg_handle* h, int32_t level, int64_t* out);
 int tmg3_stream(tmg_handle* h, uint64_t* stream);
 /* the last `count` per-cycle residual stats of a sharded run */
 int tmg3_history(tmg_handle* h, int32_t count, tmg_stats* out);
+/* Host-side state of a sharded handle: the number of cycles enqueued so far (which slots
+ * tmg3_history reads) and which buffer of the finest level's double-buffered u is current.
+ * set = 0 reads it, set = 1 writes it: the host that captures the phases + exchanges of a cycle
+ * into CUDA graphs on the handle's stream (sharding.py: ShardedEngine3.capture / replay)
+ * restores the state after the capture (captured cycles do not run) and advances it after
+ * every replay. */
+int tmg3_cycle_state(tmg_handle* h, int64_t* count, int32_t* parity, int32_t set);
 
 /* ReferenceEngine.rebuild() after a mesh / material change (solvers.py:145-255):
  * rebuilds every operator from the new tree and re-uploads u. rhs is kept. */

@@ -28,7 +28,7 @@ EXPORTS = ("tmg_create", "tmg_rebuild", "tmg_set_rhs", "tmg_set_u", "tmg_get_u",
            "tmg_level_counts", "tmg_get_kinds", "tmg_get_table", "tmg_time_cycles",
            "tmg_profile_cycles", "tmg_launches_per_cycle", "tmg_destroy", "tmg_last_error",
            "tmg_device_count", "tmg3_create", "tmg3_rebuild", "tmg_dim", "tmg3_shard", "tmg3_phase",
-           "tmg3_field", "tmg3_stream", "tmg3_history", "tmg3_storage", "tmg3_fused")
+           "tmg3_field", "tmg3_stream", "tmg3_history", "tmg3_storage", "tmg3_fused", "tmg3_cycle_state")
 
 
 class Config(C.Structure):
@@ -98,6 +98,7 @@ def lib() -> C.CDLL:
         "tmg3_storage": ([H, C.c_int32, P(C.c_int64)], C.c_int),
         "tmg3_fused": ([H, C.c_int32, P(C.c_int32)], C.c_int),
         "tmg3_history": ([H, C.c_int32, C.c_void_p], C.c_int),
+        "tmg3_cycle_state": ([H, P(C.c_int64), P(C.c_int32), C.c_int32], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -861,6 +861,12 @@ int tmg3_history(tmg_handle* h, int32_t count, tmg_stats* out) {
   return e3_history(h->e3, count, out, g_err);
 }
 
+int tmg3_cycle_state(tmg_handle* h, int64_t* count, int32_t* parity, int32_t set) {
+  DeviceGuard dg_(h);
+  if (!h || !h->e3 || !count || !parity) return fail(TMG_EINVAL, "null argument or not a 3D handle");
+  return e3_cycle_state(h->e3, count, parity, set, g_err);
+}
+
 int tmg_rebuild(tmg_handle* h, const tmg_tree* tree) {
   DeviceGuard dg_(h);
   if (h && h->e3) return fail(TMG_EINVAL, "3D handle: use tmg3_rebuild");

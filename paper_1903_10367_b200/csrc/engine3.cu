@@ -1363,6 +1363,7 @@ int phase3(Engine3* e, int phase, int l) {
         LAUNCH3(kname("k3_up", l), k3_up, e->L[l].grid, blk, a);
       } else if (boxmg) TRY3(launch_up_boxmg(e, l, a));
       else TRY3(launch_up_lin(e, l, a));
+      if (l == e->ltop) pp_advance(e);  // the buffer just completed is the iterate (TMG_F_U names it)
       return TMG_OK;
     }
     case TMG_PH_INJECT: {
@@ -1384,10 +1385,6 @@ int phase3(Engine3* e, int phase, int l) {
 
 int e3_shard(Engine3* e, int ls, const int32_t* lo, const int32_t* hi, std::string& err) {
   ErrScope es(e, err);
-  if (e->pp) {  // sharded runs use the phase kernels with g on the current buffer
-    e->pp = false;
-    e->graph_dirty = true;
-  }
   if (ls <= e->lmin || ls > e->ltop) return fail3(e, TMG_EINVAL, "shard level must lie in (lmin, ltop]");
   e->own_lo.assign(e->ltop + 1, 0);
   e->own_hi.assign(e->ltop + 1, 0);
@@ -1484,6 +1481,20 @@ int e3_history(Engine3* e, int count, tmg_stats* out, std::string& err) {
   ErrScope es(e, err);
   if (count < 0 || count > e->cap || count > e->host_counter) return fail3(e, TMG_EINVAL, "bad history count");
   return read_stats(e, e->host_counter - count, count, out);
+}
+
+int e3_cycle_state(Engine3* e, int64_t* count, int32_t* parity, int set, std::string& err) {
+  ErrScope es(e, err);
+  if (!e->sharded) return fail3(e, TMG_EINVAL, "handle is not sharded (tmg3_shard)");
+  if (!set) {
+    *count = e->host_counter;
+    *parity = e->par;
+    return TMG_OK;
+  }
+  if (*count < 0 || (*parity != 0 && *parity != 1)) return fail3(e, TMG_EINVAL, "bad cycle state");
+  e->host_counter = *count;
+  if (e->pp && *parity != e->par) pp_advance(e);
+  return TMG_OK;
 }
 
 // one cycle from the graph of the current state (+ the fused-pass state machine)

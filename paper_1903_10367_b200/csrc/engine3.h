@@ -35,3 +35,4 @@ int e3_storage(Engine3* e, int level, int64_t* out, std::string& err);
 int e3_fused(Engine3* e, int level, int32_t* out, std::string& err);
 int e3_stream(Engine3* e, uint64_t* s);
 int e3_history(Engine3* e, int count, tmg_stats* out, std::string& err);
+int e3_cycle_state(Engine3* e, int64_t* count, int32_t* parity, int set, std::string& err);

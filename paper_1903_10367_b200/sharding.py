@@ -233,7 +233,8 @@ class GpuShard:
         self._views = {}
 
     def view(self, field: int, level: int):
-        key = (field, level)
+        # the finest level's u is double buffered: its current buffer alternates every cycle
+        key = (field, level, self.state()[1] if field == _abi.F_U and level == self.eng.ltop else 0)
         if key not in self._views:
             import ctypes as C
             import torch
@@ -249,6 +250,15 @@ class GpuShard:
 
     def phase(self, ph: int, level: int = 0) -> None:
         _abi.check(_abi.lib().tmg3_phase(self.eng._h, ph, level))
+
+    def state(self, new=None):
+        """(cycles enqueued, parity of the finest level's double buffer); ``new`` sets it."""
+        import ctypes as C
+        c, p = C.c_int64(), C.c_int32()
+        if new is not None:
+            c.value, p.value = new
+        _abi.check(_abi.lib().tmg3_cycle_state(self.eng._h, C.byref(c), C.byref(p), 0 if new is None else 1))
+        return c.value, p.value
 
     def fused(self, level: int) -> bool:
         """Whether the engine runs level's smoothing fused with the restriction (PH_SMR)."""
@@ -281,6 +291,7 @@ class ShardedEngine3:
         self.jac = variant == "adafac-jac"
         self.lmin = lmin
         self._fz = {}
+        self._graphs = None
 
     def _views(self, field, level):
         return [s.view(field, level) for s in self.shards]
@@ -336,6 +347,42 @@ class ShardedEngine3:
         for _ in range(n):
             self.cycle()
         return self.shards[0].history(n)
+
+    # -- the cycle as CUDA graphs (one process per GPU) -----------------------------------
+    def capture(self) -> bool:
+        """Capture the cycle -- every phase kernel and every NCCL exchange between them, all on
+        the engine's stream -- into two CUDA graphs, one per parity of the finest level's double
+        buffer, so a cycle costs one graph launch instead of ~40 host enqueues.  Returns False
+        (and stays on the eager path) if the capture fails."""
+        import torch
+        if len(self.shards) != 1:
+            raise RuntimeError("graph capture is for one shard per process")
+        sh = self.shards[0]
+        before = sh.state()
+        graphs, pool = [], None
+        try:
+            for _ in range(2):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, pool=pool, stream=sh.stream, capture_error_mode="thread_local"):
+                    self.cycle()
+                pool = g.pool()
+                graphs.append(g)
+        except Exception as exc:  # stay on the eager path
+            import sys
+            print(f"sharded cycle: CUDA graph capture failed ({exc!r}); running eagerly", file=sys.stderr)
+            sh.state(before)
+            self._graphs = None
+            return False
+        sh.state(before)  # the captured cycles did not run
+        self._graphs, self._next = graphs, 0
+        return True
+
+    def replay(self) -> None:
+        """One cycle from the captured graphs (launch on the shard's stream)."""
+        self._graphs[self._next].replay()
+        c, p = self.shards[0].state()
+        self.shards[0].state((c + 1, p ^ 1))
+        self._next ^= 1
 
 
 def owned_u(pl: Plan, level: int, rank: int, u: np.ndarray) -> np.ndarray:
