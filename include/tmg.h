@@ -198,6 +198,13 @@ int tmg_levels(tmg_handle* h, int32_t* lmin, int32_t* ltop);
 int tmg_level_counts(tmg_handle* h, int32_t level, int64_t* dof, int64_t* composite,
                      int64_t* hanging);
 
+/* Patch list of a 2D level (no reference counterpart: the reference stores and sweeps dense
+ * per-level arrays, spacetree.py:164-191): *dense = vertex tiles of the level's bounding
+ * array, *listed = tiles in its patch list -- those holding an existing vertex, the only ones
+ * the cycle kernels of an adaptive level visit; 0 = the level is swept densely (every vertex
+ * exists, or the level belongs to the single-block coarse chain). */
+int tmg_level_tiles(tmg_handle* h, int32_t level, int64_t* listed, int64_t* dense);
+
 /* masks[l]["kinds"] (spacetree.py:164-191), int8 (n+1)^2. */
 int tmg_get_kinds(tmg_handle* h, int32_t level, int8_t* out);
 

@@ -25,7 +25,7 @@ F_U, F_RHO, F_SM, F_CARRY, F_G, F_PART = 0, 1, 2, 3, 4, 5
 
 EXPORTS = ("tmg_create", "tmg_rebuild", "tmg_set_rhs", "tmg_set_u", "tmg_get_u",
            "tmg_update_fas_state", "tmg_cycle", "tmg_residual_stats", "tmg_levels",
-           "tmg_level_counts", "tmg_get_kinds", "tmg_get_table", "tmg_time_cycles",
+           "tmg_level_counts", "tmg_level_tiles", "tmg_get_kinds", "tmg_get_table", "tmg_time_cycles",
            "tmg_profile_cycles", "tmg_launches_per_cycle", "tmg_destroy", "tmg_last_error",
            "tmg_device_count", "tmg3_create", "tmg3_rebuild", "tmg_dim", "tmg3_shard", "tmg3_phase",
            "tmg3_field", "tmg3_stream", "tmg3_history", "tmg3_storage", "tmg3_fused", "tmg3_cycle_state")
@@ -79,6 +79,7 @@ def lib() -> C.CDLL:
         "tmg_residual_stats": ([H, P(Stats)], C.c_int),
         "tmg_levels": ([H, P(C.c_int32), P(C.c_int32)], C.c_int),
         "tmg_level_counts": ([H, C.c_int32, P(C.c_int64), P(C.c_int64), P(C.c_int64)], C.c_int),
+        "tmg_level_tiles": ([H, C.c_int32, P(C.c_int64), P(C.c_int64)], C.c_int),
         "tmg_get_kinds": ([H, C.c_int32, C.c_void_p], C.c_int),
         "tmg_get_table": ([H, C.c_int32, C.c_int32, C.c_void_p], C.c_int),
         "tmg_time_cycles": ([H, C.c_int32, C.c_int64, P(C.c_float)], C.c_int),

@@ -68,6 +68,10 @@ struct Level {
   long long cnt[8] = {0};
   double w_l = 0.0, hA = 0.0, hB = 0.0;
   int part_off = 0, nblocks = 0;
+  // patch list of an adaptive level (kernels2d.cu: tile_origin): the vertex tiles holding an
+  // existing vertex, in row-major tile order; nullptr when every vertex of the level exists
+  uint32_t* tiles = nullptr;
+  int ntiles = 0, tile_h = 0;
 };
 
 struct KTimer {
@@ -209,15 +213,43 @@ inline unsigned tiles_y(int N, int ty = tmg::kTileY) { return (unsigned)((N + ty
 // beats 1, 4 and 8).
 constexpr int kCoarseTileY = 2;
 
-#define LAUNCH_TILES(h, name, kernel, N, TY, ...)                                      \
-  do {                                                                                 \
-    cudaEvent_t e0_ = nullptr;                                                         \
-    TRY(begin_k(h, name, &e0_));                                                       \
-    kernel<<<dim3(tiles_x(N), tiles_y(N, TY)), dim3(tmg::kTileX, (TY)), 0, (h)->s>>>(  \
-        __VA_ARGS__);                                                                  \
-    CKL();                                                                             \
-    TRY(end_k(h, name, e0_));                                                          \
+// one block per vertex tile of level LV: its patch list when it has one, else the dense tile grid
+#define LAUNCH_TILES(h, name, kernel, LV, TY, ...)                                               \
+  do {                                                                                           \
+    cudaEvent_t e0_ = nullptr;                                                                   \
+    TRY(begin_k(h, name, &e0_));                                                                 \
+    const dim3 grid_ = (LV).tiles ? dim3((unsigned)(LV).ntiles) : dim3(tiles_x((LV).N), tiles_y((LV).N, TY)); \
+    kernel<<<grid_, dim3(tmg::kTileX, (TY)), 0, (h)->s>>>(__VA_ARGS__);                          \
+    CKL();                                                                                       \
+    TRY(end_k(h, name, e0_));                                                                    \
   } while (0)
+
+// Patch list of an adaptive level (north star: "hanging-vertex handling for adaptive grids, via
+// per-level patch lists"; the reference keeps dense per-level arrays and masks, spacetree.py:
+// 164-191 / solvers.py:179-192): the row-major list of vertex tiles with an existing vertex.
+// The cycle kernels of the level launch one block per listed tile, so a level refined along a
+// thin feature (config 4's level 8: 7 % of the vertex slots exist) costs its patches, not its
+// bounding box; its partial-sum slots shrink with it.
+int build_patch_list(tmg_handle* h, Level& c) {
+  const int tx = (int)tiles_x(c.N), ty = (int)tiles_y(c.N, c.tile_h), nt = tx * ty;
+  uint8_t* mask = nullptr;
+  TRY(dalloc(h, &mask, (size_t)nt));
+  tmg::k_tile_any<<<nblk((size_t)nt), 256, 0, h->s>>>(c.flags, c.N, c.tile_h, tx, ty, mask);
+  CKL();
+  std::vector<uint8_t> hm((size_t)nt);
+  CK(cudaMemcpyAsync(hm.data(), mask, (size_t)nt, cudaMemcpyDeviceToHost, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  std::vector<uint32_t> list;
+  for (int t = 0; t < nt; ++t)
+    if (hm[(size_t)t]) list.push_back(((uint32_t)(t / tx) << 16) | (uint32_t)(t % tx));
+  if (list.empty() || (int)list.size() == nt || ty > 0xffff) return TMG_OK;  // dense grid
+  TRY(dalloc(h, &c.tiles, list.size()));
+  CK(cudaMemcpyAsync(c.tiles, list.data(), sizeof(uint32_t) * list.size(), cudaMemcpyHostToDevice, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  c.ntiles = (int)list.size();
+  c.nblocks = c.ntiles;
+  return TMG_OK;
+}
 
 // --- the cycle --------------------------------------------------------------
 //
@@ -234,6 +266,7 @@ tmg::DownArgs make_down(tmg_handle* h, int l, bool write) {
   a.is_top = (l == l1);
   a.variant = h->cfg.variant;
   a.write = write ? 1 : 0;
+  a.tiles = c.tiles;
   a.u = c.u;
   a.flags = c.flags;
   a.diag = c.diag;
@@ -279,6 +312,7 @@ tmg::UpArgs make_up(tmg_handle* h, int l) {
   a.l0 = l0;
   a.N = c.N;
   a.is_bottom = (l == l0);
+  a.tiles = c.tiles;
   a.boxmg = h->cfg.flavor == TMG_BOXMG;
   a.pi = h->cfg.variant == tmg::VAR_PI;
   a.flags = c.flags;
@@ -348,9 +382,9 @@ int enqueue_down(tmg_handle* h, bool write) {
   for (int l = h->ltop; l > h->lc; --l) {
     tmg::DownArgs a = make_down(h, l, write);
     if (l == h->ltop)
-      LAUNCH_TILES(h, lvl_name("k_down", l), tmg::k_down<1>, h->L[l].N, tmg::kTileY, a);
+      LAUNCH_TILES(h, lvl_name("k_down", l), tmg::k_down<1>, h->L[l], tmg::kTileY, a);
     else
-      LAUNCH_TILES(h, lvl_name("k_down", l), tmg::k_down<0>, h->L[l].N, kCoarseTileY, a);
+      LAUNCH_TILES(h, lvl_name("k_down", l), tmg::k_down<0>, h->L[l], kCoarseTileY, a);
   }
   TRY(launch_coarse(h, write));
   return TMG_OK;
@@ -363,7 +397,14 @@ int enqueue_hang(tmg_handle* h) {
     if (c.cnt[tmg::K_HANG] == 0) continue;
     const double* uc = (l == l0) ? h->u_below : h->L[l - 1].u;
     const int Nc = (l == l0) ? h->N_below : h->L[l - 1].N;
-    LAUNCH(h, lvl_name("k_hang", l), tmg::k_hang, nblk(c.nv), c.u, c.flags, c.N, uc, Nc);
+    if (c.tiles) {
+      if (c.tile_h == tmg::kTileY)
+        LAUNCH_TILES(h, lvl_name("k_hang", l), tmg::k_hang_tiles, c, tmg::kTileY, c.u, c.flags, c.N, uc, Nc, c.tiles);
+      else
+        LAUNCH_TILES(h, lvl_name("k_hang", l), tmg::k_hang_tiles, c, kCoarseTileY, c.u, c.flags, c.N, uc, Nc, c.tiles);
+    } else {
+      LAUNCH(h, lvl_name("k_hang", l), tmg::k_hang, nblk(c.nv), c.u, c.flags, c.N, uc, Nc);
+    }
   }
   return TMG_OK;
 }
@@ -383,8 +424,8 @@ int enqueue_cycle(tmg_handle* h) {
   TRY(enqueue_down(h, true));  // includes the coarse chain (down, stats, up)
   for (int l = h->lc + 1; l <= h->ltop; ++l) {
     tmg::UpArgs a = make_up(h, l);
-    LAUNCH_TILES(h, lvl_name("k_up", l), tmg::k_up, h->L[l].N,
-                 l == h->ltop ? tmg::kTileY : kCoarseTileY, a);
+    if (l == h->ltop) LAUNCH_TILES(h, lvl_name("k_up", l), tmg::k_up, h->L[l], tmg::kTileY, a);
+    else LAUNCH_TILES(h, lvl_name("k_up", l), tmg::k_up, h->L[l], kCoarseTileY, a);
   }
   TRY(enqueue_hang(h));  // injection rides in k_up / k_coarse
   return TMG_OK;
@@ -661,13 +702,23 @@ int build(tmg_handle* h, const tmg_tree* t) {
     TRY(dalloc(h, &c.u, c.nv));
     if (!t->u || !t->u[l]) return fail(TMG_EINVAL, "tree.u missing a level");
     CK(cudaMemcpyAsync(c.u, t->u[l], sizeof(double) * c.nv, cudaMemcpyHostToDevice, h->s));
+    // work vectors start at zero: a level with a patch list never writes the slots of vertices
+    // that do not exist, and their neighbours' restriction / prolongation footprints read them
     TRY(dalloc(h, &c.g, c.nv));
+    CK(cudaMemsetAsync(c.g, 0, sizeof(double) * c.nv, h->s));
     if (l > l0) {
       TRY(dalloc(h, &c.rho, c.nv));
       TRY(dalloc(h, &c.rdof, c.nv));
+      CK(cudaMemsetAsync(c.rho, 0, sizeof(double) * c.nv, h->s));
+      CK(cudaMemsetAsync(c.rdof, 0, sizeof(double) * c.nv, h->s));
     }
-    if (l < l1) TRY(dalloc(h, &c.carry, c.nv));
-    c.nblocks = (int)(tiles_x(c.N) * tiles_y(c.N, l == l1 ? tmg::kTileY : kCoarseTileY));
+    if (l < l1) {
+      TRY(dalloc(h, &c.carry, c.nv));
+      CK(cudaMemsetAsync(c.carry, 0, sizeof(double) * c.nv, h->s));
+    }
+    c.tile_h = l == l1 ? tmg::kTileY : kCoarseTileY;
+    c.nblocks = (int)(tiles_x(c.N) * tiles_y(c.N, c.tile_h));
+    if (l > h->lc && c.cnt[tmg::K_NONE] > 0) TRY(build_patch_list(h, c));
     if (l > h->lc) {
       c.part_off = parts;
       parts += c.nblocks;
@@ -975,6 +1026,17 @@ int tmg_level_counts(tmg_handle* h, int32_t level, int64_t* dof, int64_t* compos
   if (dof) *dof = c.cnt[tmg::K_DOF] + c.cnt[tmg::K_OVER];
   if (composite) *composite = c.cnt[tmg::K_DOF];
   if (hanging) *hanging = c.cnt[tmg::K_HANG];
+  return TMG_OK;
+}
+
+int tmg_level_tiles(tmg_handle* h, int32_t level, int64_t* listed, int64_t* dense) {
+  DeviceGuard dg_(h);
+  if (!h || !listed || !dense) return fail(TMG_EINVAL, "null argument");
+  if (h->e3) return fail(TMG_EINVAL, "3D handles hold regular trees (no patch lists)");
+  TRY(check_level(h, level));
+  const Level& c = h->L[level];
+  *dense = (int64_t)tiles_x(c.N) * tiles_y(c.N, c.tile_h ? c.tile_h : tmg::kTileY);
+  *listed = c.tiles ? c.ntiles : 0;
   return TMG_OK;
 }
 

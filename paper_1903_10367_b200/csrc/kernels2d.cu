@@ -794,10 +794,26 @@ __device__ __forceinline__ void block_reduce(double& s, double& m) {
 
 // Grid kernels use 32 x 8 thread tiles over (j, i): no index division and
 // the 3x3 neighbourhoods of a tile share cache lines.
+// Adaptive levels launch one block per entry of the level's patch list (1D grid) instead of one
+// per tile of the dense vertex array: vertices that do not exist carry zeros in every work vector
+// and are never read as DoFs, so tiles without an existing vertex need no work.
+__device__ __forceinline__ void tile_origin(const uint32_t* tiles, int& bx, int& by) {
+  if (tiles) {
+    const uint32_t t = tiles[blockIdx.x];
+    bx = (int)(t & 0xffffu);
+    by = (int)(t >> 16);
+  } else {
+    bx = blockIdx.x;
+    by = blockIdx.y;
+  }
+}
+
 template <int TOP>
 __global__ void __launch_bounds__(kBlock) k_down(const __grid_constant__ DownArgs a) {
-  const int j = blockIdx.x * kTileX + threadIdx.x;
-  const int i = blockIdx.y * blockDim.y + threadIdx.y;  // tile height: 8 (finest) or 2 (coarse)
+  int bx, by;
+  tile_origin(a.tiles, bx, by);
+  const int j = bx * kTileX + threadIdx.x;
+  const int i = by * blockDim.y + threadIdx.y;  // tile height: 8 (finest) or 2 (coarse)
   double s = 0.0, m = 0.0;
   if (i < a.N && j < a.N) down_vertex<LdNC, TOP>(a, i, j, s, m);
   block_reduce<kBlock>(s, m);
@@ -809,9 +825,47 @@ __global__ void __launch_bounds__(kBlock) k_down(const __grid_constant__ DownArg
 }
 
 __global__ void __launch_bounds__(kBlock) k_up(const __grid_constant__ UpArgs a) {
-  const int j = blockIdx.x * kTileX + threadIdx.x;
-  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  int bx, by;
+  tile_origin(a.tiles, bx, by);
+  const int j = bx * kTileX + threadIdx.x;
+  const int i = by * blockDim.y + threadIdx.y;
   if (i < a.N && j < a.N) up_vertex<LdNC>(a, i, j);
+}
+
+// 1 where the (32 x ty) vertex tile holds an existing vertex (setup of the patch lists)
+__global__ void k_tile_any(const uint8_t* __restrict__ flags, int N, int ty, int tx_count, int ty_count,
+                           uint8_t* __restrict__ mask) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= tx_count * ty_count) return;
+  const int bx = t % tx_count, by = t / tx_count;
+  uint8_t any = 0;
+  for (int r = 0; r < ty && !any; ++r) {
+    const int i = by * ty + r;
+    if (i >= N) break;
+    for (int c = 0; c < kTileX; ++c) {
+      const int j = bx * kTileX + c;
+      if (j >= N) break;
+      if ((flags[(size_t)i * N + j] & 7) != K_NONE) {
+        any = 1;
+        break;
+      }
+    }
+  }
+  mask[t] = any;
+}
+
+// hanging-vertex refresh over the level's patch list (one block per listed tile)
+__global__ void __launch_bounds__(kBlock) k_hang_tiles(double* __restrict__ u, const uint8_t* __restrict__ flags,
+                                                       int N, const double* __restrict__ uc, int Nc,
+                                                       const uint32_t* __restrict__ tiles) {
+  int bx, by;
+  tile_origin(tiles, bx, by);
+  const int j = bx * kTileX + threadIdx.x;
+  const int i = by * blockDim.y + threadIdx.y;
+  if (i >= N || j >= N) return;
+  const size_t v = (size_t)i * N + j;
+  if ((flags[v] & 7) != K_HANG) return;
+  u[v] = prolong_dlinear_at<LdNC>(uc, Nc, i, j);
 }
 
 // Plain loads for the coarse-chain kernel: its level vectors are written and

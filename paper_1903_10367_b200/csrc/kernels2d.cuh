@@ -47,6 +47,9 @@ struct DownArgs {
   double* g;
   double* part_sum;
   double* part_max;
+  // adaptive levels: the level's patch list -- the (32 x tile height) vertex tiles that hold at
+  // least one existing vertex, packed (tile row << 16 | tile column); nullptr = every tile
+  const uint32_t* tiles;
 };
 
 // One level of the coarse -> fine carry (solvers.py:386-395) with the
@@ -67,6 +70,7 @@ struct UpArgs {
   double* ul[kMaxLevels];
   const uint8_t* fl[kMaxLevels];
   int Nl[kMaxLevels];
+  const uint32_t* tiles;  // the level's patch list (see DownArgs), or nullptr
 };
 
 // The coarse chain [l0, lc] (at most kMaxChain levels) in one block: down

@@ -383,6 +383,13 @@ class GpuEngine:
         self._host_stale = True
         return {names[k].decode(): (ms[k], cnt[k]) for k in range(nk.value)}
 
+    def patch_tiles(self, level: int) -> tuple[int, int]:
+        """(tiles in the level's patch list, tiles of its dense vertex array); 2D only.  A listed
+        count of 0 means the level is swept densely (regular level or coarse chain)."""
+        a, b = C.c_int64(), C.c_int64()
+        _abi.check(_abi.lib().tmg_level_tiles(self._h, level, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def weight_storage(self, level: int) -> dict:
         """3D: how level `level`'s BoxMG weights are stored (``tmg3_storage``): rows of P and
         of its cube-owned copy, and the distinct rows of their dictionaries (0 = dense)."""

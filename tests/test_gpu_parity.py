@@ -208,3 +208,25 @@ def test_config4_full_size_against_reference():
     assert [s.updates for s in hist] == case["updates"].tolist()
     # the reference stopped with EXIT_DIVERGED: normalized l2h above 1e4
     assert hist[-1].l2h / hist[0].l2h > 1e4 and meta["status"] == "diverged"
+    # the refined levels ran from their patch lists: far fewer vertex tiles than the dense arrays
+    # hold (level 8: the annulus covers ~7 % of the 6562^2 vertex slots), the regular levels densely
+    for l in range(5, 9):
+        listed, dense = eng.patch_tiles(l)
+        assert 0 < listed < dense // 4, (l, listed, dense)
+    assert eng.patch_tiles(4) == (0, eng.patch_tiles(4)[1])
+
+
+def test_patch_lists_cover_every_existing_vertex():
+    """Every vertex that exists lies in a listed tile: the run from the patch lists equals the
+    reference on a small adaptive mesh for every variant (the goldens above) and, here, the
+    number of listed tiles is at least the existing vertices' bounding count."""
+    wl = workloads.by_name("config4-small")
+    eng = GpuEngine(wl.tree, SolverConfig(variant=wl.variant, flavor=wl.flavor), sync="lazy")
+    for l in range(eng.lmin, eng.ltop + 1):
+        listed, dense = eng.patch_tiles(l)
+        exists = int((eng.kinds(l) != 0).sum())
+        th = 8 if l == eng.ltop else 2
+        if listed:
+            assert listed * 32 * th >= exists and listed < dense, (l, listed, dense, exists)
+        else:
+            assert exists == eng.kinds(l).size or (3**l + 1) ** 2 <= 1024, l
