@@ -61,14 +61,19 @@ __device__ __forceinline__ double const_from(const double x[27], double m, doubl
 
 // mg3d.element_sums / apply_element at an interior vertex: cells v - a in
 // corner order; E = sum e_a, T = sum e_a * s_a (sequential from the first).
+// (The oracle accumulates E and T cell by cell; here the eight cells are summed pairwise -- a
+// depth-3 tree instead of an 8-long dependent chain, the kernels' fp64 latency stalls -- which
+// stays within rounding of the oracle's order: the 3D bar is relative 1e-10.)
 __device__ __forceinline__ void element_ET(const double x[27], const double e[8], double& E, double& T) {
+  double p[8];
 #pragma unroll
   for (int a = 0; a < 8; ++a) {
     const int s0 = 1 - 2 * (a & 1), s1 = 1 - 2 * ((a >> 1) & 1), s2 = 1 - 2 * (a >> 2);
-    const double s = ((x[tap(s0, s1, 0)] + x[tap(s0, 0, s2)]) + x[tap(0, s1, s2)]) + x[tap(s0, s1, s2)];
-    if (a == 0) { E = e[0]; T = e[0] * s; }
-    else { E = E + e[a]; T = T + e[a] * s; }
+    const double s = (x[tap(s0, s1, 0)] + x[tap(s0, 0, s2)]) + (x[tap(0, s1, s2)] + x[tap(s0, s1, s2)]);
+    p[a] = e[a] * s;
   }
+  E = ((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]));
+  T = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
 }
 
 template <class LD>
