@@ -112,39 +112,3 @@ struct Chain3 {
 };
 
 }  // namespace t3
-
-namespace t3 {
-
-// Fused fine pass (kernels3d_ffp.cu): completes the previous cycle's update of
-// the finest level and runs this cycle's finest-level down sweep and its
-// restriction to level ltop-1 in one 2.5D sweep.
-constexpr int kFT = 8;                 // coarse tile (J, K) per CTA
-constexpr int kFU = 3 * kFT + 6;       // u_new window (fine offset -4)
-constexpr int kFR = 3 * kFT + 4;       // rho window (offset -3)
-constexpr int kFS = 3 * kFT + 2;       // sm / restriction window (offset -2)
-constexpr int kFC = 3 * kFT + 5;       // cell window (offset -4)
-constexpr int kFThreads = 256;
-
-struct Ffp3 {
-  int N, Nc, tiles, chunk;  // tiles per axis, coarse planes per i-chunk
-  int apply;                // 1: u_new = u + (P carry_c + g_in); 0: u_new = u
-  int variant, jac;
-  const double* u_in;
-  double* u_out;
-  const double* g_in;
-  double* g_out;
-  const double* carry_c;
-  const double* P;
-  Op3 op;
-  const double* rhs;
-  double w, hw, scale;
-  double* bR;   // R rho_top at interior coarse vertices
-  double* bT;   // R sm_top
-  int l, l0;
-  double* ul[kMaxLevels];
-  int Nl[kMaxLevels];
-  double* part_sum;
-  double* part_max;
-};
-
-}  // namespace t3

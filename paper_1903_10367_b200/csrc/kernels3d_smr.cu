@@ -203,7 +203,8 @@ constexpr int kRSplit = 13;
 template <bool DICT, int RV, int GH, bool DEC = false>
 __global__ void __launch_bounds__(DEC ? kRThreads : (RV ? kRTasks + kRK * kRJ : kRThreads), 1)
     k3_smr(const __grid_constant__ Smr A) {
-  static_assert(!DEC || (DICT && RV == 1), "the decoupled schedule needs the dictionary and RV 1");
+  static_assert(RV == 1 && GH == 7, "one restriction thread (pair) per coarse vertex, 7-column smoothing groups");
+  static_assert(!DEC || DICT, "the decoupled schedule needs the dictionary");
   constexpr int kSPairs = kSPer<GH>, kSCols = GH * kSPairs, kSGroups = kSW * (kSH / GH);
   constexpr int kRStages = DEC ? kRStagesB : t3::kRStages;  // rho slots
   constexpr int oRTab = kRStages * kRSlot;
@@ -547,66 +548,7 @@ __global__ void __launch_bounds__(DEC ? kRThreads : (RV ? kRTasks + kRK * kRJ : 
         // fine plane s feeds coarse plane m3 (offset o) and, for o >= 1, m3 + 1 (offset o - 3);
         // this role's plane among them (warp-uniform)
         const int m3 = m3c, o = oc;
-        if constexpr (RV == 1) {
-          restrict_body(s, ssl, m3, o, k3c, k6c, sr + oS + (s & 1) * kSBuf, ps);
-          continue;
-        }
-        int m = -1, off = 0;
-        if (((m3 - Ia) & 1) == role) {
-          m = m3;
-          off = o;
-        } else if (o >= 1) {
-          m = m3 + 1;
-          off = o - 3;
-        }
-        if (rtask && m >= Ia && m < Ib) {
-          constexpr int ld = kRW;  // both windows: immediate offsets in the sums
-          const double* xr = sr + (rs_ % kRStages) * kRSlot + (3 * wj + 3) * kRW + 3 * wk + 3;
-          const double* xs = sr + oS + (s & 1) * kSBuf + (3 * wj + 2) * kRW + 3 * wk + 2;
-          // the weights of slots (off + 2) * 25 + q of plane m: DICT from the plane's staged rows
-          // (waited for once, at the plane's first fine plane, off = -2), else its P box
-          const double* wp;
-          int ws;
-          if (DICT) {
-            if (off == -2) wait_plane(m);
-            wp = rows_of(m) + tab_of(m)[kRTabLoc + w] * kRRowS + (off + 2) * 25;
-            ws = 1;
-          } else {
-            wp = sr + oRP + (ps % kPStages) * 2 * kPBox + wj * kPW + wk + 1 + (m == m3 ? 0 : kPBox);
-            ws = kRJ * kPW;
-          }
-          double aR = accR, aS = accS;
-          if (A.jac) {
-#pragma unroll
-            for (int q = 0; q < 25; ++q) {
-              const int oj = q / 5 - 2, ok = q % 5 - 2;
-              const bool ctr = off == 0 && q == 12;
-              const double wt = ctr ? 1.0 : wp[q * ws];
-              double x = xr[oj * ld + ok];
-              if (ctr && A.zc) x = 0.0;
-              aR = aR + wt * x;
-              aS = aS + wt * xs[oj * ld + ok];
-            }
-          } else {
-#pragma unroll
-            for (int q = 0; q < 25; ++q) {
-              const int oj = q / 5 - 2, ok = q % 5 - 2;
-              const bool ctr = off == 0 && q == 12;
-              const double wt = ctr ? 1.0 : wp[q * ws];
-              double x = xr[oj * ld + ok];
-              if (ctr && A.zc) x = 0.0;
-              aR = aR + wt * x;
-            }
-          }
-          if (off == 2) {  // plane m complete
-            const size_t ix = ((size_t)m * Nc + rJ) * Nc + rK;
-            A.bR[ix] = aR;
-            if (A.jac) A.bT[ix] = aS;
-            aR = aS = 0.0;
-          }
-          accR = aR;
-          accS = aS;
-        }
+        restrict_body(s, ssl, m3, o, k3c, k6c, sr + oS + (s & 1) * kSBuf, ps);
       }
     }
   }
