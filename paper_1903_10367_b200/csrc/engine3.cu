@@ -18,6 +18,7 @@
 #include "kernels3d_smr.cu"
 #include "kernels3d_top4r.cu"
 #include "kernels3d_updict.cu"
+#include "kernels3d_smc.cu"
 #include "kernels3d_dict.cu"
 #include "kernels3d_rap.cu"
 #include "kernels3d_uplin.cu"
@@ -37,6 +38,8 @@ struct Lvl3 {
   uint32_t *Pdi = nullptr, *Pcdi = nullptr;
   uint8_t* Ptab = nullptr;  // k3_up_tma step tables over Pc's dictionary
   uint8_t* Pstab = nullptr;  // k3_smr tile-plane tables over P's dictionary
+  double* Pds = nullptr;     // P's dictionary in fine-plane slices (k3_smc)
+  uint8_t* Pctab = nullptr;  // k3_smc tile-plane tables (31 x 4 vertex tiles)
   double* Td = nullptr;      // level ltop-1: the Galerkin rows as a row dictionary (op.tdict)
   uint32_t* Tdi = nullptr;
   size_t Tdn = 0;
@@ -542,6 +545,87 @@ SmoothS make_smooth_s(Engine3* e, int l) {
   return a;
 }
 
+// TMG_SMC=0 keeps k3_smr on the dictionary path (A/B)
+bool use_smc() {
+  static const bool on = [] { const char* v = std::getenv("TMG_SMC"); return !(v && v[0] == '0'); }();
+  return on;
+}
+
+// the cell-owned kernel's inputs for level l as the coarse one: the sliced dictionary and the
+// tile-plane tables (one_row: every vertex uses row 0, the d-linear flavour)
+int build_smc(Engine3* e, int l, bool one_row) {
+  Lvl3& c = e->L[l];
+  c.Pds = nullptr;
+  c.Pctab = nullptr;
+  if (!c.Pd || c.Pdn == 0) return TMG_OK;
+  const int n = c.N - 2, tK = (n + kCK - 1) / kCK, tJ = (n + kCJ - 1) / kCJ;
+  const size_t cnt = (size_t)n * tJ * tK;
+  uint8_t* tab = nullptr;
+  TRY3(alloc3(e, &tab, cnt * kCTabBytes, false));
+  if (one_row) {
+    k3_smc_tables_one<<<nblk(cnt, 128), 128, 0, e->s>>>(tab, cnt);
+    CKL3();
+  } else {
+    int* dover = nullptr;
+    TRY3(alloc3(e, &dover, 1));
+    const size_t Ncp = ((size_t)c.N + 3) / 4 * 4;
+    k3_smc_tables<<<nblk(cnt, 128), 128, 0, e->s>>>(c.Pdi, c.N, (int)Ncp, tK, tJ, tab, dover);
+    CKL3();
+    int over = 0;
+    CK3(cudaMemcpyAsync(&over, dover, sizeof(int), cudaMemcpyDeviceToHost, e->s));
+    CK3(cudaStreamSynchronize(e->s));
+    if (over) return TMG_OK;  // a tile plane meets too many rows: k3_smr's path
+  }
+  TRY3(alloc3(e, &c.Pds, c.Pdn * 5 * kCSl, false));
+  k3_dict_slices<<<nblk(c.Pdn * 5 * kCSl, 256), 256, 0, e->s>>>(c.Pd, c.Pdn, c.Pds);
+  CKL3();
+  c.Pctab = tab;
+  return TMG_OK;
+}
+
+int launch_smc(Engine3* e, int l, bool smooth, int clo, int chi) {
+  Lvl3& c = e->L[l];
+  Lvl3& cc = e->L[l - 1];
+  Smc A{};
+  A.N = c.N;
+  A.Nc = cc.N;
+  A.ilo = clo < 0 ? 1 : clo;
+  A.ihi = chi < 0 ? cc.N - 1 : chi;
+  const int n = A.ihi - A.ilo;
+  if (n <= 0) return TMG_OK;
+  const int nk = cc.N - 2;
+  A.tilesK = (nk + kCK - 1) / kCK;
+  A.tilesJ = (nk + kCJ - 1) / kCJ;
+  const int tiles = A.tilesK * A.tilesJ;
+  int best = 1;  // coarse-plane chunks: about a whole number of waves of two CTAs per SM
+  double best_eff = 0.0;
+  for (int nch = 1; nch <= std::min(n, 32); ++nch) {
+    const int chunk = (n + nch - 1) / nch, nb = tiles * ((n + chunk - 1) / chunk);
+    const double waves = (double)nb / (2 * num_sms());
+    const double eff = waves / std::ceil(waves) * (double)chunk / (chunk + 1.0);
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = nch; }
+  }
+  A.chunk = (n + best - 1) / best;
+  A.jac = smooth ? 1 : 0;
+  A.zc = e->cfg.variant == VAR_AFACC ? 1 : 0;
+  A.scale = e->cfg.omega * 3.0 / 8.0;
+  A.bR = cc.bR;
+  A.bT = cc.bT;
+  A.pds = cc.Pds;
+  A.ptab = cc.Pctab;
+  const uint64_t N = (uint64_t)c.N;
+  if (!tmap3(&A.tr, c.rho, N, N, N, N * 8, N * N * 8, kCW, kCH, 1))
+    return fail3(e, TMG_ECUDA, "tensor map encoding failed (k3_smc)");
+  const dim3 grid(tiles, (n + A.chunk - 1) / A.chunk);
+  cudaEvent_t e0_ = nullptr;
+  TRY3(begin_k(e, &e0_));
+  if (smooth) k3_smc<true><<<grid, kCThreads, kSmcSmem, e->s>>>(A);
+  else k3_smc<false><<<grid, kCThreads, kSmcSmem, e->s>>>(A);
+  CKL3();
+  TRY3(end_k(e, kname("k3_smooth", l), e0_));
+  return TMG_OK;
+}
+
 // k3_smr over the finest level: adaFACx smoothing (when `smooth`) and the restriction of rho / sm
 // into level ltop-1's bR / bT
 // (sharded: the coarse planes [clo, chi) a rank owns; its rho must hold 3 planes below and 1 above
@@ -549,6 +633,7 @@ SmoothS make_smooth_s(Engine3* e, int l) {
 int launch_smr(Engine3* e, int l, bool smooth, int clo = -1, int chi = -1) {
   Lvl3& c = e->L[l];
   Lvl3& cc = e->L[l - 1];
+  if (cc.Pds && use_smc()) return launch_smc(e, l, smooth, clo, chi);
   Smr A{};
   A.N = c.N;
   A.Nc = cc.N;
@@ -872,6 +957,7 @@ int refresh_pc(Engine3* e, int l) {
       CK3(cudaStreamSynchronize(e->s));
       if (over) c.Pd = nullptr, c.Pdn = 0;
     }
+    TRY3(build_smc(e, l, false));
   }
   return TMG_OK;
 }
@@ -1168,9 +1254,12 @@ int build(Engine3* e, const tmg_tree3* t) {
         TRY3(alloc3(e, &cc.Pstab, cnt * kRTabBytes, false));
         k3_smr_tables_one<<<nblk(cnt, 128), 128, 0, e->s>>>(cc.Pstab, cnt);
         CKL3();
+        TRY3(build_smc(e, l, true));
       }
     }
     if (e->smr) {
+      CK3(cudaFuncSetAttribute(k3_smc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmcSmem));
+      CK3(cudaFuncSetAttribute(k3_smc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmcSmem));
       CK3(cudaFuncSetAttribute(k3_smr<false, 1, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmem));
       CK3(cudaFuncSetAttribute(k3_smr<true, 1, 7, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmemDB));
       for (int l = e->smr_lo - 1; l < l1; ++l) {
