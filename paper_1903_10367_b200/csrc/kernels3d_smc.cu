@@ -19,8 +19,8 @@
 //   * When a coarse plane completes, the 4 cells around a coarse vertex add their partial sums:
 //     along K by a warp shuffle, along J through a small shared-memory exchange (fixed order).
 // CTA = 5 cell rows x 32 cells (5 consumer warps) for a tile of 4 x 31 coarse vertices, plus one
-// producer warp: a 3-slot ring of {rho plane (TMA box 100 x 17), the step's weight slices} and a
-// 4-slot ring of the tile-plane tables (distinct dictionary rows of the tile's vertices in a
+// producer warp: a 4-slot ring of rho planes (TMA box 100 x 17), a 3-slot ring of the steps' weight
+// slices and a 4-slot ring of the tile-plane tables (distinct dictionary rows of the tile's vertices in a
 // coarse plane + each vertex's index), completion on mbarriers.  The weights come from a sliced
 // copy of P's row dictionary (5 slices of 25 weights per row, one per fine plane offset, padded
 // to 26 doubles so that a slice is a 16-byte-aligned 208-byte bulk copy): a step stages only the
@@ -42,16 +42,15 @@ constexpr int kCRho = (kCW * kCH * 8 + 127) / 128 * 128 / 8;   // 1712 doubles
 constexpr int kCSl = 26;                           // doubles per weight slice (25 + pad)
 constexpr int kCRows = 32;                         // distinct rows per tile plane (cap)
 constexpr int kCWts = 2 * kCRows * kCSl;           // one step's slices: [coarse plane c | nx][row][26]
-constexpr int kCSlot = kCRho + kCWts;              // 3376 doubles = 27008 B (128-byte multiple)
-constexpr int kCR = 3;                             // ring depth (steps)
+constexpr int kCR = 4, kCWR = 3;                   // ring depths: rho planes, weight slice sets
 constexpr int kCNT = 4;                            // table ring (coarse planes)
 constexpr int kCTabBytes = 272;                    // {n, ids[32]} uint32, local[124] uint8 at byte 132
 constexpr int kCTabLoc = 132;
-constexpr int oCTab = kCR * kCSlot;
+constexpr int oCWts = kCR * kCRho, oCTab = oCWts + kCWR * kCWts;
 constexpr int oCScr = oCTab + kCNT * kCTabBytes / 8;
 constexpr int kCScr = kCCJ * 32 * 2;               // one exchange buffer: [cell row][lane][field]
 constexpr size_t kSmcSmem = sizeof(double) * (oCScr + 2 * kCScr);
-static_assert(kCSlot % 16 == 0 && kCRho % 16 == 0, "slots stay 128-byte aligned");
+static_assert(kCWts % 16 == 0 && kCRho % 16 == 0, "slots stay 128-byte aligned");
 static_assert(2 * (kSmcSmem + 1024) <= 227 * 1024, "two CTAs per SM");
 
 // P's row dictionary in slices: Pds[(id * 5 + si) * 26 + q] = Pd[id * kDictW + si * 25 + q]
@@ -127,7 +126,7 @@ struct Smc {
 template <bool JAC>
 __global__ void __launch_bounds__(kCThreads, 2) k3_smc(const __grid_constant__ Smc A) {
   extern __shared__ __align__(128) double sc[];
-  __shared__ __align__(8) uint64_t full[kCR], done[kCR], tful[kCNT];
+  __shared__ __align__(8) uint64_t full[kCR], done[kCR], wful[kCWR], wdone[kCWR], tful[kCNT];
   const int N = A.N, Nc = A.Nc, n = Nc - 2;
   const int tk = blockIdx.x % A.tilesK, tj = blockIdx.x / A.tilesK;
   const int K0 = 1 + tk * kCK, J0 = 1 + tj * kCJ;
@@ -143,6 +142,10 @@ __global__ void __launch_bounds__(kCThreads, 2) k3_smc(const __grid_constant__ S
     for (int q = 0; q < kCR; ++q) {
       mbar_init(&full[q], 1);
       mbar_init(&done[q], kCCJ);
+    }
+    for (int q = 0; q < kCWR; ++q) {
+      mbar_init(&wful[q], 1);
+      mbar_init(&wdone[q], kCCJ);
     }
     for (int q = 0; q < kCNT; ++q) mbar_init(&tful[q], 1);
     mbar_fence_init();
@@ -170,8 +173,9 @@ __global__ void __launch_bounds__(kCThreads, 2) k3_smc(const __grid_constant__ S
       issue_tab(Ia + 1);
     }
     for (int t = p0; t <= pEnd; ++t) {
-      const int r = t - p0, sl = r % kCR;
-      if (r >= kCR) mbar_wait(&done[sl], (unsigned)(r / kCR - 1) & 1u);  // iteration t - kCR consumed
+      const int r = t - p0, sl = r % kCR, wl = r % kCWR;
+      if (r >= kCR) mbar_wait(&done[sl], (unsigned)(r / kCR - 1) & 1u);      // rho of iteration t - kCR consumed
+      if (r >= kCWR) mbar_wait(&wdone[wl], (unsigned)(r / kCWR - 1) & 1u);  // slices of iteration t - kCWR
       const int s = t - 1;
       const int m3 = s >= 0 ? s / 3 : -1, o = s - 3 * m3;
       const bool rs = s >= s0 && s <= pEnd - 1;
@@ -195,18 +199,19 @@ __global__ void __launch_bounds__(kCThreads, 2) k3_smc(const __grid_constant__ S
         nn_ = (int)T[0];
         if (lane < nn_) idn = T[1 + lane];
       }
-      double* slot = sc + sl * kCSlot;
+      double* wslot = sc + oCWts + wl * kCWts;
       if (lane == 0) {
         fence_proxy_async();
-        mbar_expect_tx(&full[sl], (unsigned)(sizeof(double) * kCW * kCH) + (unsigned)(8 * kCSl) * (unsigned)(nc_ + nn_));
-        tma_load_3d(slot, &A.tr, &full[sl], fk0, fj0, t);
+        mbar_expect_tx(&full[sl], (unsigned)(sizeof(double) * kCW * kCH));
+        tma_load_3d(sc + sl * kCRho, &A.tr, &full[sl], fk0, fj0, t);
+        if (nc_ + nn_) mbar_expect_tx(&wful[wl], (unsigned)(8 * kCSl) * (unsigned)(nc_ + nn_));
+        else mbar_arrive(&wful[wl]);
       }
       __syncwarp();
       if (lane < nc_)
-        bulk_load(slot + kCRho + lane * kCSl, A.pds + ((size_t)idc * 5 + (o + 2)) * kCSl, 8 * kCSl, &full[sl]);
+        bulk_load(wslot + lane * kCSl, A.pds + ((size_t)idc * 5 + (o + 2)) * kCSl, 8 * kCSl, &wful[wl]);
       if (lane < nn_)
-        bulk_load(slot + kCRho + (kCRows + lane) * kCSl, A.pds + ((size_t)idn * 5 + (o - 1)) * kCSl, 8 * kCSl,
-                  &full[sl]);
+        bulk_load(wslot + (kCRows + lane) * kCSl, A.pds + ((size_t)idn * 5 + (o - 1)) * kCSl, 8 * kCSl, &wful[wl]);
     }
     return;
   }
@@ -247,8 +252,8 @@ __global__ void __launch_bounds__(kCThreads, 2) k3_smc(const __grid_constant__ S
   double* scr = sc + oCScr;
 
   for (int t = p0; t <= pEnd; ++t) {
-    const int r = t - p0, sl = r % kCR;
-    const double* slot = sc + sl * kCSlot;
+    const int r = t - p0, sl = r % kCR, wl = r % kCWR;
+    const double* slot = sc + sl * kCRho;
     mbar_wait(&full[sl], (unsigned)(r / kCR) & 1u);
     // ---- the 5 x 5 rho window of plane t; completes sm(t - 1) of the cell's 9 columns ----
     double W[5][5];
@@ -298,7 +303,8 @@ __global__ void __launch_bounds__(kCThreads, 2) k3_smc(const __grid_constant__ S
             for (int dk = 0; dk < 2; ++dk) roff[pl][dj][dk] = (pl * kCRows + tb[vix[dj][dk]]) * kCSl;
         }
       }
-      const double* wts = slot + kCRho;
+      mbar_wait(&wful[wl], (unsigned)(r / kCWR) & 1u);
+      const double* wts = sc + oCWts + wl * kCWts;
 #pragma unroll
       for (int dj = 0; dj < 2; ++dj)
 #pragma unroll
@@ -375,7 +381,10 @@ __global__ void __launch_bounds__(kCThreads, 2) k3_smc(const __grid_constant__ S
 #pragma unroll
       for (int b = 0; b < 3; ++b) X[a * 3 + b] = W[a + 1][b + 1];
     __syncwarp();
-    if (ckl == 0) mbar_arrive(&done[sl]);
+    if (ckl == 0) {
+      mbar_arrive(&done[sl]);
+      mbar_arrive(&wdone[wl]);
+    }
   }
 }
 
