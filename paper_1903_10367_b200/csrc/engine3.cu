@@ -37,7 +37,6 @@ struct Lvl3 {
   double *Pd = nullptr, *Pcd = nullptr;
   uint32_t *Pdi = nullptr, *Pcdi = nullptr;
   uint8_t* Ptab = nullptr;  // k3_up_tma step tables over Pc's dictionary
-  uint8_t* Pstab = nullptr;  // k3_smr tile-plane tables over P's dictionary
   double* Pds = nullptr;     // P's dictionary in fine-plane slices (k3_smc)
   uint8_t* Pctab = nullptr;  // k3_smc tile-plane tables (31 x 4 vertex tiles)
   double* Td = nullptr;      // level ltop-1: the Galerkin rows as a row dictionary (op.tdict)
@@ -545,12 +544,6 @@ SmoothS make_smooth_s(Engine3* e, int l) {
   return a;
 }
 
-// TMG_SMC=0 keeps k3_smr on the dictionary path (A/B)
-bool use_smc() {
-  static const bool on = [] { const char* v = std::getenv("TMG_SMC"); return !(v && v[0] == '0'); }();
-  return on;
-}
-
 // the cell-owned kernel's inputs for level l as the coarse one: the sliced dictionary and the
 // tile-plane tables (one_row: every vertex uses row 0, the d-linear flavour)
 int build_smc(Engine3* e, int l, bool one_row) {
@@ -633,7 +626,7 @@ int launch_smc(Engine3* e, int l, bool smooth, int clo, int chi) {
 int launch_smr(Engine3* e, int l, bool smooth, int clo = -1, int chi = -1) {
   Lvl3& c = e->L[l];
   Lvl3& cc = e->L[l - 1];
-  if (cc.Pds && use_smc()) return launch_smc(e, l, smooth, clo, chi);
+  if (cc.Pds) return launch_smc(e, l, smooth, clo, chi);  // P has a row dictionary: the cell-owned kernel
   Smr A{};
   A.N = c.N;
   A.Nc = cc.N;
@@ -662,16 +655,12 @@ int launch_smr(Engine3* e, int l, bool smooth, int clo = -1, int chi = -1) {
   const uint64_t N = (uint64_t)c.N, Nc = (uint64_t)cc.N;
   const uint64_t dp[4] = {Nc, Nc, Nc, 125}, sp[3] = {Nc * 8, Nc * Nc * 8, Nc * Nc * Nc * 8};
   const uint32_t bp[4] = {kPW, kRJ, 1, 25};
-  if (!tmap3(&A.tr, c.rho, N, N, N, N * 8, N * N * 8, kRW, kRH, 1) || (!cc.Pd && !tmap4(&A.tp, cc.P, dp, sp, bp)))
+  if (!tmap3(&A.tr, c.rho, N, N, N, N * 8, N * N * 8, kRW, kRH, 1) || !tmap4(&A.tp, cc.P, dp, sp, bp))
     return fail3(e, TMG_ECUDA, "tensor map encoding failed (k3_smr)");
-  A.pd = cc.Pd;
-  A.ptab = cc.Pstab;
-  A.tilesJ = (nk + kRJ - 1) / kRJ;
   const dim3 grid(tiles, (n + A.chunk - 1) / A.chunk);
   cudaEvent_t e0_ = nullptr;
   TRY3(begin_k(e, &e0_));
-  if (cc.Pd) k3_smr<true, 1, 7, true><<<grid, kRThreads, kSmrSmemDB, e->s>>>(A);
-  else k3_smr<false, 1, 7><<<grid, kRTasks + kRK * kRJ, kSmrSmem, e->s>>>(A);
+  k3_smr<<<grid, kRThreads, kSmrSmem, e->s>>>(A);
   CKL3();
   TRY3(end_k(e, kname("k3_smooth", l), e0_));
   return TMG_OK;
@@ -925,7 +914,7 @@ int refresh_pc(Engine3* e, int l) {
   const char* env = std::getenv("TMG_PDICT");
   if (e->cfg.throttled || (env && env[0] == '0') || l < e->ltop - 2 || c.Pd || c.Pcd) return TMG_OK;
   const bool force = env && env[0] == '2';
-  // Pc's dictionary feeds k3_up_dict, P's the restriction in k3_smr
+  // Pc's dictionary feeds k3_up_dict, P's the restriction in k3_smc
   TRY3(build_dict(e, RowsView{c.Pc, nc, Kp, nc * nc * Kp, kQS, nc, Kp}, nc * nc * nc, force, &c.Pcd, &c.Pcdi,
                     &c.Pcdp, &c.Pcdn));
   if (c.Pcd) {  // k3_up_tma's step tables; a step meeting more than kQRows rows keeps the dense stream
@@ -944,20 +933,8 @@ int refresh_pc(Engine3* e, int l) {
   {
     const size_t Nc = c.N, Ncp = (Nc + 3) / 4 * 4;  // id rows padded to 16 bytes
     TRY3(build_dict(e, RowsView{c.P, c.nv, 0, c.nv, 125, Nc, Ncp}, c.nv, force, &c.Pd, &c.Pdi, &c.Pdp, &c.Pdn));
-    if (c.Pd) {  // k3_smr's tile-plane tables; a tile plane meeting more than kRRows rows keeps the dense P
-      const int n = c.N - 2, tK = (n + kRK - 1) / kRK, tJ = (n + kRJ - 1) / kRJ;
-      const size_t cnt = (size_t)n * tJ * tK;
-      TRY3(alloc3(e, &c.Pstab, cnt * kRTabBytes, false));
-      int* dover = nullptr;
-      TRY3(alloc3(e, &dover, 1));
-      k3_smr_tables<<<nblk(cnt, 128), 128, 0, e->s>>>(c.Pdi, c.N, (int)Ncp, tK, tJ, c.Pstab, dover);
-      CKL3();
-      int over = 0;
-      CK3(cudaMemcpyAsync(&over, dover, sizeof(int), cudaMemcpyDeviceToHost, e->s));
-      CK3(cudaStreamSynchronize(e->s));
-      if (over) c.Pd = nullptr, c.Pdn = 0;
-    }
     TRY3(build_smc(e, l, false));
+    if (!c.Pds) c.Pd = nullptr, c.Pdn = 0;  // a tile plane meets too many rows: the dense stream (k3_smr)
   }
   return TMG_OK;
 }
@@ -1234,7 +1211,7 @@ int build(Engine3* e, const tmg_tree3* t) {
     e->smr_lo = e->lc + 2;  // every level whose coarser level is a grid (not chain) level
     if (e->smr && cfg.flavor == TMG_GEOMETRIC) {
       // d-linear transfer: one constant weight row for every interior coarse vertex (its fine
-      // offsets +-2 never leave the grid), so k3_smr's dictionary variant runs on a one-row
+      // offsets +-2 never leave the grid), so the dictionary kernel k3_smc runs on a one-row
       // dictionary and tile-plane tables that all name row 0
       double row[kDictW] = {0.0};
       for (int a = -2; a <= 2; ++a)
@@ -1249,19 +1226,13 @@ int build(Engine3* e, const tmg_tree3* t) {
         CK3(cudaMemcpyAsync(cc.Pd, row, sizeof(row), cudaMemcpyHostToDevice, e->s));
         CK3(cudaStreamSynchronize(e->s));
         cc.Pdn = 1;
-        const int n = cc.N - 2, tK = (n + kRK - 1) / kRK, tJ = (n + kRJ - 1) / kRJ;
-        const size_t cnt = (size_t)n * tJ * tK;
-        TRY3(alloc3(e, &cc.Pstab, cnt * kRTabBytes, false));
-        k3_smr_tables_one<<<nblk(cnt, 128), 128, 0, e->s>>>(cc.Pstab, cnt);
-        CKL3();
         TRY3(build_smc(e, l, true));
       }
     }
     if (e->smr) {
       CK3(cudaFuncSetAttribute(k3_smc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmcSmem));
       CK3(cudaFuncSetAttribute(k3_smc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmcSmem));
-      CK3(cudaFuncSetAttribute(k3_smr<false, 1, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmem));
-      CK3(cudaFuncSetAttribute(k3_smr<true, 1, 7, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmemDB));
+      CK3(cudaFuncSetAttribute(k3_smr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmrSmem));
       for (int l = e->smr_lo - 1; l < l1; ++l) {
         Lvl3& cc = e->L[l];
         if (!cc.bR) TRY3(alloc3(e, &cc.bR, cc.nv));

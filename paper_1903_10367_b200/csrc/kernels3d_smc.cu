@@ -279,11 +279,17 @@ __global__ void __launch_bounds__(kCThreads, 2) k3_smc(const __grid_constant__ S
           const double F = (W[a][b + 1] + W[a + 2][b + 1]) + ar[a + 1][b];
           const double G = -(ce * F + cc * D);
           const double H = cm * W[a + 1][b + 1] - ce * D;
-          const double sm = SA[q] + G;
-          Y[q] = (pl_ok && ((vmask >> q) & 1u)) ? sm : 0.0;
+          Y[q] = SA[q] + G;
           SA[q] = SG[q] + H;
           SG[q] = G;
         }
+      // sm exists at interior fine vertices only: cells on the domain boundary and the planes
+      // outside [1, N - 2] are the rare case
+      if (!pl_ok || vmask != 0x1ffu) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q)
+          if (!pl_ok || !((vmask >> q) & 1u)) Y[q] = 0.0;
+      }
     }
     // ---- restriction of fine plane s = t - 1 (x = rho(s) kept from the last iteration) ----
     const int s = t - 1;
