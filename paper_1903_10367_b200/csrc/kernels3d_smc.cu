@@ -28,6 +28,8 @@
 // two CTAs fit an SM.  Summation order differs from the oracle's o-major order (3D bar: 1e-10).
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "kernels3d.cuh"
 
 namespace t3 {
@@ -311,38 +313,47 @@ __global__ void __launch_bounds__(kCThreads, 2) k3_smc(const __grid_constant__ S
       }
       mbar_wait(&wful[wl], (unsigned)(r / kCWR) & 1u);
       const double* wts = sc + oCWts + wl * kCWts;
+      // the step's multiply-adds, specialised by which coarse planes the fine plane feeds (uniform)
+      auto feed = [&](auto CC, auto NN) {
+        constexpr bool C = decltype(CC)::value, NX = decltype(NN)::value;
 #pragma unroll
-      for (int dj = 0; dj < 2; ++dj)
+        for (int dj = 0; dj < 2; ++dj)
 #pragma unroll
-        for (int dk = 0; dk < 2; ++dk) {
-          if (!cok[dj][dk]) continue;
-          const double* wc = wts + roff[0][dj][dk];
-          const double* wn = wts + roff[1][dj][dk];
-          double aR = acc[0][dj][dk][0], aS = acc[0][dj][dk][1], bR_ = acc[1][dj][dk][0], bS_ = acc[1][dj][dk][1];
+          for (int dk = 0; dk < 2; ++dk) {
+            if (!cok[dj][dk]) continue;
+            const double* wc = wts + roff[0][dj][dk];
+            const double* wn = wts + roff[1][dj][dk];
+            double aR = acc[0][dj][dk][0], aS = acc[0][dj][dk][1], bR_ = acc[1][dj][dk][0], bS_ = acc[1][dj][dk][1];
 #pragma unroll
-          for (int a = dj; a < 3; ++a)
+            for (int a = dj; a < 3; ++a)
 #pragma unroll
-            for (int b = dk; b < 3; ++b) {
-              const int q = (a - 3 * dj + 2) * 5 + (b - 3 * dk + 2);
-              double x = X[a * 3 + b];
-              const double y = JAC ? Y[a * 3 + b] : 0.0;
-              if (c) {
-                const double w = wc[q];
-                const bool ctr = a == 0 && b == 0 && dj == 0 && dk == 0 && o == 0;
-                aR = aR + w * ((ctr && A.zc) ? 0.0 : x);
-                if (JAC) aS = aS + w * y;
+              for (int b = dk; b < 3; ++b) {
+                const int q = (a - 3 * dj + 2) * 5 + (b - 3 * dk + 2);
+                const double x = X[a * 3 + b];
+                const double y = JAC ? Y[a * 3 + b] : 0.0;
+                if (C) {
+                  const double w = wc[q];
+                  const bool ctr = a == 0 && b == 0 && dj == 0 && dk == 0;  // the coarse vertex itself (o = 0)
+                  aR = aR + w * ((ctr && o == 0 && A.zc) ? 0.0 : x);
+                  if (JAC) aS = aS + w * y;
+                }
+                if (NX) {
+                  const double w = wn[q];
+                  bR_ = bR_ + w * x;
+                  if (JAC) bS_ = bS_ + w * y;
+                }
               }
-              if (nx) {
-                const double w = wn[q];
-                bR_ = bR_ + w * x;
-                if (JAC) bS_ = bS_ + w * y;
-              }
-            }
-          acc[0][dj][dk][0] = aR;
-          acc[0][dj][dk][1] = aS;
-          acc[1][dj][dk][0] = bR_;
-          acc[1][dj][dk][1] = bS_;
-        }
+            acc[0][dj][dk][0] = aR;
+            acc[0][dj][dk][1] = aS;
+            acc[1][dj][dk][0] = bR_;
+            acc[1][dj][dk][1] = bS_;
+          }
+      };
+      using std::true_type;
+      using std::false_type;
+      if (c && nx) feed(true_type{}, true_type{});
+      else if (c) feed(true_type{}, false_type{});
+      else if (nx) feed(false_type{}, true_type{});
       if (o == 2) {
         // coarse plane m3 is complete: vertex (vj, vk) = (cjl - 1, ckl - 1) collects the partial sums of
         // its four cells -- along K from lane - 1 by shuffle, along J from the cell row below through
