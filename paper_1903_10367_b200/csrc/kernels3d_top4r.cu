@@ -54,44 +54,86 @@ __global__ void __launch_bounds__(kT4B, 2) k3_top4r(const __grid_constant__ Top3
   };
   if (col.lt == 0)
     for (int g = 0; g < kT4S; ++g) issue(g);
-  double U[3][(kT4R + 2) * 3], C[2][(kT4R + 1) * 2];
-  auto read_u = [&](int sl, double* u18) {
+  // Register window.  X[.]: a u plane's 4 x 3 neighbourhood of the thread's two vertices.  LS: per
+  // vertex and quadrant (s1, s2) the "L sum" of a plane, x(j+s1, k) + x(j, k+s2) + x(j+s1, k+s2) --
+  // the three vertices of that plane which the quadrant's cell couples to (j, k) with -1/12 from
+  // the planes i - 1 and i + 1 (in-line neighbours have weight 0).  A plane's L sums serve the
+  // vertex planes below and above it: they are formed once when the plane arrives (14 additions
+  // per two vertices, the column pair sums of rows (j, j+1) serve both), multiplied with the
+  // arriving cell plane for the vertex plane below, and once more with the next cell plane for the
+  // vertex plane above (TL, one partial sum per vertex carried to the next step).  The own plane
+  // contributes its four diagonal neighbours d with ep = e(i-1) + e(i):
+  //   E = sum ep,  T = sum_q e_m L_m + e_p L_p + ep d    (~27 fp64 operations per vertex; the
+  // cell-by-cell form element_ET spends 42).
+  double X[2][(kT4R + 2) * 3], LS[kT4R * 4], C[2][(kT4R + 1) * 2], TL[kT4R];
+  auto read_u = [&](int sl, double* u12) {
 #pragma unroll
     for (int r = 0; r < kT4R + 2; ++r)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) u18[r * 3 + c] = us[sl][(jj + r) * k2RowU + tx + c];
+      for (int c = 0; c < 3; ++c) u12[r * 3 + c] = us[sl][(jj + r) * k2RowU + tx + c];
   };
-  auto read_c = [&](int sl, double* c10) {
+  auto read_c = [&](int sl, double* c6) {
 #pragma unroll
     for (int r = 0; r < kT4R + 1; ++r)
 #pragma unroll
-      for (int c = 0; c < 2; ++c) c10[r * 2 + c] = cs[sl][(jj + r) * k2RowC + tx + c];
+      for (int c = 0; c < 2; ++c) c6[r * 2 + c] = cs[sl][(jj + r) * k2RowC + tx + c];
+  };
+  // l8[aa * 4 + q], q = 2 * (s1 > 0) + (s2 > 0)
+  auto lsums = [&](const double* u12, double* l8) {
+    double V[kT4R + 1][2];  // column pair sums of rows (r, r + 1) at columns k - 1, k + 1
+#pragma unroll
+    for (int r = 0; r < kT4R + 1; ++r) {
+      V[r][0] = u12[r * 3] + u12[(r + 1) * 3];
+      V[r][1] = u12[r * 3 + 2] + u12[(r + 1) * 3 + 2];
+    }
+#pragma unroll
+    for (int aa = 0; aa < kT4R; ++aa)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int up = q >> 1, rt = q & 1;
+        l8[aa * 4 + q] = u12[(aa + 2 * up) * 3 + 1] + V[aa + up][rt];
+      }
+  };
+  // sum_q c[cell of quadrant q] * l8[q] of vertex aa (cell window index (aa + up) * 2 + rt)
+  auto dotl = [&](const double* c6, const double* l8, int aa) {
+    double t = c6[aa * 2] * l8[aa * 4];
+    t = t + c6[aa * 2 + 1] * l8[aa * 4 + 1];
+    t = t + c6[aa * 2 + 2] * l8[aa * 4 + 2];
+    t = t + c6[aa * 2 + 3] * l8[aa * 4 + 3];
+    return t;
   };
   // prologue: packets 0 (u plane ia - 1) and 1 (u plane ia, cell plane ia - 1)
   mbar_wait(&bars[0], 0u);
-  read_u(0, U[0]);
+  read_u(0, X[1]);
+  lsums(X[1], LS);
   mbar_wait(&bars[1], 0u);
-  read_u(1, U[1]);
   read_c(1, C[0]);
+#pragma unroll
+  for (int aa = 0; aa < kT4R; ++aa) TL[aa] = dotl(C[0], LS, aa);
+  read_u(1, X[0]);
+  lsums(X[0], LS);
   __syncthreads();
   if (col.lt == 0) {
     fence_proxy_async();
     issue(3);
     issue(4);
   }
-  // step i (phase ph = (i - ia) % 6): packet g = i - ia + 2 in slot (ph + 2) % 3
+  // step i (phase ph = (i - ia) % 6): packet g = i - ia + 2 in slot (ph + 2) % 3; on entry X0 =
+  // u plane i, LS = its L sums, Cm = cell plane i - 1, TL = sum_q Cm L(i - 1)
   auto step = [&](auto PH, int i) {
     constexpr int ph = decltype(PH)::value;
     constexpr int sl = (ph + 2) % 3;
-    double* Um = U[ph % 3];
-    double* U0 = U[(ph + 1) % 3];
-    double* Up = U[(ph + 2) % 3];
+    double* X0 = X[ph % 2];
+    double* Xp = X[(ph + 1) % 2];
     double* Cm = C[ph % 2];
     double* C0 = C[(ph + 1) % 2];
     const int g = i - ia + 2;
     mbar_wait(&bars[sl], (unsigned)(g / kT4S) & 1u);
-    read_u(sl, Up);
     read_c(sl, C0);
+    double tn[kT4R];  // vertex plane i + 1's lower part: cell plane i with L(i)
+#pragma unroll
+    for (int aa = 0; aa < kT4R; ++aa) tn[aa] = dotl(C0, LS, aa);
+    read_u(sl, Xp);
     double rhs[kT4R];
 #pragma unroll
     for (int aa = 0; aa < kT4R; ++aa) rhs[aa] = rs[sl][(jj + aa) * k2RowR + tx + 1];
@@ -100,38 +142,39 @@ __global__ void __launch_bounds__(kT4B, 2) k3_top4r(const __grid_constant__ Top3
       fence_proxy_async();
       issue(g + kT4S);
     }
-    if (!live) return;
+    lsums(Xp, LS);
+    if (live) {
+      double ep[(kT4R + 1) * 2], er[kT4R + 1];
 #pragma unroll
-    for (int aa = 0; aa < kT4R; ++aa) {
-      if (j + aa > N - 2) continue;
-      double x[27], e[8];
+      for (int q = 0; q < (kT4R + 1) * 2; ++q) ep[q] = Cm[q] + C0[q];
 #pragma unroll
-      for (int r = 0; r < 3; ++r)
+      for (int r = 0; r < kT4R + 1; ++r) er[r] = ep[r * 2] + ep[r * 2 + 1];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          x[r * 3 + c] = Um[(aa + r) * 3 + c];
-          x[9 + r * 3 + c] = U0[(aa + r) * 3 + c];
-          x[18 + r * 3 + c] = Up[(aa + r) * 3 + c];
-        }
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {  // cell (i - bit0, j + aa - bit1, k - bit2)
-        const int c0b = c & 1, c1 = (c >> 1) & 1, c2 = c >> 2;
-        e[c] = (c0b ? Cm : C0)[(aa + 1 - c1) * 2 + 1 - c2];
+      for (int aa = 0; aa < kT4R; ++aa) {
+        if (j + aa > N - 2) continue;
+        const double E = er[aa] + er[aa + 1];
+        // own plane: diagonal neighbour of quadrant q at window row aa + 2 up, column 2 rt
+        double td = ep[aa * 2] * X0[aa * 3];
+        td = td + ep[aa * 2 + 1] * X0[aa * 3 + 2];
+        td = td + ep[aa * 2 + 2] * X0[(aa + 2) * 3];
+        td = td + ep[aa * 2 + 3] * X0[(aa + 2) * 3 + 2];
+        const double T = (TL[aa] + dotl(C0, LS, aa)) + td;
+        const double xc = X0[(aa + 1) * 3 + 1];
+        const double dg = K_D * E;
+        const double au = (dg * xc) - (K_E * T);
+        const double rho = rhs[aa] - au;
+        const double t = a.hw * rho;
+        s = s + t * t;
+        mx = fmax(mx, fabs(rho));
+        const size_t v = (size_t)i * NN + col_off + (size_t)aa * N;
+        const double gv = div_pos(a.w * rho, dg);
+        if (a.u_out) a.u_out[v] = xc + gv;
+        else a.g[v] = gv;
+        if (a.rho) a.rho[v] = rho;
       }
-      double E, T;
-      element_ET(x, e, E, T);
-      const double dg = K_D * E;
-      const double au = (dg * x[13]) - (K_E * T);
-      const double rho = rhs[aa] - au;
-      const double t = a.hw * rho;
-      s = s + t * t;
-      mx = fmax(mx, fabs(rho));
-      const size_t v = (size_t)i * NN + col_off + (size_t)aa * N;
-      const double gv = (a.w * rho) / dg;
-      if (a.u_out) a.u_out[v] = x[13] + gv;
-      else a.g[v] = gv;
-      if (a.rho) a.rho[v] = rho;
     }
+#pragma unroll
+    for (int aa = 0; aa < kT4R; ++aa) TL[aa] = tn[aa];
   };
   for (int i0 = ia; i0 < ib; i0 += 6) {
     step(std::integral_constant<int, 0>{}, i0);

@@ -20,7 +20,7 @@ cp $G/launches_config5.csv $P/${R}_config5_launches_dram.csv
 cp $G/traffic.json $P/traffic.json
 cp $G/smoke.log $P/${R}_smoke.txt
 tail -3 $G/pytest_gpu.log > $P/${R}_pytest_gpu.txt
-for k in k3_top4r k3_smr k3_up_dict k3_rap_y k3_rap_out; do
+for k in k3_top4r k3_smc k3_up_dict k3_rap_y k3_rap_out; do
   if [ -f $G/prof_$k.ncu-rep ]; then
     { echo "ncu --set full --clock-control none, one launch of $k, config 5 (python tools/run_cycles.py config5 3)";
       python tools/ncu_brief.py $G/prof_$k.ncu-rep; echo; echo "hottest source lines (instructions / stall samples):";
@@ -29,24 +29,5 @@ for k in k3_top4r k3_smr k3_up_dict k3_rap_y k3_rap_out; do
 done
 # SASS instruction census of the default config-5 kernels (TMA, bulk copies, fp64 FMA)
 { echo "cuobjdump -sass paper_1903_10367_b200/libtmg.so: instruction counts per kernel";
-  cuobjdump -sass paper_1903_10367_b200/libtmg.so | python - <<'PY'
-import re, sys, collections
-cur, cnt = None, collections.OrderedDict()
-for line in sys.stdin:
-    m = re.search(r"Function : (\S+)", line)
-    if m:
-        cur = m.group(1); cnt[cur] = collections.Counter(); continue
-    if cur:
-        m = re.search(r"^\s+/\*[0-9a-f]+\*/\s+(?:@!?U?P\d+\s+)?([A-Z0-9_.]+)", line)
-        if m:
-            op = m.group(1).split(".")[0]
-            cnt[cur][op] += 1
-want = ("k3_top4r", "k3_smr", "k3_up_dict", "k3_up_tma", "k3_down_c", "k3_rap_y", "k3_rap_out", "k3_up_lin", "k3_top2")
-ops = ("UTMALDG", "UTMASTG", "UTMAPF", "UBLKCP", "SYNCS", "DFMA", "DMUL", "DADD", "LDS", "STS", "LDG", "STG", "BAR")
-print(f"{'kernel':64s} " + " ".join(f"{o:>7s}" for o in ops))
-for k, c in cnt.items():
-    if any(w in k for w in want):
-        print(f"{k[:64]:64s} " + " ".join(f"{c.get(o, 0):7d}" for o in ops))
-PY
-} > $P/${R}_sass_census.txt
+  cuobjdump -sass paper_1903_10367_b200/libtmg.so | python tools/sass_census.py; } > $P/${R}_sass_census.txt
 ls $P | grep $R

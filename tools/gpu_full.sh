@@ -16,7 +16,7 @@ CMD="python bench.py --steps 3 --warmup 3 --no-cpu --no-ttt"
 $CMD > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_config5.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "ncu rc=$?"
 python tools/traffic.py gpurun_out/launches_config5.csv config5 6 gpurun_out/traffic.json
 CMD="python tools/run_cycles.py config5 3"
-for kv in "k3_smr 1" "k3_up_dict 1" "k3_top4r 1" "k3_rap_y 0" "k3_rap_out 0"; do
+for kv in "k3_smc 1" "k3_up_dict 1" "k3_top4r 1" "k3_rap_y 0" "k3_rap_out 0"; do
   set -- $kv
   ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c 1 -f -o gpurun_out/prof_$1 $CMD > gpurun_out/ncu_$1.log 2>&1; echo "ncu $1 rc=$?"
 done

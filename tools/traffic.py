@@ -49,7 +49,7 @@ for e in seq[starts[-2] if len(starts) > 1 else starts[-1]:]:
             break
         cur = top
         name = f"k3_down_L{top}"
-    elif fn.startswith("k3_smooth") or fn == "k3_smr":
+    elif fn.startswith("k3_smooth") or fn in ("k3_smr", "k3_smc"):
         name = f"k3_smooth_L{cur}"
     elif fn == "k3_down_c":
         cur -= 1
