@@ -58,7 +58,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     procs = []
     for src, extra in UNITS:
         obj = os.path.join(OBJDIR, src.replace(".cu", ".o"))
-        cmd = [nvcc(), *NVCC_FLAGS, *extra, *inc, "-c", "-o", obj, os.path.join(CSRC, src)]
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, *os.environ.get("TMG_NVCC_FLAGS", "").split(), *inc, "-c", "-o", obj,
+               os.path.join(CSRC, src)]
         procs.append((obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
     report, objs = [], []
     for obj, p in procs:

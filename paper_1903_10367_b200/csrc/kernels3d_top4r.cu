@@ -3,20 +3,23 @@
 //
 // Its predecessor (four rows per thread, no window) re-read the three u planes and two cell planes
 // of every step from the shared-memory ring: 19.5 shared loads per vertex, l1tex 75 % busy, 161
-// registers at 3 CTAs per SM, 2.79 ms at config 5.  Here a thread keeps u planes i-1, i and cell
-// plane i-1 of its 4 x 3 / 3 x 2 window in registers and reads only the arriving packet {u plane
-// i+1, cell plane i, rhs plane i} (12 + 6 + 2 loads per 2 vertices = 10 per vertex).  A packet's
-// slot is free as soon as it has been read, so a three-slot ring (42 KB per CTA) keeps as many
-// planes in flight as the five-slot ring did.  The step loop is unrolled by 6 = lcm(3, 2): the
-// u / cell window rotation is compile-time renaming, no register moves.  Measured at config 5:
-// two rows at 2 CTAs x 256 threads per SM (128 registers) 2.70 ms; four rows at 3 x 128 threads
-// (168 registers, 388 bytes of spills) 3.16 ms, at 2 x 128 threads (206 registers) 3.03 ms.  Per
-// vertex the expression is element_ET's.
+// registers at 3 CTAs per SM, 2.79 ms at config 5.  Here a thread keeps what it needs of u planes
+// i - 1, i and cell plane i - 1 in registers and reads only the arriving packet {u plane i + 1, cell
+// plane i, rhs plane i} (12 + 6 + 2 loads per 2 vertices = 10 per vertex); the step loop is unrolled
+// by 2 (the window's double buffers are compile-time renaming), the ring slot is a run-time index.
+// The operator is evaluated plane-wise instead of cell by cell (see "Register window" below):
+// ~27 fp64 operations per vertex instead of element_ET's 42, 2.69 -> 2.47 ms at config 5.
+// Measured alternatives: four rows at 3 x 128 threads (168 registers, 388 bytes of spills) 3.16 ms,
+// at 2 x 128 threads (206 registers) 3.03 ms; warps decoupled by per-slot empty barriers instead of
+// the per-step __syncthreads 0.04 ms slower.
 #include "kernels3d.cuh"
 
 namespace t3 {
 
-constexpr int kT4S = 3;  // packets in flight
+// ring slots: a slot is refilled with the packet kT4S ahead as soon as the CTA has read it.  Measured
+// per config-5 cycle: 3 slots 7.31 ms, 4 slots 7.25 ms, 5 / 6 / 7 slots 7.54 / 7.80 / 7.87 ms (more
+// planes in flight per CTA spread the 296 resident columns over more DRAM pages and L2 sets).
+constexpr int kT4S = 4;
 constexpr size_t kTop4rSmem = sizeof(double) * kT4S * (k2SlotU + k2SlotC + k2SlotR);
 
 constexpr int kT4R = 2;                                   // rows per thread
@@ -42,15 +45,24 @@ __global__ void __launch_bounds__(kT4B, 2) k3_top4r(const __grid_constant__ Top3
     mbar_fence_init();
   }
   __syncthreads();
-  // packet g = {u plane ia - 1 + g, cell plane ia - 2 + g, rhs plane ia - 2 + g}, g = 0 .. ib - ia + 1
+  // packet g = {u plane ia - 1 + g, cell plane ia - 2 + g, rhs plane ia - 2 + g}, g = 0 .. ib - ia + 1,
+  // in slot g % kT4S
   const int last = ib - ia + 1;
-  auto issue = [&](int g) {
+  auto issue = [&](int g) {  // thread 0
     if (g > last) return;
     const int sl = g % kT4S, pu = ia - 1 + g, pc = pu - 1;
     mbar_expect_tx(&bars[sl], k2BoxBytes + k2BoxBytesC + 8u * k2SlotR);
     tma_load_3d(us[sl], &a.tm, &bars[sl], col.k0 - 1, col.j0 - 1, pu);
     tma_load_3d(cs[sl], &a.tmc, &bars[sl], col.k0 - 1, col.j0 - 1, pc < 0 ? -1 : pc / a.crun);
     tma_load_3d(rs[sl], &a.tmr, &bars[sl], col.k0 - 1, col.j0, pc);
+  };
+  // the CTA has read the slot of packet g (and every earlier one): refill it
+  auto refill = [&](int g) {
+    __syncthreads();
+    if (col.lt == 0) {
+      fence_proxy_async();
+      issue(g + kT4S);
+    }
   };
   if (col.lt == 0)
     for (int g = 0; g < kT4S; ++g) issue(g);
@@ -108,27 +120,24 @@ __global__ void __launch_bounds__(kT4B, 2) k3_top4r(const __grid_constant__ Top3
   lsums(X[1], LS);
   mbar_wait(&bars[1], 0u);
   read_c(1, C[0]);
+  read_u(1, X[0]);
+  refill(0);
+  refill(1);
 #pragma unroll
   for (int aa = 0; aa < kT4R; ++aa) TL[aa] = dotl(C[0], LS, aa);
-  read_u(1, X[0]);
   lsums(X[0], LS);
-  __syncthreads();
-  if (col.lt == 0) {
-    fence_proxy_async();
-    issue(3);
-    issue(4);
-  }
-  // step i (phase ph = (i - ia) % 6): packet g = i - ia + 2 in slot (ph + 2) % 3; on entry X0 =
+  // step i (phase ph = (i - ia) % 2): packet g = i - ia + 2 in slot sl (parity par); on entry X0 =
   // u plane i, LS = its L sums, Cm = cell plane i - 1, TL = sum_q Cm L(i - 1)
+  int sl = 2 % kT4S;
+  unsigned par = 0u;
   auto step = [&](auto PH, int i) {
     constexpr int ph = decltype(PH)::value;
-    constexpr int sl = (ph + 2) % 3;
     double* X0 = X[ph % 2];
     double* Xp = X[(ph + 1) % 2];
     double* Cm = C[ph % 2];
     double* C0 = C[(ph + 1) % 2];
     const int g = i - ia + 2;
-    mbar_wait(&bars[sl], (unsigned)(g / kT4S) & 1u);
+    mbar_wait(&bars[sl], par);
     read_c(sl, C0);
     double tn[kT4R];  // vertex plane i + 1's lower part: cell plane i with L(i)
 #pragma unroll
@@ -137,10 +146,10 @@ __global__ void __launch_bounds__(kT4B, 2) k3_top4r(const __grid_constant__ Top3
     double rhs[kT4R];
 #pragma unroll
     for (int aa = 0; aa < kT4R; ++aa) rhs[aa] = rs[sl][(jj + aa) * k2RowR + tx + 1];
-    __syncthreads();  // the slot is read: refill it with packet g + 3
-    if (col.lt == 0) {
-      fence_proxy_async();
-      issue(g + kT4S);
+    refill(g);
+    if (++sl == kT4S) {
+      sl = 0;
+      par ^= 1u;
     }
     lsums(Xp, LS);
     if (live) {
@@ -176,13 +185,9 @@ __global__ void __launch_bounds__(kT4B, 2) k3_top4r(const __grid_constant__ Top3
 #pragma unroll
     for (int aa = 0; aa < kT4R; ++aa) TL[aa] = tn[aa];
   };
-  for (int i0 = ia; i0 < ib; i0 += 6) {
+  for (int i0 = ia; i0 < ib; i0 += 2) {
     step(std::integral_constant<int, 0>{}, i0);
     if (i0 + 1 < ib) step(std::integral_constant<int, 1>{}, i0 + 1);
-    if (i0 + 2 < ib) step(std::integral_constant<int, 2>{}, i0 + 2);
-    if (i0 + 3 < ib) step(std::integral_constant<int, 3>{}, i0 + 3);
-    if (i0 + 4 < ib) step(std::integral_constant<int, 4>{}, i0 + 4);
-    if (i0 + 5 < ib) step(std::integral_constant<int, 5>{}, i0 + 5);
   }
   __shared__ double red_s[kT4B / 32], red_m[kT4B / 32];
   for (int o = 16; o > 0; o >>= 1) {
