@@ -418,7 +418,7 @@ def run_ours(args, dist: Dist):
     n_fine = wl.fine_dofs()
 
     # ---- device-resident timing (value) ------------------------------------
-    eng = GpuEngine(wl.tree, SolverConfig(variant=wl.variant, flavor=wl.flavor), device=dev,
+    eng = GpuEngine(wl.tree, SolverConfig(variant=wl.variant, flavor=wl.flavor, fused_cycle=args.fused_cycle), device=dev,
                     sync="lazy")
     eng.rhs.update(wl.rhs)
     eng.advance_many(max(args.warmup, 3))
@@ -520,7 +520,7 @@ def run_ours(args, dist: Dist):
         pin = torch.empty(tree.u[l].shape, dtype=torch.float64, pin_memory=True).numpy()
         pin[...] = tree.u[l]
         tree.u[l] = pin
-    e2 = GpuEngine(tree, SolverConfig(variant=wl2.variant, flavor=wl2.flavor), device=dev,
+    e2 = GpuEngine(tree, SolverConfig(variant=wl2.variant, flavor=wl2.flavor, fused_cycle=args.fused_cycle), device=dev,
                    sync="eager")
     e2.rhs.update(wl2.rhs)
     for _ in range(max(args.warmup, 3)):
@@ -594,7 +594,7 @@ def run_sharded(args, dist: Dist):
     wl = workloads.by_name(args.workload)
     n_fine = wl.fine_dofs()
     pl = sharding.plan(wl.tree.depth, dist.ws)
-    eng = GpuEngine(wl.tree, SolverConfig(variant=wl.variant, flavor=wl.flavor), device=dev,
+    eng = GpuEngine(wl.tree, SolverConfig(variant=wl.variant, flavor=wl.flavor, fused_cycle=args.fused_cycle), device=dev,
                     sync="lazy")
     eng.rhs.update(wl.rhs)
     eng._flush_rhs()
@@ -696,6 +696,8 @@ def main():
                     help="--impl reference: largest sample whose K + W cycles fit this many seconds")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-1e-8 run")
+    ap.add_argument("--fused-cycle", action="store_true",
+                    help="2D: the whole cycle as one persistent cooperative launch (k_cycle)")
     ap.add_argument("--ttt-cap", type=int, default=200, help="cycle cap of the time-to-1e-8 run")
     ap.add_argument("--no-shard-graph", action="store_true",
                     help="sharded path: enqueue every phase and exchange from the host instead of replaying "

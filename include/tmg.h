@@ -71,6 +71,10 @@ typedef struct {
    * BoxMG P + Galerkin rows one level per cycle, finest first (the paper's
    * throttled setup; the reference builds all levels in rebuild()) */
   int32_t throttled;
+  /* 2D: run the whole cycle as ONE persistent cooperative launch (k_cycle: all levels' down
+   * sweeps, stats, carries, FAS injection and hanging refresh behind grid barriers) instead of
+   * one launch per level and sweep.  Same iterates; the residual norm's summation order differs. */
+  int32_t fused_cycle;
 } tmg_config;
 
 /* The spacetree data model, spacetree.py:86-120.  refined[l] for l < lmax

@@ -35,7 +35,7 @@ class Config(C.Structure):
     _fields_ = [("variant", C.c_int32), ("flavor", C.c_int32), ("omega", C.c_double),
                 ("omega_tilde", C.c_double), ("omega_hat", C.c_double),
                 ("damping_scale", C.c_double), ("rtilde_true_operator", C.c_int32),
-                ("device", C.c_int32), ("throttled", C.c_int32)]
+                ("device", C.c_int32), ("throttled", C.c_int32), ("fused_cycle", C.c_int32)]
 
 
 class Tree(C.Structure):

@@ -116,6 +116,10 @@ struct tmg_handle {
   size_t flush_bytes = 0;
   // coarse chain (cluster kernel) and its argument blocks
   int lc = 0, part_base = 0;
+  // fused cycle (k_cycle): per-warp stats partials, grid barrier words, persistent grid size
+  double* wpart = nullptr;
+  unsigned* bar = nullptr;
+  int cycle_grid = 0;
   unsigned long long* stamps = nullptr;  // k_coarse phase timestamps (diagnostics)
   double* scratch = nullptr;             // per-CTA residual partials of the cluster chain
 };
@@ -420,7 +424,54 @@ int enqueue_fas(tmg_handle* h) {
   return enqueue_hang(h);
 }
 
+// The whole cycle in one persistent cooperative launch (k_cycle, cfg.fused_cycle).
+int launch_cycle(tmg_handle* h) {
+  const int l0 = h->lmin, l1 = h->ltop;
+  tmg::CycleArgs a{};
+  a.l0 = l0;
+  a.ltop = l1;
+  a.do_up = 1;
+  a.hist = h->hist;
+  a.counter = h->counter;
+  a.cap = h->cap;
+  a.wpart = h->wpart;
+  a.bar = h->bar;
+  a.stamps = h->stamps;
+  for (int l = l0; l <= l1; ++l) {
+    Level& c = h->L[l];
+    const int k = l - l0;
+    a.down[k] = make_down(h, l, true);
+    a.up[k] = make_up(h, l);
+    a.tile_h[k] = c.tiles ? c.tile_h : 1;
+    a.units[k] = c.tiles ? c.ntiles * c.tile_h : c.N * (int)tiles_x(c.N);
+    if (c.cnt[tmg::K_HANG] > 0) {
+      a.hang_lv[a.nhang++] = k;
+      a.hang[k].u = c.u;
+      a.hang[k].flags = c.flags;
+      a.hang[k].N = c.N;
+      a.hang[k].uc = (l == l0) ? h->u_below : h->L[l - 1].u;
+      a.hang[k].Nc = (l == l0) ? h->N_below : h->L[l - 1].N;
+    }
+  }
+  cudaEvent_t e0 = nullptr;
+  TRY(begin_k(h, "k_cycle", &e0));
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((unsigned)h->cycle_grid);
+  lc.blockDim = dim3(tmg::kTileX, tmg::kTileY);
+  lc.stream = h->s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&lc, tmg::k_cycle, a));
+  CKL();
+  TRY(end_k(h, "k_cycle", e0));
+  return TMG_OK;
+}
+
 int enqueue_cycle(tmg_handle* h) {
+  if (h->cfg.fused_cycle) return launch_cycle(h);
   TRY(enqueue_down(h, true));  // includes the coarse chain (down, stats, up)
   for (int l = h->lc + 1; l <= h->ltop; ++l) {
     tmg::UpArgs a = make_up(h, l);
@@ -729,6 +780,17 @@ int build(tmg_handle* h, const tmg_tree* t) {
   CK(cudaMemcpyAsync(h->u_below, t->u[l0 - 1], sizeof(double) * h->N_below * h->N_below,
                      cudaMemcpyHostToDevice, h->s));
   h->part_base = parts;
+  if (h->cfg.fused_cycle) {
+    if (l1 - l0 + 1 > tmg::kCycleLevels) return fail(TMG_EINVAL, "fused cycle: too many levels");
+    int occ = 0, sms = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tmg::k_cycle, tmg::kBlock, 0));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->cfg.device));
+    if (occ < 1) return fail(TMG_ECUDA, "k_cycle does not fit an SM");
+    h->cycle_grid = occ * sms;
+    TRY(dalloc(h, &h->wpart, (size_t)2 * h->cycle_grid * tmg::kCycleWarps));
+    TRY(dalloc(h, &h->bar, 2));
+    CK(cudaMemsetAsync(h->bar, 0, 2 * sizeof(unsigned), h->s));
+  }
   TRY(dalloc(h, &h->stamps, 64));
   TRY(dalloc(h, &h->scratch, 2 * tmg::kClusterCTAs));
   h->nparts = parts;

@@ -1022,6 +1022,143 @@ __global__ void __launch_bounds__(kCoarseBlock) k_coarse_cl(const __grid_constan
   }
 }
 
+// ---------------------------------------------------------------------------
+// The fused cycle: one persistent launch (cooperative: every CTA resident), grid barriers between
+// the level phases.  The barrier is a self-resetting arrival counter + generation word (release /
+// acquire at gpu scope, bar.sync on both sides), so plain (L1-cached) loads after it observe what
+// any CTA wrote before it; every work vector is written in one phase and only read in later ones.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks, unsigned& gen) {
+  __syncthreads();  // the CTA's writes happen-before thread 0's release below (bar.sync is cumulative)
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    unsigned old, cur;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    if (old == nblocks - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(bar), "r"(0u) : "memory");
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(gen + 1u) : "memory");
+    } else {
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+      } while (cur == gen);
+    }
+  }
+  ++gen;
+  __syncthreads();
+}
+
+// unit w of a level -> vertex (i, j) of this lane: a row of 32 vertices of the dense array, or of
+// a listed tile
+__device__ __forceinline__ void unit_vertex(const uint32_t* tiles, int tile_h, int N, int w, int lane, int& i,
+                                            int& j) {
+  if (tiles) {
+    const int e = w / tile_h, r = w - e * tile_h;
+    const uint32_t t = tiles[e];
+    i = (int)(t >> 16) * tile_h + r;
+    j = (int)(t & 0xffffu) * kTileX + lane;
+  } else {
+    const int tx = (N + kTileX - 1) / kTileX;
+    i = w / tx;
+    j = (w - i * tx) * kTileX + lane;
+  }
+}
+
+#ifndef CYC_MINB
+#define CYC_MINB 1
+#endif
+__global__ void __launch_bounds__(kBlock, CYC_MINB) k_cycle(const __grid_constant__ CycleArgs a) {
+  __shared__ double rs[kCycleWarps], rm[kCycleWarps];
+  const int tid = threadIdx.y * kTileX + threadIdx.x, lane = tid & 31;
+  const int gw = blockIdx.x * kCycleWarps + (tid >> 5), nw = gridDim.x * kCycleWarps;
+  const unsigned nb = gridDim.x;
+  // the barrier's generation word cannot advance before this CTA's first arrival: read it once
+  unsigned gen;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(a.bar + 1) : "memory");
+  int nst = 0;
+  auto stamp = [&]() {
+    if (a.stamps && blockIdx.x == 0 && tid == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.stamps[nst] = t;
+    }
+    ++nst;
+  };
+  stamp();
+  double s = 0.0, m = 0.0;
+  for (int l = a.ltop; l >= a.l0; --l) {
+    const DownArgs& d = a.down[l - a.l0];
+    const int th = a.tile_h[l - a.l0], nu = a.units[l - a.l0];
+    for (int w = gw; w < nu; w += nw) {
+      int i, j;
+      unit_vertex(d.tiles, th, d.N, w, lane, i, j);
+      if (i < d.N && j < d.N) {
+        if (d.is_top) down_vertex<LdGen, 1>(d, i, j, s, m);
+        else down_vertex<LdGen, 0>(d, i, j, s, m);
+      }
+    }
+    if (l == a.l0) {  // this warp's share of the composite residual norm
+      for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_down_sync(0xffffffffu, s, o);
+        m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+      }
+      if (lane == 0) {
+        a.wpart[2 * gw] = s;
+        a.wpart[2 * gw + 1] = m;
+      }
+    }
+    grid_barrier(a.bar, nb, gen);
+    stamp();
+  }
+  if (blockIdx.x == 0) {  // fixed-order reduction of the warps' partials -> history slot
+    double x = 0.0, y = 0.0;
+    for (int k = tid; k < nw; k += kBlock) {
+      x += __ldcg(a.wpart + 2 * k);
+      y = fmax(y, __ldcg(a.wpart + 2 * k + 1));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      x += __shfl_down_sync(0xffffffffu, x, o);
+      y = fmax(y, __shfl_down_sync(0xffffffffu, y, o));
+    }
+    if (lane == 0) { rs[tid >> 5] = x; rm[tid >> 5] = y; }
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0, u = 0.0;
+      for (int k = 0; k < kCycleWarps; ++k) { t += rs[k]; u = fmax(u, rm[k]); }
+      const int slot = *a.counter;
+      a.hist[2 * (slot % a.cap)] = sqrt(t);
+      a.hist[2 * (slot % a.cap) + 1] = u;
+      *a.counter = slot + 1;
+    }
+  }
+  stamp();
+  if (!a.do_up) return;
+  for (int l = a.l0; l <= a.ltop; ++l) {
+    const UpArgs& u = a.up[l - a.l0];
+    const int th = a.tile_h[l - a.l0], nu = a.units[l - a.l0];
+    for (int w = gw; w < nu; w += nw) {
+      int i, j;
+      unit_vertex(u.tiles, th, u.N, w, lane, i, j);
+      if (i < u.N && j < u.N) up_vertex<LdGen>(u, i, j);
+    }
+    if (l < a.ltop || a.nhang) grid_barrier(a.bar, nb, gen);
+    stamp();
+  }
+  for (int q = 0; q < a.nhang; ++q) {  // hanging refresh, coarse to fine (solvers.py:292-296)
+    const int li = a.hang_lv[q];
+    const HangArgs& hg = a.hang[li];
+    const int th = a.tile_h[li], nu = a.units[li];
+    const uint32_t* tiles = a.up[li].tiles;
+    for (int w = gw; w < nu; w += nw) {
+      int i, j;
+      unit_vertex(tiles, th, hg.N, w, lane, i, j);
+      if (i < hg.N && j < hg.N) {
+        const size_t v = (size_t)i * hg.N + j;
+        if ((hg.flags[v] & 7) == K_HANG) hg.u[v] = prolong_dlinear_at<LdGen>(hg.uc, hg.Nc, i, j);
+      }
+    }
+    if (q + 1 < a.nhang) grid_barrier(a.bar, nb, gen);
+    stamp();
+  }
+}
+
 // FAS injection (solvers.py:283-288), standalone update_fas_state()
 __global__ void k_inject_u(double* __restrict__ uc, const uint8_t* __restrict__ flags_c, int Nc,
                            const double* __restrict__ uf, int Nf) {

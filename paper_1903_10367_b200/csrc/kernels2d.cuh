@@ -91,6 +91,35 @@ struct CoarseArgs {
   UpArgs up[kMaxChain];
 };
 
+// The whole additive cycle in ONE persistent launch (north star: "one fused kernel launch per
+// additive cycle that updates all levels"; the sweep order is pipeline.py:242-386's / solvers.py:
+// 345-395's): every level's down sweep, the stats finalisation, every level's carry + update + FAS
+// injection and the hanging-vertex refresh, separated by grid-wide barriers.  A unit of work is one
+// warp row (32 consecutive vertices of a vertex row: of the dense array, or of a patch-list tile).
+constexpr int kCycleLevels = 10;
+constexpr int kCycleWarps = kBlock / 32;
+struct HangArgs {
+  double* u;
+  const uint8_t* flags;
+  int N, Nc;
+  const double* uc;
+};
+struct CycleArgs {
+  int l0, ltop, do_up, nhang;
+  double* hist;
+  int* counter;
+  int cap;
+  double* wpart;       // one (sum, max) pair per warp of the grid
+  unsigned* bar;       // grid barrier: {arrival count, generation}
+  unsigned long long* stamps;  // optional %globaltimer stamp per phase (CTA 0; diagnostics)
+  int units[kCycleLevels];   // warp rows per level (index l - l0)
+  int tile_h[kCycleLevels];  // rows per patch-list tile (levels with a list)
+  int hang_lv[kCycleLevels]; // levels with hanging vertices, ascending (index l - l0)
+  DownArgs down[kCycleLevels];
+  UpArgs up[kCycleLevels];
+  HangArgs hang[kCycleLevels];
+};
+
 __global__ void k_flags(uint8_t* flags, int n, const uint8_t* ref_prev, const uint8_t* ref_cur);
 __global__ void k_take(uint8_t* flags_c, int Nc, const uint8_t* flags_f, int Nf);
 __global__ void k_eff(double* eff, double* epsm, double* reff, const double* eps,
@@ -118,6 +147,7 @@ __global__ void k_down(const __grid_constant__ DownArgs a);
 __global__ void k_up(const __grid_constant__ UpArgs a);
 __global__ void k_coarse(const __grid_constant__ CoarseArgs a);
 __global__ void k_coarse_cl(const __grid_constant__ CoarseArgs a, double* scratch);
+__global__ void k_cycle(const __grid_constant__ CycleArgs a);
 __global__ void k_inject_u(double* uc, const uint8_t* flags_c, int Nc, const double* uf, int Nf);
 __global__ void k_hang(double* u, const uint8_t* flags, int N, const double* uc, int Nc);
 

@@ -51,6 +51,11 @@ class SolverConfig:
     # BoxMG, 3D: d-linear start, BoxMG P + Galerkin rows one level per cycle
     # (the paper's throttled setup; not in the reference, which builds eagerly)
     throttled: bool = False
+    # 2D: the whole cycle as ONE persistent cooperative launch (k_cycle: every level's down sweep,
+    # stats, carries, injection and hanging refresh behind grid barriers) instead of one launch per
+    # level and sweep.  Same iterates; measured slower than the level launches on the BASELINE
+    # configs, so it is opt-in.  Not in the reference (blueprint: pipeline.py)
+    fused_cycle: bool = False
 
     def __post_init__(self):
         if self.variant not in VARIANTS:
@@ -185,7 +190,8 @@ class GpuEngine:
                            math.nan if c.omega_tilde is None else float(c.omega_tilde),
                            float(c.omega_hat), float(c.damping_scale),
                            1 if c.rtilde_true_operator else 0, int(self.device),
-                           1 if getattr(c, "throttled", False) else 0)
+                           1 if getattr(c, "throttled", False) else 0,
+                           1 if getattr(c, "fused_cycle", False) else 0)
 
     def _create(self) -> None:
         L = _abi.lib()

@@ -26,9 +26,9 @@ GPU_CASES = [n for n in case_names(full_only=True) if not n.endswith("_v10")]
 RTOL_HIST = 1e-10
 
 
-def gpu_run(case, sync="eager"):
+def gpu_run(case, sync="eager", **kw):
     tree = case.build_tree(Spacetree)
-    eng = GpuEngine(tree, SolverConfig(**case.cfg), sync=sync)
+    eng = GpuEngine(tree, SolverConfig(**case.cfg, **kw), sync=sync)
     for l, b in case.rhs().items():
         eng.rhs[l] = b
     if case.meta["fas_first"]:
@@ -177,6 +177,44 @@ def test_degenerate_collapse_raises_arithmetic_error():
     tree.eps[2][:, :] = 0.0  # zero material everywhere on the fine level -> det == 0
     with pytest.raises(ArithmeticError):
         GpuEngine(tree, SolverConfig(variant="adafac-jac", flavor="boxmg"))
+
+
+@pytest.mark.parametrize("name", GPU_CASES)
+def test_fused_cycle_matches_reference(name):
+    """SolverConfig(fused_cycle=True): the whole cycle as one persistent cooperative launch
+    (k_cycle, grid barriers between the level phases; the sweep of pipeline.py:242-386 /
+    solvers.py:345-395) reproduces the reference run like the level-by-level launches do --
+    iterates bit-identical for the geometric flavour -- with one kernel launch per cycle."""
+    case = load(name)
+    tree, eng, hist = gpu_run(case, sync="lazy", fused_cycle=True)
+    assert eng.launches_per_cycle() == 1
+    boxmg = case.cfg.get("flavor") == "boxmg"
+    rt = RTOL_HIST if boxmg else 1e-13
+    np.testing.assert_allclose([s.l2h for s in hist], case["l2h"], rtol=rt, atol=0)
+    np.testing.assert_allclose([s.linf for s in hist], case["linf"], rtol=rt, atol=0)
+    assert [s.updates for s in hist] == case["updates"].tolist()
+    for l in case.levels_with("u_"):
+        want = case[f"u_{l}"]
+        if boxmg:
+            assert np.abs(tree.u[l] - want).max() <= 1e-10 * max(np.abs(want).max(), 1e-300), f"u level {l}"
+        else:
+            assert np.array_equal(tree.u[l], want), f"u level {l} not bitwise equal"
+
+
+def test_fused_cycle_config4_equals_level_launches():
+    """BASELINE config 4 (patch lists, hanging vertices on four levels): the one-launch cycle's
+    iterate is bitwise the level-by-level launches' after 10 cycles."""
+    us = []
+    for fused in (False, True):
+        wl = workloads.config4()
+        eng = GpuEngine(wl.tree, SolverConfig(variant=wl.variant, flavor=wl.flavor, fused_cycle=fused), sync="lazy")
+        eng.rhs.update(wl.rhs)
+        hist = eng.advance_many(10)
+        eng.pull()
+        us.append(([s.l2h for s in hist], [wl.tree.u[l].copy() for l in range(eng.lmin, eng.ltop + 1)]))
+    np.testing.assert_allclose(us[0][0], us[1][0], rtol=1e-13)
+    for a, b in zip(us[0][1], us[1][1]):
+        assert np.array_equal(a, b)
 
 
 def test_config4_full_size_against_reference():
