@@ -599,7 +599,8 @@ def run_sharded(args, dist: Dist):
     eng.rhs.update(wl.rhs)
     eng._flush_rhs()
     sh = sharding.GpuShard(eng, pl, dist.rank)
-    se = sharding.ShardedEngine3([sh], sharding.DistTransport(pl, dist.rank), wl.variant)
+    se = sharding.ShardedEngine3([sh], sharding.DistTransport(pl, dist.rank), wl.variant,
+                                 split=True if args.force_split else None)
     st = sh.stream
     with torch.cuda.stream(st):
         se.cycle()  # eager once (NCCL channels, lazily allocated buffers), then the captured graphs
@@ -702,6 +703,9 @@ def main():
     ap.add_argument("--no-shard-graph", action="store_true",
                     help="sharded path: enqueue every phase and exchange from the host instead of replaying "
                          "the captured CUDA graphs")
+    ap.add_argument("--force-split", action="store_true",
+                    help="sharded path at one rank: run the split (edge planes / exchange / inner planes) "
+                         "schedule that ranks with neighbours run")
     ap.add_argument("--force-shard", action="store_true",
                     help="3D: run the sharded (NCCL) path even on one rank (testing)")
     args = ap.parse_args()

@@ -150,6 +150,13 @@ int tmg_dim(tmg_handle* h);
 #define TMG_F_PART 5 /* 2 doubles: sum of squares, max (all-reduced across ranks) */
 int tmg3_shard(tmg_handle* h, int32_t ls, const int32_t* lo, const int32_t* hi);
 int tmg3_phase(tmg_handle* h, int32_t phase, int32_t level);
+/* TMG_PH_DOWN / TMG_PH_UP of a sharded level restricted to the owned planes inside [lo, hi): the
+ * host splits a phase into the planes a neighbour rank needs (computed first, their halo exchange
+ * started) and the rest (computed while the exchange is in flight).  `first` / `last` mark the
+ * first / last part of the phase in this cycle (residual partials restart at the first part; the
+ * finest level's double buffer flips after the last). */
+int tmg3_phase_range(tmg_handle* h, int32_t phase, int32_t level, int32_t lo, int32_t hi, int32_t first,
+                     int32_t last);
 /* *out = 1 when the sharded cycle of level `level` runs TMG_PH_SMR instead of TMG_PH_SMOOTH */
 int tmg3_fused(tmg_handle* h, int32_t level, int32_t* out);
 /* device address and element count of a field of a level (zero-copy views) */

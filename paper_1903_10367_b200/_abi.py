@@ -27,7 +27,7 @@ EXPORTS = ("tmg_create", "tmg_rebuild", "tmg_set_rhs", "tmg_set_u", "tmg_get_u",
            "tmg_update_fas_state", "tmg_cycle", "tmg_residual_stats", "tmg_levels",
            "tmg_level_counts", "tmg_level_tiles", "tmg_get_kinds", "tmg_get_table", "tmg_time_cycles",
            "tmg_profile_cycles", "tmg_launches_per_cycle", "tmg_destroy", "tmg_last_error",
-           "tmg_device_count", "tmg3_create", "tmg3_rebuild", "tmg_dim", "tmg3_shard", "tmg3_phase",
+           "tmg_device_count", "tmg3_create", "tmg3_rebuild", "tmg_dim", "tmg3_shard", "tmg3_phase", "tmg3_phase_range",
            "tmg3_field", "tmg3_stream", "tmg3_history", "tmg3_storage", "tmg3_fused", "tmg3_cycle_state")
 
 
@@ -94,6 +94,7 @@ def lib() -> C.CDLL:
         "tmg_dim": ([H], C.c_int),
         "tmg3_shard": ([H, C.c_int32, P(C.c_int32), P(C.c_int32)], C.c_int),
         "tmg3_phase": ([H, C.c_int32, C.c_int32], C.c_int),
+        "tmg3_phase_range": ([H, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32], C.c_int),
         "tmg3_field": ([H, C.c_int32, C.c_int32, P(C.c_uint64), P(C.c_int64)], C.c_int),
         "tmg3_stream": ([H, P(C.c_uint64)], C.c_int),
         "tmg3_storage": ([H, C.c_int32, P(C.c_int64)], C.c_int),

@@ -944,6 +944,13 @@ int tmg3_phase(tmg_handle* h, int32_t phase, int32_t level) {
   return e3_phase(h->e3, phase, level, g_err);
 }
 
+int tmg3_phase_range(tmg_handle* h, int32_t phase, int32_t level, int32_t lo, int32_t hi, int32_t first,
+                     int32_t last) {
+  DeviceGuard dg_(h);
+  if (!h || !h->e3) return fail(TMG_EINVAL, "null argument or not a 3D handle");
+  return e3_phase_range(h->e3, phase, level, lo, hi, first, last, g_err);
+}
+
 int tmg3_field(tmg_handle* h, int32_t field, int32_t level, uint64_t* ptr, int64_t* count) {
   DeviceGuard dg_(h);
   if (!h || !h->e3 || !ptr || !count) return fail(TMG_EINVAL, "null argument or not a 3D handle");

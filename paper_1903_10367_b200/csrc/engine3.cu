@@ -111,6 +111,9 @@ struct Engine3 {
   std::vector<int> own_blocks2, own_chunk2;  // two-row kernels (k3_top2 / k3_smooth2r)
   double* red = nullptr;            // {sum, max} of this cycle's stats
   int top_parts = 0;
+  // tmg3_phase_range: the part of the owned planes the current phase call works on
+  int rng_lo = 0, rng_hi = 1 << 30;
+  bool rng_first = true, rng_last = true;
   // finest level double buffered (pp): the down sweep writes u + g of the finest level into
   // the other buffer (g never reaches HBM) and the up sweep adds P carry there; ubuf[par]
   // holds the current iterate, one captured graph per parity
@@ -1291,6 +1294,9 @@ void tiling(int N, int ilo, int ihi, int* chunk, int* blocks, int ty = kSY) {
 
 int interior_lo(Engine3* e, int l) { return std::max(1, e->own_lo[l]); }
 int interior_hi(Engine3* e, int l) { return std::min(e->L[l].N - 1, e->own_hi[l]); }
+// ... clipped to the part a tmg3_phase_range call names (DOWN / UP only)
+int part_lo(Engine3* e, int l) { return std::max(interior_lo(e, l), e->rng_lo); }
+int part_hi(Engine3* e, int l) { return std::min(interior_hi(e, l), e->rng_hi); }
 
 // sharded cycle: level l's adaFACx smoothing runs fused with the restriction into l - 1 (k3_smr
 // over the owned coarse planes of l - 1, phase TMG_PH_SMR) -- the grid levels above the shard
@@ -1307,23 +1313,30 @@ int phase3(Engine3* e, int phase, int l) {
   switch (phase) {
     case TMG_PH_DOWN: {
       if (l < e->ls || l > e->ltop) return fail3(e, TMG_EINVAL, "DOWN: level is not sharded");
-      const int lo = interior_lo(e, l), hi = interior_hi(e, l);
+      const int lo = part_lo(e, l), hi = part_hi(e, l);
+      if (l == e->ltop && e->rng_first) e->top_parts = 0;
       if (hi <= lo) return TMG_OK;
       Lvl3& c = e->L[l];
       if (l == e->ltop) {
         Top3 a = make_top(e, l);
         a.ilo = lo;
         a.ihi = hi;
+        // the part's own column chunks; its residual partials follow those of the earlier parts
+        int blocks = e->own_blocks2[l];
         a.chunk = e->own_chunk2[l];
-        e->top_parts = e->own_blocks2[l];
+        if (lo != interior_lo(e, l) || hi != interior_hi(e, l)) tiling(c.N, lo, hi, &a.chunk, &blocks, k2Y);
+        if (e->top_parts + blocks > e->nparts) return fail3(e, TMG_EINVAL, "DOWN: too many parts of the finest level");
+        a.part_sum += e->top_parts;
+        a.part_max += e->top_parts;
+        e->top_parts += blocks;
         cudaEvent_t e0_ = nullptr;
         TRY3(begin_k(e, &e0_));
         if (c.op.kind == OP_CONST)
-          k3_top2<OP_CONST><<<e->own_blocks2[l], dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
+          k3_top2<OP_CONST><<<blocks, dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
         else if (use_top4(a))
-          k3_top4r<<<e->own_blocks2[l], dim3(kSX, k2Y / kT4R), kTop4rSmem, e->s>>>(a);
+          k3_top4r<<<blocks, dim3(kSX, k2Y / kT4R), kTop4rSmem, e->s>>>(a);
         else
-          k3_top2<OP_ELEMENT><<<e->own_blocks2[l], dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
+          k3_top2<OP_ELEMENT><<<blocks, dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
         CKL3();
         TRY3(end_k(e, kname("k3_down", l), e0_));
       } else if (fused3(e, l + 1)) {  // restrictions formed by TMG_PH_SMR of level l + 1
@@ -1411,8 +1424,11 @@ int phase3(Engine3* e, int phase, int l) {
     }
     case TMG_PH_UP: {
       if (l < e->ls || l > e->ltop) return fail3(e, TMG_EINVAL, "UP: level is not sharded");
-      const int lo = interior_lo(e, l), hi = interior_hi(e, l);
-      if (hi <= lo) return TMG_OK;
+      const int lo = part_lo(e, l), hi = part_hi(e, l);
+      if (hi <= lo) {
+        if (l == e->ltop && e->rng_last) pp_advance(e);
+        return TMG_OK;
+      }
       Up3 a = make_up(e, l);
       a.ilo = lo;
       a.ihi = hi;
@@ -1423,7 +1439,7 @@ int phase3(Engine3* e, int phase, int l) {
         LAUNCH3(kname("k3_up", l), k3_up, e->L[l].grid, blk, a);
       } else if (boxmg) TRY3(launch_up_boxmg(e, l, a));
       else TRY3(launch_up_lin(e, l, a));
-      if (l == e->ltop) pp_advance(e);  // the buffer just completed is the iterate (TMG_F_U names it)
+      if (l == e->ltop && e->rng_last) pp_advance(e);  // the buffer just completed is the iterate (TMG_F_U names it)
       return TMG_OK;
     }
     case TMG_PH_INJECT: {
@@ -1462,6 +1478,10 @@ int e3_shard(Engine3* e, int ls, const int32_t* lo, const int32_t* hi, std::stri
     tiling(e->L[l].N, a, std::max(a + 1, b), &e->own_chunk2[l], &e->own_blocks2[l], k2Y);
     maxb = std::max(maxb, std::max(e->own_blocks[l], e->own_blocks2[l]));
   }
+  {  // tmg3_phase_range: up to four parts of the finest level, each with at most its own chunks
+    const int N = e->L[e->ltop].N;
+    maxb += 4 * ((N - 2 + kSX - 1) / kSX) * ((N - 2 + k2Y - 1) / k2Y) * 8;
+  }
   e->ls = ls;
   e->sharded = true;
   if (maxb > e->nparts) {
@@ -1477,13 +1497,27 @@ int e3_shard(Engine3* e, int ls, const int32_t* lo, const int32_t* hi, std::stri
 int e3_phase(Engine3* e, int phase, int level, std::string& err) {
   ErrScope es(e, err);
   if (!e->sharded) return fail3(e, TMG_EINVAL, "handle is not sharded (tmg3_shard)");
-  if (phase == TMG_PH_DOWN && level == e->ltop && e->thr_next >= e->lmin) {
+  if (phase == TMG_PH_DOWN && level == e->ltop && e->rng_first && e->thr_next >= e->lmin) {
     // throttled setup at the start of a sharded cycle; every rank holds the full operators
     TRY3(boxmg_level(e, e->thr_next));
     TRY3(check_degenerate(e));
     --e->thr_next;
   }
   return phase3(e, phase, level);
+}
+
+int e3_phase_range(Engine3* e, int phase, int level, int lo, int hi, int first, int last, std::string& err) {
+  ErrScope es(e, err);
+  if (phase != TMG_PH_DOWN && phase != TMG_PH_UP) return fail3(e, TMG_EINVAL, "phase ranges: DOWN and UP only");
+  e->rng_lo = lo;
+  e->rng_hi = hi;
+  e->rng_first = first != 0;
+  e->rng_last = last != 0;
+  const int rc = e3_phase(e, phase, level, err);
+  e->rng_lo = 0;
+  e->rng_hi = 1 << 30;
+  e->rng_first = e->rng_last = true;
+  return rc;
 }
 
 int e3_fused(Engine3* e, int level, int32_t* out, std::string& err) {

@@ -30,6 +30,7 @@ int e3_profile_cycles(Engine3* e, int ncycles, int cap, const char** names, floa
 int e3_launches_per_cycle(Engine3* e, int32_t* n, std::string& err);
 int e3_shard(Engine3* e, int ls, const int32_t* lo, const int32_t* hi, std::string& err);
 int e3_phase(Engine3* e, int phase, int level, std::string& err);
+int e3_phase_range(Engine3* e, int phase, int level, int lo, int hi, int first, int last, std::string& err);
 int e3_field(Engine3* e, int field, int level, uint64_t* ptr, int64_t* count, std::string& err);
 int e3_storage(Engine3* e, int level, int64_t* out, std::string& err);
 int e3_fused(Engine3* e, int level, int32_t* out, std::string& err);

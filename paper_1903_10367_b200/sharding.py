@@ -9,14 +9,21 @@ below ``ls`` (a few MB) are replicated and computed redundantly on every
 rank.  One process per GPU; the reference is serial, so this
 module has no reference counterpart.
 
-Per cycle, phase by phase (``tmg3_phase``), with the data exchanges between
-phases:
+Per cycle, phase by phase (``tmg3_phase`` / ``tmg3_phase_range``), with the data exchanges
+between phases.  A phase whose result a neighbour needs is split: the planes the neighbour needs
+are computed first and their exchange is started, the rest of the owned planes is computed while
+the exchange is in flight (NCCL runs on its own stream; the engine's stream waits for it only
+where the received planes are read).
 
 ==========================  ==================================================
-phase                       exchange after it
+phase                       exchange
 ==========================  ==================================================
+(cycle start)               u_l, every sharded l, ONE batch: plane a-1 from
+                            r-1 and b from r+1 -- in flight during the first
+                            half of DOWN(ltop)'s inner planes
 DOWN(l), l = ltop..ls       rho_l: planes a-2, a-1 from rank r-1, b from r+1
-                            (a-3 .. a-1 and b when l is fused, below)
+  edge planes first         (a-3 .. a-1 and b when l is fused, below) -- in
+  then the inner planes     flight during the inner planes
 SMR(l) (adaFACx, l > ls,    -- (the smoothing of l runs fused with the
 tmg3_fused; else SMOOTH)    restriction into the owned planes of l-1: sm
                             never leaves the chip, DOWN(l-1) reads b_R, b_T)
@@ -25,10 +32,12 @@ SMOOTH(l) (adaFACx)         sm_l: planes a-2, a-1 from rank r-1
                             ls-1 restricts from them)
 REDUCE                      all-reduce (sum of squares, max) of the residual
 REPL (levels lmin..ls-1)    --
-UP(l), l = ls..ltop         before it: carry_{l-1} plane B from rank r+1
-(after all UP)              u_l: planes a-1 from r-1 and b from r+1, every l;
-                            all-gather u_ls, then INJECT into the replicated
-                            levels
+UP(l), l = ls..ltop         carry_l plane a to rank r-1 (read by its UP(l+1)):
+  plane a first, then the   in flight during the rest of UP(l)
+  rest
+(after all UP)              all-gather u_ls, then INJECT into the replicated
+                            levels (the u halos move at the next cycle's start;
+                            ``sync_halos`` moves them on demand)
 ==========================  ==================================================
 
 The exchanges are P2P send/recv and collectives on zero-copy torch views of
@@ -115,26 +124,36 @@ class DistTransport:
         import torch.distributed as dist
         self.dist, self.pl, self.rank = dist, pl, rank
 
-    def halo(self, views, level: int, w_dn: int, w_up: int) -> None:
-        """views[0]: this rank's (N,N,N) field view.  Receive w_dn planes below
-        the owned range from rank-1 and w_up above it from rank+1."""
+    def halo_begin(self, items):
+        """items: (views, level, w_dn, w_up) per field; views[0] is this rank's (N,N,N) view.
+        Start ONE batch that receives w_dn planes below the owned range from rank-1 and w_up
+        above it from rank+1 (and sends the matching owned planes), for every item.  The batch is
+        ordered after the work already enqueued on the current stream; returns the pending
+        requests for halo_end."""
         d, r, R = self.dist, self.rank, self.pl.world
-        v = views[0]
-        a, b = self.pl.rng(level, r)
         ops = []
-        if r > 0:
-            if w_up:
-                ops.append(d.P2POp(d.isend, v[a:a + w_up], r - 1))
-            if w_dn:
-                ops.append(d.P2POp(d.irecv, v[a - w_dn:a], r - 1))
-        if r < R - 1:
-            if w_dn:
-                ops.append(d.P2POp(d.isend, v[b - w_dn:b], r + 1))
-            if w_up:
-                ops.append(d.P2POp(d.irecv, v[b:b + w_up], r + 1))
-        if ops:
-            for req in d.batch_isend_irecv(ops):
-                req.wait()
+        for views, level, w_dn, w_up in items:
+            v = views[0]
+            a, b = self.pl.rng(level, r)
+            if r > 0:
+                if w_up:
+                    ops.append(d.P2POp(d.isend, v[a:a + w_up], r - 1))
+                if w_dn:
+                    ops.append(d.P2POp(d.irecv, v[a - w_dn:a], r - 1))
+            if r < R - 1:
+                if w_dn:
+                    ops.append(d.P2POp(d.isend, v[b - w_dn:b], r + 1))
+                if w_up:
+                    ops.append(d.P2POp(d.irecv, v[b:b + w_up], r + 1))
+        return d.batch_isend_irecv(ops) if ops else []
+
+    def halo_end(self, pending) -> None:
+        """The current stream (the host, on CPU) waits for the exchange."""
+        for req in pending:
+            req.wait()
+
+    def halo(self, views, level: int, w_dn: int, w_up: int) -> None:
+        self.halo_end(self.halo_begin([(views, level, w_dn, w_up)]))
 
     def gather(self, views, level: int) -> None:
         """Fill every interior plane of views[0] from its owner."""
@@ -173,16 +192,31 @@ class LocalTransport:
         if self.sync:
             self.sync()
 
-    def halo(self, views, level: int, w_dn: int, w_up: int) -> None:
+    def halo_begin(self, items):
+        """Snapshot the planes to be sent NOW (a plane computed after this call does not travel);
+        halo_end delivers them (a halo plane read before halo_end is stale) -- the semantics of
+        the asynchronous exchange, so the tests see a wrong split."""
         self._s()
         R = self.pl.world
-        for r in range(R):
-            a, b = self.pl.rng(level, r)
-            if r > 0 and w_dn:
-                views[r][a - w_dn:a] = views[r - 1][a - w_dn:a]
-            if r < R - 1 and w_up:
-                views[r][b:b + w_up] = views[r + 1][b:b + w_up]
+        out = []
+        for views, level, w_dn, w_up in items:
+            for r in range(R):
+                a, b = self.pl.rng(level, r)
+                if r > 0 and w_dn:
+                    out.append((views[r], a - w_dn, a, views[r - 1][a - w_dn:a].clone()))
+                if r < R - 1 and w_up:
+                    out.append((views[r], b, b + w_up, views[r + 1][b:b + w_up].clone()))
         self._s()
+        return out
+
+    def halo_end(self, pending) -> None:
+        self._s()
+        for dst, lo, hi, data in pending:
+            dst[lo:hi] = data
+        self._s()
+
+    def halo(self, views, level: int, w_dn: int, w_up: int) -> None:
+        self.halo_end(self.halo_begin([(views, level, w_dn, w_up)]))
 
     def gather(self, views, level: int) -> None:
         self._s()
@@ -248,8 +282,14 @@ class GpuShard:
             self._views[key] = torch.as_tensor(_CAI(p.value, shape), device=f"cuda:{self.eng.device}")
         return self._views[key]
 
-    def phase(self, ph: int, level: int = 0) -> None:
-        _abi.check(_abi.lib().tmg3_phase(self.eng._h, ph, level))
+    def phase(self, ph: int, level: int = 0, rng=None, first: bool = True, last: bool = True) -> None:
+        """One phase; ``rng = (lo, hi)`` restricts DOWN / UP to the owned planes inside it
+        (``first`` / ``last``: the first / last part of this phase in the cycle)."""
+        if rng is None:
+            _abi.check(_abi.lib().tmg3_phase(self.eng._h, ph, level))
+        else:
+            _abi.check(_abi.lib().tmg3_phase_range(self.eng._h, ph, level, int(rng[0]), int(rng[1]),
+                                                   1 if first else 0, 1 if last else 0))
 
     def state(self, new=None):
         """(cycles enqueued, parity of the finest level's double buffer); ``new`` sets it."""
@@ -285,11 +325,13 @@ class ShardedEngine3:
     per process), all of them with LocalTransport.
     """
 
-    def __init__(self, shards, transport, variant: str, lmin: int = 1):
+    def __init__(self, shards, transport, variant: str, lmin: int = 1, split: bool | None = None):
         self.shards, self.tr = shards, transport
         self.pl = shards[0].pl
         self.jac = variant == "adafac-jac"
         self.lmin = lmin
+        # split the phases a neighbour waits for (edge planes, exchange, inner planes)
+        self.split = self.pl.world > 1 if split is None else split
         self._fz = {}
         self._graphs = None
 
@@ -304,20 +346,69 @@ class ShardedEngine3:
             self._fz[level] = f.pop()
         return self._fz[level]
 
+    # -- split phases ---------------------------------------------------------------------
+    def _ranks(self):
+        return [s.rank for s in self.shards]
+
+    def _phase_parts(self, ph, level, parts, first, last):
+        """parts(rank) -> list of (lo, hi) plane ranges; one ranged phase call per range."""
+        for s in self.shards:
+            rs = [r for r in parts(s.rank) if r[1] > r[0]]
+            for k, r in enumerate(rs):
+                s.phase(ph, level, rng=r, first=first and k == 0, last=last and k == len(rs) - 1)
+
+    def _can_split(self, level, w_dn, w_up) -> bool:
+        if not self.split:
+            return False
+        return all(self.pl.interior(level, r)[1] - self.pl.interior(level, r)[0] >= w_dn + w_up + 2
+                   for r in range(self.pl.world))
+
+    def _down(self, l, w_dn, w_up, pend_u=None):
+        """DOWN(l) followed by the rho halo (w_dn planes below, w_up above).  Split: the planes a
+        neighbour receives -- the first w_up and the last w_dn owned planes -- first, then the
+        exchange in flight during the inner planes.  ``pend_u`` (finest level): the u halos started
+        at the top of the cycle; only the first and the last owned plane read them, so half of the
+        inner planes run before they are waited for."""
+        pl, tr = self.pl, self.tr
+        rho = self._views(_abi.F_RHO, l)
+        if not self._can_split(l, w_dn, w_up):
+            if pend_u is not None:
+                tr.halo_end(pend_u)
+            for s in self.shards:
+                s.phase(_abi.PH_DOWN, l)
+            tr.halo(rho, l, w_dn, w_up)
+            return
+        first = True
+        mid = {}
+        for r in range(pl.world):
+            a, b = pl.interior(l, r)
+            mid[r] = a + w_up + (b - w_dn - a - w_up) // 2 if pend_u is not None else a + w_up
+        if pend_u is not None:
+            self._phase_parts(_abi.PH_DOWN, l, lambda r: [(pl.interior(l, r)[0] + w_up, mid[r])], True, False)
+            first = False
+            tr.halo_end(pend_u)
+        self._phase_parts(_abi.PH_DOWN, l, lambda r: [(pl.interior(l, r)[0], pl.interior(l, r)[0] + w_up),
+                                                       (pl.interior(l, r)[1] - w_dn, pl.interior(l, r)[1])],
+                          first, False)
+        pend = tr.halo_begin([(rho, l, w_dn, w_up)])
+        self._phase_parts(_abi.PH_DOWN, l, lambda r: [(mid[r], pl.interior(l, r)[1] - w_dn)], False, True)
+        tr.halo_end(pend)
+
     def cycle(self) -> None:
         pl, tr = self.pl, self.tr
         ls, top = pl.ls, pl.depth
+        # the iterate's halo planes (of the previous cycle's update), every sharded level in one batch
+        pend_u = tr.halo_begin([(self._views(_abi.F_U, l), l, 1, 1) for l in range(ls, top + 1)])
         for l in range(top, ls - 1, -1):
-            for s in self.shards:
-                s.phase(_abi.PH_DOWN, l)
+            pu = pend_u if l == top else None
             if self.jac and l > ls and self._fused(l):
                 # smoothing fused with the restriction into l - 1 (sm stays on chip): rho needs
                 # the 3 planes below (sm of the 2 below) and 1 above, no sm halo
-                tr.halo(self._views(_abi.F_RHO, l), l, 3, 1)
+                self._down(l, 3, 1, pu)
                 for s in self.shards:
                     s.phase(_abi.PH_SMR, l)
                 continue
-            tr.halo(self._views(_abi.F_RHO, l), l, 2, 1)
+            self._down(l, 2, 1, pu)
             if self.jac:
                 for s in self.shards:
                     s.phase(_abi.PH_SMOOTH, l)
@@ -332,16 +423,32 @@ class ShardedEngine3:
         tr.reduce(self._views(_abi.F_PART, 0))
         for s in self.shards:
             s.phase(_abi.PH_REPL)
+        pend = None
         for l in range(ls, top + 1):
-            if l - 1 >= ls:
-                tr.halo(self._views(_abi.F_CARRY, l - 1), l - 1, 0, 1)
-            for s in self.shards:
-                s.phase(_abi.PH_UP, l)
-        for l in range(ls, top + 1):
-            tr.halo(self._views(_abi.F_U, l), l, 1, 1)
+            if pend is not None:
+                tr.halo_end(pend)  # carry_{l-1}: plane b from rank r+1
+                pend = None
+            if l < top and self._can_split(l, 0, 1):
+                # the first owned plane of carry_l goes to rank r-1 while the rest of UP(l) runs
+                self._phase_parts(_abi.PH_UP, l, lambda r: [(pl.interior(l, r)[0], pl.interior(l, r)[0] + 1)],
+                                  True, False)
+                pend = tr.halo_begin([(self._views(_abi.F_CARRY, l), l, 0, 1)])
+                self._phase_parts(_abi.PH_UP, l, lambda r: [(pl.interior(l, r)[0] + 1, pl.interior(l, r)[1])],
+                                  False, True)
+            else:
+                for s in self.shards:
+                    s.phase(_abi.PH_UP, l)
+                if l < top:
+                    pend = tr.halo_begin([(self._views(_abi.F_CARRY, l), l, 0, 1)])
         tr.gather(self._views(_abi.F_U, ls), ls)
         for s in self.shards:
             s.phase(_abi.PH_INJECT)
+
+    def sync_halos(self) -> None:
+        """Move the iterate's halo planes now (the cycle moves them at its start)."""
+        pl = self.pl
+        self.tr.halo_end(self.tr.halo_begin([(self._views(_abi.F_U, l), l, 1, 1)
+                                             for l in range(pl.ls, pl.depth + 1)]))
 
     def run(self, n: int):
         for _ in range(n):

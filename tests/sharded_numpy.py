@@ -46,10 +46,12 @@ class NumpyShard:
         return torch.from_numpy(arr)
 
     # -- helpers ----------------------------------------------------------------
-    def _own(self, l):
-        """slice of owned interior planes (i) and the interior (j, k) box."""
+    def _own(self, l, rng=None):
+        """slice of owned interior planes (i) -- inside rng when given -- and the interior (j, k) box."""
         lo, hi = self.pl.interior(l, self.rank)
-        return (slice(lo, hi), slice(1, -1), slice(1, -1))
+        if rng is not None:
+            lo, hi = max(lo, rng[0]), min(hi, rng[1])
+        return (slice(lo, max(lo, hi)), slice(1, -1), slice(1, -1))
 
     def _rhs(self, l):
         r = self.rhs.get(l)
@@ -60,7 +62,7 @@ class NumpyShard:
             return self.cfg.omega_hat ** (self.top - l)
         return self.cfg.omega
 
-    def _down(self, l, own):
+    def _down(self, l, own, first=True):
         e, cfg = self.e, self.cfg
         op = e.ops[l]
         dof = e.masks[l]["dof"]
@@ -91,8 +93,10 @@ class NumpyShard:
         if l == self.top:
             r = rho[own]
             hw = e.hw[l]
-            self.part[0] = float(((hw * r) ** 2).sum())
-            self.part[1] = float(np.abs(r).max()) if r.size else 0.0
+            if first:
+                self.part[:] = 0.0
+            self.part[0] += float(((hw * r) ** 2).sum())
+            self.part[1] = max(self.part[1], float(np.abs(r).max()) if r.size else 0.0)
 
     def _smooth(self, l, own):
         s = mg3d.apply_const(self.rho[l], 1.0)
@@ -122,11 +126,13 @@ class NumpyShard:
         return self.fuse and self.cfg.variant == "adafac-jac" and self.pl.ls < level <= self.top
 
     # -- phases -----------------------------------------------------------------
-    def phase(self, ph, level=0):
+    def phase(self, ph, level=0, rng=None, first=True, last=True):
         ls, top, l0 = self.pl.ls, self.top, self.l0
         full = (slice(1, -1),) * 3
+        if rng is not None:
+            assert ph in (_abi.PH_DOWN, _abi.PH_UP)
         if ph == _abi.PH_DOWN:
-            self._down(level, self._own(level))
+            self._down(level, self._own(level, rng), first)
         elif ph == _abi.PH_SMOOTH:
             if self.cfg.variant == "adafac-jac" and level > l0:
                 self._smooth(level, self._own(level))
@@ -145,9 +151,9 @@ class NumpyShard:
             for l in range(l0, ls):
                 self._up(l, full)
         elif ph == _abi.PH_UP:
-            own = self._own(level)
+            own = self._own(level, rng)
             self._up(level, own)
-            lo, hi = self.pl.interior(level, self.rank)
+            lo, hi = own[0].start, own[0].stop
             fine = self.t.u[level]
             for lc in range(level - 1, ls - 1, -1):
                 # walk-down: fine c-points in owned planes -> coarser sharded levels

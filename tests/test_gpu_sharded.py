@@ -111,5 +111,25 @@ def test_gpu_dist_transport_world1_nccl():
         eng.pull()
         np.testing.assert_allclose([s.l2h for s in h], [s.l2h for s in hs], rtol=1e-12)
         close(wl2.tree.u[4], wl.tree.u[4])
+        sh.close()
+        # the split schedule (edge planes, exchange, inner planes: tmg3_phase_range) forced on the
+        # single rank, eagerly and replayed from the captured CUDA graphs
+        wl3 = workloads.by_name("config5-L4")
+        eng3 = GpuEngine(wl3.tree, SolverConfig(variant=wl3.variant, flavor=wl3.flavor), sync="lazy")
+        eng3.rhs.update(wl3.rhs)
+        eng3._flush_rhs()
+        sh3 = sharding.GpuShard(eng3, pl, 0)
+        se3 = sharding.ShardedEngine3([sh3], sharding.DistTransport(pl, 0), wl3.variant, split=True)
+        with torch.cuda.stream(sh3.stream):
+            se3.cycle()
+            assert se3.capture()
+            se3.replay()
+            se3.replay()
+        torch.cuda.synchronize()
+        h3 = sh3.history(3)
+        eng3.pull()
+        np.testing.assert_allclose([s.l2h for s in h3], [s.l2h for s in hs], rtol=1e-12)
+        close(wl3.tree.u[4], wl.tree.u[4])
+        sh3.close()
     finally:
         dist.destroy_process_group()
