@@ -13,6 +13,10 @@
 //   rows(step)   one 992-byte bulk copy per distinct row, from L2
 //   u, g, carry  TMA boxes (evict-first in L2, so the dictionary stays)
 //
+// Measured and dropped: an L2 prefetch of a step's dictionary rows 4-5 steps ahead of their staging
+// copies (1.745 -> 1.88 ms: the kernel runs at the DRAM rate of its access pattern, 4.8 TB/s, and
+// the prefetches add traffic for row sets the stager would have kept).
+//
 // Warp-specialised: warp 6 is the producer -- it keeps the three rings (slots,
 // tables, rows) ahead of the consumers, and after the consumers of a step have
 // arrived on its `done` barrier stores the step's u with one TMA store and
