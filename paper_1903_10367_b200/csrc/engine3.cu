@@ -1669,8 +1669,12 @@ int e3_set_u(Engine3* e, int level, const double* u, std::string& err) {
   ErrScope es(e, err);
   TRY3(check_level(e, level));
   CK3(cudaMemcpyAsync(e->L[level].u, u, sizeof(double) * e->L[level].nv, cudaMemcpyHostToDevice, e->s));
-  if (e->pp && level == e->ltop)  // both buffers: the down sweep writes interior vertices only
-    CK3(cudaMemcpyAsync(e->ubuf[e->par ^ 1], u, sizeof(double) * e->L[level].nv, cudaMemcpyHostToDevice, e->s));
+  if (e->pp && level == e->ltop) {
+    // the other buffer takes the boundary (Dirichlet) values: the down sweep writes every interior vertex
+    const int N = e->L[level].N;
+    k3_copy_boundary<<<nblk((size_t)N * N), 256, 0, e->s>>>(e->ubuf[e->par ^ 1], e->L[level].u, N);
+    CKL3();
+  }
   CK3(cudaStreamSynchronize(e->s));
   return TMG_OK;
 }

@@ -447,6 +447,17 @@ __global__ void k3_inject(double* uc, int Nc, const double* uf, int Nf) {
   uc[vid(Nc, I, J, K)] = uf[vid(Nf, 3 * I, 3 * J, 3 * K)];
 }
 
+// the six boundary faces of an N^3 vertex array (the Dirichlet values), dst <- src
+__global__ void k3_copy_boundary(double* __restrict__ dst, const double* __restrict__ src, int N) {
+  const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (size_t)N * N) return;
+  const int a = (int)(q / N), b = (int)(q % N);
+  const size_t f[6] = {vid(N, 0, a, b), vid(N, N - 1, a, b), vid(N, a, 0, b),
+                       vid(N, a, N - 1, b), vid(N, a, b, 0), vid(N, a, b, N - 1)};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) dst[f[k]] = src[f[k]];
+}
+
 // ===========================================================================
 // setup
 // ===========================================================================
