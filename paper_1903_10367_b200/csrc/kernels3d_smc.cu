@@ -26,6 +26,9 @@
 // to 26 doubles so that a slice is a 16-byte-aligned 208-byte bulk copy): a step stages only the
 // two slices it multiplies (<= 13 KB) instead of whole rows for three coarse planes (100 KB), so
 // two CTAs fit an SM.  Summation order differs from the oracle's o-major order (3D bar: 1e-10).
+// The kernel needs its 168 registers (12 warps per SM): tiles of 5 / 6 coarse rows (7 / 8 warps per
+// CTA, so 128 registers and 320 bytes of spills in the step loop) measured 2.98 / 3.12 ms against
+// 1.97 ms at config 5; three rho slots instead of four change nothing.
 #include <cuda.h>
 
 #include <type_traits>
