@@ -164,7 +164,9 @@ int tmg3_field(tmg_handle* h, int32_t field, int32_t level, uint64_t* ptr, int64
 /* storage of level `level`'s BoxMG operators (no reference counterpart): out[0] rows of P
  * (coarse vertices), out[1] distinct rows in its row dictionary (0 = stored dense), out[2]
  * rows of the cube-owned copy Pc (coarse cubes; 0 = none), out[3] distinct rows of Pc's
- * dictionary, out[4] rows of the Galerkin table, out[5] distinct rows of its dictionary.
+ * dictionary, out[4] rows of the Galerkin table, out[5] rows its run-length form along k stores
+ * (kernels3d_rle.cu: only the rows that differ from their predecessor in a 32-vertex segment; 0 =
+ * dense planes only).
  * Dictionaries (lossless, bitwise-verified) are built at setup for levels ltop-1 (and
  * ltop-2) when rows repeat (piecewise-constant coefficients); TMG_PDICT=0 disables, 2 forces
  * them. */

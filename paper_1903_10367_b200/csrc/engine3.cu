@@ -22,6 +22,7 @@
 #include "kernels3d_dict.cu"
 #include "kernels3d_rap.cu"
 #include "kernels3d_uplin.cu"
+#include "kernels3d_rle.cu"
 
 namespace {
 
@@ -689,7 +690,8 @@ int enqueue_down(Engine3* e, bool write) {
       Down3 a = make_down(e, l, write);
       a.bR = c.bR;
       a.bT = c.bT;
-      if (jac) LAUNCH3(kname("k3_down", l), (k3_down_c<true, true, true>), c.c_grid, 128, a);
+      if (a.op.rtab && jac) LAUNCH3(kname("k3_down", l), (k3_down_c<true, true, true, true>), c.c_grid, 128, a);
+      else if (jac) LAUNCH3(kname("k3_down", l), (k3_down_c<true, true, true>), c.c_grid, 128, a);
       else LAUNCH3(kname("k3_down", l), (k3_down_c<true, false, true>), c.c_grid, 128, a);
     } else {
       Down3 a = make_down(e, l, write);
@@ -942,6 +944,57 @@ int refresh_pc(Engine3* e, int l) {
   return TMG_OK;
 }
 
+// Run-length form of level l's Galerkin table along k (kernels3d_rle.cu): the operator stream of
+// k3_down_c.  Kept when it stores less than 60 % of the dense rows.
+int build_rle(Engine3* e, int l) {
+  Lvl3& c = e->L[l];
+  c.op.rtab = nullptr;
+  const char* env = std::getenv("TMG_PDICT");
+  if (!c.tbl || c.N - 2 < 64 || (env && env[0] == '0')) return TMG_OK;
+  const bool force = env && env[0] == '2';
+  const int rseg = (c.N - 2 + 31) / 32;
+  const size_t segs = (size_t)c.N * c.N * rseg;
+  uint32_t *rmask = nullptr, *rcnt = nullptr, *rbase = nullptr;
+  TRY3(alloc3(e, &rmask, segs, false));
+  TRY3(alloc3(e, &rbase, segs + 1, false));
+  CK3(cudaMalloc(&rcnt, sizeof(uint32_t) * (segs + 1)));
+  void* tmp = nullptr;
+  auto done = [&](int rc) {
+    cudaFree(rcnt);
+    if (tmp) cudaFree(tmp);
+    return rc;
+  };
+#define CKR(x)                                                                  \
+  do {                                                                          \
+    cudaError_t e_ = (x);                                                       \
+    if (e_ != cudaSuccess) return done(fail3(e, TMG_ECUDA, cudaGetErrorString(e_))); \
+  } while (0)
+  CKR(cudaMemsetAsync(rcnt + segs, 0, sizeof(uint32_t), e->s));
+  k3_rle_mask<<<148 * 16, 256, 0, e->s>>>(c.tbl, c.N, rseg, rmask, rcnt);
+  CKR(cudaGetLastError());
+  size_t tb = 0;
+  CKR(cub::DeviceScan::ExclusiveSum(nullptr, tb, rcnt, rbase, segs + 1, e->s));
+  CKR(cudaMalloc(&tmp, tb));
+  CKR(cub::DeviceScan::ExclusiveSum(tmp, tb, rcnt, rbase, segs + 1, e->s));
+  uint32_t total = 0;
+  CKR(cudaMemcpyAsync(&total, rbase + segs, sizeof(uint32_t), cudaMemcpyDeviceToHost, e->s));
+  CKR(cudaStreamSynchronize(e->s));
+#undef CKR
+  const size_t interior = (size_t)(c.N - 2) * (c.N - 2) * (c.N - 2);
+  if (total == 0 || (!force && (double)total > 0.6 * (double)interior)) return done(TMG_OK);  // no runs: dense planes
+  double* rtab = nullptr;
+  if (alloc3(e, &rtab, (size_t)27 * total, false) != TMG_OK) return done(TMG_ECUDA);
+  k3_rle_fill<<<148 * 16, 256, 0, e->s>>>(c.tbl, c.N, rseg, rmask, rbase, total, rtab);
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(e->s) != cudaSuccess)
+    return done(fail3(e, TMG_ECUDA, "k3_rle_fill failed"));
+  c.op.rtab = rtab;
+  c.op.rbase = rbase;
+  c.op.rmask = rmask;
+  c.op.rn = total;
+  c.op.rseg = rseg;
+  return done(TMG_OK);
+}
+
 // Galerkin rows of level l's interior vertices (k3_rap_y + k3_rap_out over slabs of coarse planes;
 // the scratch Y holds 343 doubles per slab vertex, at most about 2 GB)
 int galerkin_rows(Engine3* e, int l, const Rows& raw) {
@@ -1095,6 +1148,8 @@ int build(Engine3* e, const tmg_tree3* t) {
       c.op.tbl = c.tbl;
       c.op.tdict = c.Td;  // (null = dense planes)
       c.op.tidx = c.Tdi;
+      // the table's run-length form (eager setup only: the throttled path rewrites the rows)
+      if (!cfg.throttled && l >= l1 - 2) TRY3(build_rle(e, l));
     }
     if (cfg.throttled) e->thr_next = l1 - 1;
   }
@@ -1345,7 +1400,8 @@ int phase3(Engine3* e, int phase, int l) {
         a.ihi = hi;
         a.bR = c.bR;
         a.bT = c.bT;
-        LAUNCH3(kname("k3_down", l), (k3_down_c<true, true, true>), c.c_grid, 128, a);
+        if (a.op.rtab) LAUNCH3(kname("k3_down", l), (k3_down_c<true, true, true, true>), c.c_grid, 128, a);
+        else LAUNCH3(kname("k3_down", l), (k3_down_c<true, true, true>), c.c_grid, 128, a);
       } else {
         Down3 a = make_down(e, l, true);
         a.ilo = lo;
@@ -1537,7 +1593,7 @@ int e3_storage(Engine3* e, int level, int64_t* out, std::string& err) {
   out[2] = c.Pc ? nc * nc * nc : 0;
   out[3] = c.Pcd ? (int64_t)c.Pcdn : 0;
   out[4] = c.tbl ? (int64_t)c.nv : 0;
-  out[5] = c.Td ? (int64_t)c.Tdn : 0;
+  out[5] = c.op.rtab ? (int64_t)c.op.rn : 0;
   return TMG_OK;
 }
 

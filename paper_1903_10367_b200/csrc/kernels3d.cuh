@@ -58,6 +58,16 @@ struct Op3 {
   // is tdict[tidx[v] * kDictW + t]
   const double* tdict;
   const uint32_t* tidx;
+  // table in run-length form along k (kernels3d_rle.cu; level ltop-1's Galerkin rows): a warp segment
+  // = 32 consecutive interior k of a vertex line; only the rows that differ bitwise from their
+  // predecessor in the segment are stored, SoA: tap t of stored row r is rtab[t * rn + r];
+  // segment s = (i * N + j) * rseg + (k - 1) / 32 has its first stored row at rbase[s] and a bit per
+  // lane that starts a new row in rmask[s]
+  const double* rtab;
+  const uint32_t* rbase;
+  const uint32_t* rmask;
+  size_t rn;
+  int rseg;
 };
 
 struct Grid {

@@ -629,19 +629,50 @@ __global__ void __launch_bounds__(kSB, 3) k3_smooth_s(const __grid_constant__ Sm
 // Coarse-level down sweep with the restriction of rho and (adaFACx) sm of the
 // finer level in one pass over the P planes.  Thread per interior vertex,
 // k fastest (P planes and coarse vectors coalesced).
-template <bool BOXMG, bool JAC, bool PRE = false>
+// RLE: the operator rows come from the run-length table (kernels3d_rle.cu); a warp then owns one
+// segment of 32 consecutive k of a line instead of 32 consecutive interior vertices.
+template <bool BOXMG, bool JAC, bool PRE = false, bool RLE = false>
 __global__ void __launch_bounds__(128) k3_down_c(const __grid_constant__ Down3 a) {
   const int N = a.N, n = N - 2;
-  const size_t cnt = (size_t)(a.ihi - a.ilo) * n * n;
+  const int rseg = RLE ? a.op.rseg : 1;
+  const size_t cnt = RLE ? (size_t)(a.ihi - a.ilo) * n * rseg * 32 : (size_t)(a.ihi - a.ilo) * n * n;
   double s = 0.0, m = 0.0;
   for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < cnt;
        q += (size_t)gridDim.x * blockDim.x) {
-    const int k = 1 + (int)(q % n);
-    const size_t r = q / n;
-    const int j = 1 + (int)(r % n), i = a.ilo + (int)(r / n);
+    int i, j, k;
+    if (RLE) {
+      const size_t w = q >> 5;
+      const int seg = (int)(w % rseg);
+      const size_t r = w / rseg;
+      k = 1 + 32 * seg + (int)(q & 31);
+      j = 1 + (int)(r % n);
+      i = a.ilo + (int)(r / n);
+      if (k > n) continue;
+    } else {
+      k = 1 + (int)(q % n);
+      const size_t r = q / n;
+      j = 1 + (int)(r % n);
+      i = a.ilo + (int)(r / n);
+    }
     const size_t v = vid(N, i, j, k);
     double au, dg;
-    op_apply<LdNC>(a.op, a.u, N, i, j, k, au, dg);
+    if (RLE) {
+      const size_t sg = ((size_t)i * N + j) * rseg + ((k - 1) >> 5);
+      const unsigned lane = (unsigned)(k - 1) & 31u;
+      const size_t row = __ldg(a.op.rbase + sg) + __popc(__ldg(a.op.rmask + sg) & (0xffffffffu >> (31u - lane))) - 1;
+      double x[27];
+      load27<LdNC>(a.u, N, v, x);
+      double acc = 0.0;
+#pragma unroll
+      for (int t = 0; t < 27; ++t) {
+        const double wt = __ldg(a.op.rtab + (size_t)t * a.op.rn + row);
+        if (t == 13) dg = wt;
+        acc = acc + wt * x[t];
+      }
+      au = acc;
+    } else {
+      op_apply<LdNC>(a.op, a.u, N, i, j, k, au, dg);
+    }
     const bool cpt0 = a.variant == VAR_AFACC;
     double bR, bT = 0.0;
     if (PRE) {  // restrictions already formed by the fused fine pass

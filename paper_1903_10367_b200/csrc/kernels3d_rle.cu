@@ -1,0 +1,67 @@
+// Run-length form of a level's 27-point table along k (level ltop-1's Galerkin rows, the operator
+// stream of k3_down_c).
+//
+// On piecewise-constant coefficients the Galerkin rows repeat in runs along every axis (config 5,
+// level 5: 14.5 M rows, 1.24 M distinct; along k a 9-vertex block period holds 3 runs).  A row
+// dictionary gathered per lane measured slower than the dense planes (a warp meets ~11 distinct
+// rows: one L1 tag cycle per distinct line and load, round 1).  Here the rows stay in vertex order
+// but each warp segment -- 32 consecutive interior k of a line (i, j) -- stores only the rows that
+// differ bitwise from their predecessor, structure-of-arrays, so the lanes of a warp read tap t from
+// one short contiguous run (~11 doubles instead of 32): the same coalesced plane loads as the dense
+// table on about a third of the bytes.  Lossless by construction (bitwise comparison of all 27
+// taps); lane 0 of a segment always starts a row.  Built once at setup; kept only when it stores
+// less than 60 % of the dense rows (random coefficients: no runs, the dense planes stay).
+#include "kernels3d.cuh"
+
+namespace t3 {
+
+// pass 1: one warp per segment of the interior lines; mask = lanes whose row differs from lane - 1's
+__global__ void k3_rle_mask(const double* __restrict__ tbl, int N, int rseg, uint32_t* __restrict__ rmask,
+                            uint32_t* __restrict__ rcnt) {
+  const size_t nv = (size_t)N * N * N;
+  const int n = N - 2;
+  const size_t segs = (size_t)N * N * rseg;
+  const int lane = threadIdx.x & 31;
+  for (size_t sg = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sg < segs;
+       sg += ((size_t)gridDim.x * blockDim.x) >> 5) {
+    const int seg = (int)(sg % rseg);
+    const size_t line = sg / rseg;
+    const int j = (int)(line % N), i = (int)(line / N);
+    const int k = 1 + 32 * seg + lane;
+    const bool interior = i >= 1 && i <= n && j >= 1 && j <= n;
+    const bool valid = interior && k <= n;
+    bool diff = false;
+    if (valid) {
+      diff = lane == 0;
+      const size_t v = ((size_t)i * N + j) * N + k;
+      if (!diff)
+        for (int t = 0; t < 27 && !diff; ++t)
+          diff = __double_as_longlong(tbl[(size_t)t * nv + v]) != __double_as_longlong(tbl[(size_t)t * nv + v - 1]);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, diff);
+    if (lane == 0) {
+      rmask[sg] = m;
+      rcnt[sg] = (uint32_t)__popc(m);
+    }
+  }
+}
+
+// pass 2 (rbase = exclusive scan of rcnt): the lanes that start a row store its 27 taps
+__global__ void k3_rle_fill(const double* __restrict__ tbl, int N, int rseg, const uint32_t* __restrict__ rmask,
+                            const uint32_t* __restrict__ rbase, size_t rn, double* __restrict__ rtab) {
+  const size_t nv = (size_t)N * N * N;
+  const size_t segs = (size_t)N * N * rseg;
+  const int lane = threadIdx.x & 31;
+  for (size_t sg = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sg < segs;
+       sg += ((size_t)gridDim.x * blockDim.x) >> 5) {
+    const unsigned m = rmask[sg];
+    if (!((m >> lane) & 1u)) continue;
+    const int seg = (int)(sg % rseg);
+    const size_t line = sg / rseg;
+    const size_t v = line * N + 1 + 32 * seg + lane;
+    const size_t r = rbase[sg] + __popc(m & ((1u << lane) - 1u));
+    for (int t = 0; t < 27; ++t) rtab[(size_t)t * rn + r] = tbl[(size_t)t * nv + v];
+  }
+}
+
+}  // namespace t3

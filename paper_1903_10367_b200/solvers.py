@@ -398,11 +398,12 @@ class GpuEngine:
 
     def weight_storage(self, level: int) -> dict:
         """3D: how level `level`'s BoxMG weights are stored (``tmg3_storage``): rows of P and
-        of its cube-owned copy, and the distinct rows of their dictionaries (0 = dense)."""
+        of its cube-owned copy, the distinct rows of their dictionaries (0 = dense), and the rows
+        the run-length form of the Galerkin table stores (0 = dense planes only)."""
         out = (C.c_int64 * 6)()
         _abi.check(_abi.lib().tmg3_storage(self._h, level, out))
         return {"p_rows": out[0], "p_distinct": out[1], "pc_rows": out[2], "pc_distinct": out[3],
-                "galerkin_rows": out[4], "galerkin_distinct": out[5]}
+                "galerkin_rows": out[4], "galerkin_stored": out[5]}
 
     def launches_per_cycle(self) -> int:
         n = C.c_int32()

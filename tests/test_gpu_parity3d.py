@@ -236,6 +236,7 @@ def test_3d_weight_dictionary_equals_dense(variant, wname, monkeypatch):
     wl1 = make()
     e1, h1 = gpu_run(wl1, n, variant)
     st = e1.weight_storage(4)
+    assert st["galerkin_stored"] > 0, st  # forced (TMG_PDICT=2) even without runs
     if wname == "config5-L5":
         assert 0 < st["p_distinct"] <= st["p_rows"], st
         assert 0 < st["pc_distinct"] <= st["pc_rows"], st
@@ -244,7 +245,7 @@ def test_3d_weight_dictionary_equals_dense(variant, wname, monkeypatch):
     monkeypatch.setenv("TMG_PDICT", "0")
     wl2 = make()
     e2, h2 = gpu_run(wl2, n, variant)
-    assert e2.weight_storage(4)["p_distinct"] == 0
+    assert e2.weight_storage(4)["p_distinct"] == 0 and e2.weight_storage(4)["galerkin_stored"] == 0
     np.testing.assert_allclose([s.l2h for s in h1], [s.l2h for s in h2], rtol=1e-12)
     np.testing.assert_allclose([s.linf for s in h1], [s.linf for s in h2], rtol=1e-12)
     for l in range(1, 6):
@@ -254,12 +255,13 @@ def test_3d_weight_dictionary_equals_dense(variant, wname, monkeypatch):
 def test_3d_weight_dictionary_default_on_blocks():
     """On blockwise-constant coefficients (config 5's structure) the default setup stores level
     ltop-1's weights (P for the restriction, the cube-owned copy for the prolongation) as
-    dictionaries: far fewer distinct rows than coarse vertices / cubes; the Galerkin rows stay
-    dense."""
+    dictionaries: far fewer distinct rows than coarse vertices / cubes; the Galerkin rows (the
+    operator stream of k3_down_c) are stored in run-length form along k."""
     wl = workloads.config5(levels=5, block=27)  # config 5's block size (9 level-4 cells)
     eng, _ = gpu_run(wl, 1)
     st = eng.weight_storage(wl.tree.depth - 1)
     print(st)
     assert 0 < st["p_distinct"] <= st["p_rows"] // 4, st
     assert 0 < st["pc_distinct"] <= st["pc_rows"] // 4, st
-    assert st["galerkin_distinct"] == 0, st
+    interior = (3 ** (wl.tree.depth - 1) - 1) ** 3
+    assert 0 < st["galerkin_stored"] <= 0.6 * interior, st
