@@ -660,16 +660,17 @@ __global__ void __launch_bounds__(128) k3_down_c(const __grid_constant__ Down3 a
       const size_t sg = ((size_t)i * N + j) * rseg + ((k - 1) >> 5);
       const unsigned lane = (unsigned)(k - 1) & 31u;
       const size_t row = __ldg(a.op.rbase + sg) + __popc(__ldg(a.op.rmask + sg) & (0xffffffffu >> (31u - lane))) - 1;
-      double x[27];
+      double x[27], w[27];
       load27<LdNC>(a.u, N, v, x);
+      const double* rt = a.op.rtab + row;
+      const size_t rn = a.op.rn;
+#pragma unroll
+      for (int t = 0; t < 27; ++t) w[t] = __ldg(rt + (size_t)t * rn);
       double acc = 0.0;
 #pragma unroll
-      for (int t = 0; t < 27; ++t) {
-        const double wt = __ldg(a.op.rtab + (size_t)t * a.op.rn + row);
-        if (t == 13) dg = wt;
-        acc = acc + wt * x[t];
-      }
+      for (int t = 0; t < 27; ++t) acc = acc + w[t] * x[t];
       au = acc;
+      dg = w[13];
     } else {
       op_apply<LdNC>(a.op, a.u, N, i, j, k, au, dg);
     }
