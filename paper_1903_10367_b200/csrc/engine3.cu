@@ -955,12 +955,14 @@ int build_rle(Engine3* e, int l) {
   const int rseg = (c.N - 2 + 31) / 32;
   const size_t segs = (size_t)c.N * c.N * rseg;
   uint32_t *rmask = nullptr, *rcnt = nullptr, *rbase = nullptr;
+  uint8_t* rdup = nullptr;
   TRY3(alloc3(e, &rmask, segs, false));
   TRY3(alloc3(e, &rbase, segs + 1, false));
   CK3(cudaMalloc(&rcnt, sizeof(uint32_t) * (segs + 1)));
   void* tmp = nullptr;
   auto done = [&](int rc) {
     cudaFree(rcnt);
+    if (rdup) cudaFree(rdup);
     if (tmp) cudaFree(tmp);
     return rc;
   };
@@ -969,8 +971,9 @@ int build_rle(Engine3* e, int l) {
     cudaError_t e_ = (x);                                                       \
     if (e_ != cudaSuccess) return done(fail3(e, TMG_ECUDA, cudaGetErrorString(e_))); \
   } while (0)
+  CKR(cudaMalloc(&rdup, segs));
   CKR(cudaMemsetAsync(rcnt + segs, 0, sizeof(uint32_t), e->s));
-  k3_rle_mask<<<148 * 16, 256, 0, e->s>>>(c.tbl, c.N, rseg, rmask, rcnt);
+  k3_rle_mask<<<148 * 16, 256, 0, e->s>>>(c.tbl, c.N, rseg, rmask, rcnt, rdup);
   CKR(cudaGetLastError());
   size_t tb = 0;
   CKR(cub::DeviceScan::ExclusiveSum(nullptr, tb, rcnt, rbase, segs + 1, e->s));
@@ -984,7 +987,8 @@ int build_rle(Engine3* e, int l) {
   if (total == 0 || (!force && (double)total > 0.6 * (double)interior)) return done(TMG_OK);  // no runs: dense planes
   double* rtab = nullptr;
   if (alloc3(e, &rtab, (size_t)27 * total, false) != TMG_OK) return done(TMG_ECUDA);
-  k3_rle_fill<<<148 * 16, 256, 0, e->s>>>(c.tbl, c.N, rseg, rmask, rbase, total, rtab);
+  k3_rle_fill<<<148 * 16, 256, 0, e->s>>>(c.tbl, c.N, rseg, rmask, rbase, rdup, total, rtab);
+  k3_rle_link<<<nblk((size_t)c.N * rseg, 128), 128, 0, e->s>>>(c.N, rseg, rdup, rbase);
   if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(e->s) != cudaSuccess)
     return done(fail3(e, TMG_ECUDA, "k3_rle_fill failed"));
   c.op.rtab = rtab;

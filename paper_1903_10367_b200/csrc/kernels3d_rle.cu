@@ -9,15 +9,18 @@
 // differ bitwise from their predecessor, structure-of-arrays, so the lanes of a warp read tap t from
 // one short contiguous run (~11 doubles instead of 32): the same coalesced plane loads as the dense
 // table on about a third of the bytes.  Lossless by construction (bitwise comparison of all 27
-// taps); lane 0 of a segment always starts a row.  Built once at setup; kept only when it stores
-// less than 60 % of the dense rows (random coefficients: no runs, the dense planes stay).
+// taps); lane 0 of a segment always starts a row.  A segment whose 32 rows equal those of the same
+// segment of the previous line (i, j - 1) stores nothing and points at that line's rows (inside an
+// eps block 5 of 9 lines do): consecutive lines are swept by neighbouring warps, so the repeats are
+// served by L2.  Built once at setup; kept only when it stores less than 60 % of the dense rows
+// (random coefficients: no runs, the dense planes stay).
 #include "kernels3d.cuh"
 
 namespace t3 {
 
 // pass 1: one warp per segment of the interior lines; mask = lanes whose row differs from lane - 1's
 __global__ void k3_rle_mask(const double* __restrict__ tbl, int N, int rseg, uint32_t* __restrict__ rmask,
-                            uint32_t* __restrict__ rcnt) {
+                            uint32_t* __restrict__ rcnt, uint8_t* __restrict__ rdup) {
   const size_t nv = (size_t)N * N * N;
   const int n = N - 2;
   const size_t segs = (size_t)N * N * rseg;
@@ -39,28 +42,52 @@ __global__ void k3_rle_mask(const double* __restrict__ tbl, int N, int rseg, uin
           diff = __double_as_longlong(tbl[(size_t)t * nv + v]) != __double_as_longlong(tbl[(size_t)t * nv + v - 1]);
     }
     const unsigned m = __ballot_sync(0xffffffffu, diff);
+    // the whole segment repeats the previous line's?
+    bool same = interior && j >= 2;
+    if (same && valid) {
+      const size_t v = ((size_t)i * N + j) * N + k;
+      for (int t = 0; t < 27 && same; ++t)
+        same = __double_as_longlong(tbl[(size_t)t * nv + v]) == __double_as_longlong(tbl[(size_t)t * nv + v - N]);
+    }
+    const bool dup = __all_sync(0xffffffffu, same);
     if (lane == 0) {
       rmask[sg] = m;
-      rcnt[sg] = (uint32_t)__popc(m);
+      rcnt[sg] = dup ? 0u : (uint32_t)__popc(m);
+      rdup[sg] = dup ? 1 : 0;
     }
   }
 }
 
 // pass 2 (rbase = exclusive scan of rcnt): the lanes that start a row store its 27 taps
 __global__ void k3_rle_fill(const double* __restrict__ tbl, int N, int rseg, const uint32_t* __restrict__ rmask,
-                            const uint32_t* __restrict__ rbase, size_t rn, double* __restrict__ rtab) {
+                            const uint32_t* __restrict__ rbase, const uint8_t* __restrict__ rdup, size_t rn,
+                            double* __restrict__ rtab) {
   const size_t nv = (size_t)N * N * N;
   const size_t segs = (size_t)N * N * rseg;
   const int lane = threadIdx.x & 31;
   for (size_t sg = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sg < segs;
        sg += ((size_t)gridDim.x * blockDim.x) >> 5) {
     const unsigned m = rmask[sg];
-    if (!((m >> lane) & 1u)) continue;
+    if (rdup[sg] || !((m >> lane) & 1u)) continue;
     const int seg = (int)(sg % rseg);
     const size_t line = sg / rseg;
     const size_t v = line * N + 1 + 32 * seg + lane;
     const size_t r = rbase[sg] + __popc(m & ((1u << lane) - 1u));
     for (int t = 0; t < 27; ++t) rtab[(size_t)t * rn + r] = tbl[(size_t)t * nv + v];
+  }
+}
+
+// pass 3: a repeated segment points at the rows of the nearest stored segment of the lines before it
+// (one thread per (i, segment) column walks j)
+__global__ void k3_rle_link(int N, int rseg, const uint8_t* __restrict__ rdup, uint32_t* __restrict__ rbase) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= N * rseg) return;
+  const int i = t / rseg, seg = t - i * rseg;
+  uint32_t last = 0u;
+  for (int j = 1; j <= N - 2; ++j) {
+    const size_t sg = ((size_t)i * N + j) * rseg + seg;
+    if (rdup[sg]) rbase[sg] = last;
+    else last = rbase[sg];
   }
 }
 
