@@ -973,7 +973,8 @@ int build_rle(Engine3* e, int l) {
   } while (0)
   CKR(cudaMalloc(&rdup, segs));
   CKR(cudaMemsetAsync(rcnt + segs, 0, sizeof(uint32_t), e->s));
-  k3_rle_mask<<<148 * 16, 256, 0, e->s>>>(c.tbl, c.N, rseg, rmask, rcnt, rdup);
+  const int planes = c.N - 2 <= kRleLink ? 1 : 0;  // plane repeats need the one-block-per-column link pass
+  k3_rle_mask<<<148 * 16, 256, 0, e->s>>>(c.tbl, c.N, rseg, planes, rmask, rcnt, rdup);
   CKR(cudaGetLastError());
   size_t tb = 0;
   CKR(cub::DeviceScan::ExclusiveSum(nullptr, tb, rcnt, rbase, segs + 1, e->s));
@@ -988,7 +989,8 @@ int build_rle(Engine3* e, int l) {
   double* rtab = nullptr;
   if (alloc3(e, &rtab, (size_t)27 * total, false) != TMG_OK) return done(TMG_ECUDA);
   k3_rle_fill<<<148 * 16, 256, 0, e->s>>>(c.tbl, c.N, rseg, rmask, rbase, rdup, total, rtab);
-  k3_rle_link<<<nblk((size_t)c.N * rseg, 128), 128, 0, e->s>>>(c.N, rseg, rdup, rbase);
+  if (planes) k3_rle_link2<<<rseg, kRleLink, 0, e->s>>>(c.N, rseg, rdup, rbase);
+  else k3_rle_link<<<nblk((size_t)c.N * rseg, 128), 128, 0, e->s>>>(c.N, rseg, rdup, rbase);
   if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(e->s) != cudaSuccess)
     return done(fail3(e, TMG_ECUDA, "k3_rle_fill failed"));
   c.op.rtab = rtab;

@@ -10,17 +10,19 @@
 // one short contiguous run (~11 doubles instead of 32): the same coalesced plane loads as the dense
 // table on about a third of the bytes.  Lossless by construction (bitwise comparison of all 27
 // taps); lane 0 of a segment always starts a row.  A segment whose 32 rows equal those of the same
-// segment of the previous line (i, j - 1) stores nothing and points at that line's rows (inside an
-// eps block 5 of 9 lines do): consecutive lines are swept by neighbouring warps, so the repeats are
-// served by L2.  Built once at setup; kept only when it stores less than 60 % of the dense rows
+// segment of the previous line (i, j - 1), or else of the previous plane (i - 1, j), stores nothing
+// and points at that segment's rows (inside an eps block 5 of 9 lines and 5 of 9 planes do):
+// consecutive lines are swept by neighbouring warps and a plane's stored rows are under a megabyte,
+// so the repeats are served by L2.  Built once at setup; kept only when it stores less than 60 % of the dense rows
 // (random coefficients: no runs, the dense planes stay).
 #include "kernels3d.cuh"
 
 namespace t3 {
 
 // pass 1: one warp per segment of the interior lines; mask = lanes whose row differs from lane - 1's
-__global__ void k3_rle_mask(const double* __restrict__ tbl, int N, int rseg, uint32_t* __restrict__ rmask,
-                            uint32_t* __restrict__ rcnt, uint8_t* __restrict__ rdup) {
+// rdup: 1 = the segment repeats (i, j - 1)'s, 2 = (i - 1, j)'s (tested when planes is set), 0 = stored
+__global__ void k3_rle_mask(const double* __restrict__ tbl, int N, int rseg, int planes,
+                            uint32_t* __restrict__ rmask, uint32_t* __restrict__ rcnt, uint8_t* __restrict__ rdup) {
   const size_t nv = (size_t)N * N * N;
   const int n = N - 2;
   const size_t segs = (size_t)N * N * rseg;
@@ -49,11 +51,21 @@ __global__ void k3_rle_mask(const double* __restrict__ tbl, int N, int rseg, uin
       for (int t = 0; t < 27 && same; ++t)
         same = __double_as_longlong(tbl[(size_t)t * nv + v]) == __double_as_longlong(tbl[(size_t)t * nv + v - N]);
     }
-    const bool dup = __all_sync(0xffffffffu, same);
+    int dup = __all_sync(0xffffffffu, same) ? 1 : 0;
+    if (!dup && planes) {
+      same = interior && i >= 2;
+      if (same && valid) {
+        const size_t v = ((size_t)i * N + j) * N + k;
+        const size_t NN = (size_t)N * N;
+        for (int t = 0; t < 27 && same; ++t)
+          same = __double_as_longlong(tbl[(size_t)t * nv + v]) == __double_as_longlong(tbl[(size_t)t * nv + v - NN]);
+      }
+      if (__all_sync(0xffffffffu, same)) dup = 2;
+    }
     if (lane == 0) {
       rmask[sg] = m;
       rcnt[sg] = dup ? 0u : (uint32_t)__popc(m);
-      rdup[sg] = dup ? 1 : 0;
+      rdup[sg] = (uint8_t)dup;
     }
   }
 }
@@ -88,6 +100,50 @@ __global__ void k3_rle_link(int N, int rseg, const uint8_t* __restrict__ rdup, u
     const size_t sg = ((size_t)i * N + j) * rseg + seg;
     if (rdup[sg]) rbase[sg] = last;
     else last = rbase[sg];
+  }
+}
+
+// pass 3 with plane repeats: one block per segment column, thread = line j, planes in order.  A
+// plane repeat takes the (already linked) base of (i - 1, j); a line repeat takes the base of the
+// nearest line before it that is not one (block-wide max scan of the line index).
+constexpr int kRleLink = 1024;
+__global__ void __launch_bounds__(kRleLink) k3_rle_link2(int N, int rseg, const uint8_t* __restrict__ rdup,
+                                                         uint32_t* __restrict__ rbase) {
+  __shared__ uint32_t sb[kRleLink];
+  __shared__ int wtop[kRleLink / 32];
+  const int seg = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int n = N - 2, j = tid + 1;
+  const bool on = j <= n;
+  for (int i = 1; i <= n; ++i) {
+    const size_t sg = ((size_t)i * N + j) * rseg + seg;
+    int d = 0;
+    uint32_t b = 0u;
+    if (on) {
+      d = rdup[sg];
+      b = d == 2 ? rbase[sg - (size_t)N * rseg] : rbase[sg];
+    }
+    sb[tid] = b;
+    int v = (on && d != 1) ? tid : -1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v = max(v, t);
+    }
+    if (lane == 31) wtop[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+      int w = wtop[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w = max(w, t);
+      }
+      wtop[lane] = w;
+    }
+    __syncthreads();
+    if (wid > 0) v = max(v, wtop[wid - 1]);
+    if (on && d) rbase[sg] = sb[v];
+    __syncthreads();
   }
 }
 
