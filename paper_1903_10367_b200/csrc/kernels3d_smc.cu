@@ -28,7 +28,9 @@
 // two CTAs fit an SM.  Summation order differs from the oracle's o-major order (3D bar: 1e-10).
 // The kernel needs its 168 registers (12 warps per SM): tiles of 5 / 6 coarse rows (7 / 8 warps per
 // CTA, so 128 registers and 320 bytes of spills in the step loop) measured 2.98 / 3.12 ms against
-// 1.97 ms at config 5; three rho slots instead of four change nothing.
+// 1.97 ms at config 5; three rho slots instead of four change nothing; the step unrolled by two with
+// the rho windows swapping roles (no copy of the window's centre, the sign of G folded into its
+// constants) 2.06 ms (20 bytes of spills).
 #include <cuda.h>
 
 #include <type_traits>
