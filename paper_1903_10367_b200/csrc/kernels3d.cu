@@ -178,6 +178,31 @@ __device__ __forceinline__ double restrict_P(const double* f, int Nf, const doub
   return acc;
 }
 
+// both restrictions of the adaFACx cycle (rho and the smoothed residual) in one pass over the 125
+// weights (each loaded once; the two sums keep restrict_P's order)
+template <class LD>
+__device__ __forceinline__ void restrict_P2(const double* f, const double* g, int Nf, const double* P, int Nc,
+                                            int I, int J, int K, bool cpt0, double& rf, double& rg) {
+  const size_t nvc = (size_t)Nc * Nc * Nc;
+  const size_t vc = vid(Nc, I, J, K);
+  const size_t fc = vid(Nf, 3 * I, 3 * J, 3 * K);
+  const long long sN = Nf, sNN = (long long)Nf * Nf;
+  double af = 0.0, ag = 0.0;
+#pragma unroll 25
+  for (int o = 0; o < 125; ++o) {
+    const int a = o / 25 - 2, b = (o / 5) % 5 - 2, c = o % 5 - 2;
+    const long long fo = (long long)fc + a * sNN + b * sN + c;
+    double x = LD::ld(f + fo);
+    const double y = LD::ld(g + fo);
+    const double w = (o == 62) ? 1.0 : LD::ld(P + (size_t)o * nvc + vc);
+    if (o == 62 && cpt0) x = 0.0;
+    af = af + w * x;
+    ag = ag + w * y;
+  }
+  rf = af;
+  rg = ag;
+}
+
 // mg3d.prolong_dlinear at fine vertex (i,j,k): axis 0, then 1, then 2,
 // wl*c[q] + (1-wl)*c[q+1] with wl = 1 - r/3.
 template <class CV>
@@ -234,13 +259,20 @@ __device__ __forceinline__ void down_vertex(const Down3& a, int i, int j, int k,
   double au, dg;
   op_apply<LD>(a.op, a.u, N, i, j, k, au, dg);
   const double rhs = a.rhs ? LD::ld(a.rhs + v) : 0.0;
-  double rho;
+  double rho, bt2 = 0.0;
+  bool have_bt = false;
   if (a.is_top) {
     rho = rhs - au;
   } else {
     const bool cpt0 = a.variant == VAR_AFACC;
-    double b = a.P ? restrict_P<LD>(a.rho_f, a.Nf, a.P, N, i, j, k, cpt0)
-                   : restrict_dlinear<LD>(a.rho_f, a.Nf, i, j, k, cpt0);
+    double b;
+    if (a.P && a.write && a.variant == VAR_JAC) {
+      restrict_P2<LD>(a.rho_f, a.sm_f, a.Nf, a.P, N, i, j, k, cpt0, b, bt2);
+      have_bt = true;
+    } else {
+      b = a.P ? restrict_P<LD>(a.rho_f, a.Nf, a.P, N, i, j, k, cpt0)
+              : restrict_dlinear<LD>(a.rho_f, a.Nf, i, j, k, cpt0);
+    }
     b = b + rhs;   // b[l] = R rho + rhs[l]   (solvers.py:370-371)
     b = b + au;    // + _bpart: overlapped -> A u (solvers.py:351-352)
     rho = b - au;
@@ -255,8 +287,9 @@ __device__ __forceinline__ void down_vertex(const Down3& a, int i, int j, int k,
     if (a.variant == VAR_BPX && !a.is_top) d = a.omega * rho;
     else d = (a.w * rho) / dg;
     if (a.variant == VAR_JAC && !a.is_top) {
-      const double bt = a.P ? restrict_P<LD>(a.sm_f, a.Nf, a.P, N, i, j, k, false)
-                            : restrict_dlinear<LD>(a.sm_f, a.Nf, i, j, k, false);
+      const double bt = have_bt ? bt2
+                        : a.P   ? restrict_P<LD>(a.sm_f, a.Nf, a.P, N, i, j, k, false)
+                                : restrict_dlinear<LD>(a.sm_f, a.Nf, i, j, k, false);
       d = d - a.ds * ((a.wt * bt) / dg);
     }
     a.g[v] = d;
