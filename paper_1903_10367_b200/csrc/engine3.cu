@@ -594,11 +594,11 @@ int launch_smc(Engine3* e, int l, bool smooth, int clo, int chi) {
   A.tilesK = (nk + kCK - 1) / kCK;
   A.tilesJ = (nk + kCJ - 1) / kCJ;
   const int tiles = A.tilesK * A.tilesJ;
-  int best = 1;  // coarse-plane chunks: about a whole number of waves of two CTAs per SM
+  int best = 1;  // coarse-plane chunks: about a whole number of waves of kCPerSM CTAs per SM
   double best_eff = 0.0;
   for (int nch = 1; nch <= std::min(n, 32); ++nch) {
     const int chunk = (n + nch - 1) / nch, nb = tiles * ((n + chunk - 1) / chunk);
-    const double waves = (double)nb / (2 * num_sms());
+    const double waves = (double)nb / (kCPerSM * num_sms());
     const double eff = waves / std::ceil(waves) * (double)chunk / (chunk + 1.0);
     if (eff > best_eff + 1e-9) { best_eff = eff; best = nch; }
   }

@@ -18,17 +18,20 @@
 //     loads instead of ~144.
 //   * When a coarse plane completes, the 4 cells around a coarse vertex add their partial sums:
 //     along K by a warp shuffle, along J through a small shared-memory exchange (fixed order).
-// CTA = 5 cell rows x 32 cells (5 consumer warps) for a tile of 4 x 31 coarse vertices, plus one
-// producer warp: a 4-slot ring of rho planes (TMA box 100 x 17), a 3-slot ring of the steps' weight
+// CTA = 11 cell rows x 32 cells (11 consumer warps) for a tile of 10 x 31 coarse vertices, plus one
+// producer warp (12 warps of 168 registers: one CTA per SM): a 4-slot ring of rho planes (TMA box 100 x 17), a 3-slot ring of the steps' weight
 // slices and a 4-slot ring of the tile-plane tables (distinct dictionary rows of the tile's vertices in a
 // coarse plane + each vertex's index), completion on mbarriers.  The weights come from a sliced
 // copy of P's row dictionary (5 slices of 25 weights per row, one per fine plane offset, padded
 // to 26 doubles so that a slice is a 16-byte-aligned 208-byte bulk copy): a step stages only the
-// two slices it multiplies (<= 13 KB) instead of whole rows for three coarse planes (100 KB), so
-// two CTAs fit an SM.  Summation order differs from the oracle's o-major order (3D bar: 1e-10).
-// The kernel needs its 168 registers (12 warps per SM): tiles of 5 / 6 coarse rows (7 / 8 warps per
-// CTA, so 128 registers and 320 bytes of spills in the step loop) measured 2.98 / 3.12 ms against
-// 1.97 ms at config 5; three rho slots instead of four change nothing; the step unrolled by two with
+// two slices it multiplies (<= 20 KB) instead of whole rows for three coarse planes.  Summation
+// order differs from the oracle's o-major order (3D bar: 1e-10).
+// Tile height, measured at config 5 (the cells of a tile overlap the next tile's by one row): 4
+// coarse rows on two CTAs of 6 warps per SM 2.02 ms (77 % of the cell lanes own coarse vertices);
+// 10 rows on one CTA of 12 warps **1.84 ms** (88 %, 11 instead of 10 consumer warps per SM); 8 rows
+// on one CTA of 10 warps 2.09 ms.
+// The kernel needs its 168 registers (12 warps per SM): two CTAs of 7 / 8 warps per SM (128
+// registers, 320 bytes of spills in the step loop) measured 2.98 / 3.12 ms; three rho slots instead of four change nothing; the step unrolled by two with
 // the rho windows swapping roles (no copy of the window's centre, the sign of G folded into its
 // constants) 2.06 ms (20 bytes of spills).
 #include <cuda.h>
@@ -39,7 +42,8 @@
 
 namespace t3 {
 
-constexpr int kCK = 31, kCJ = 4;                   // coarse vertices per tile (K, J)
+constexpr int kCK = 31, kCJ = 10;                  // coarse vertices per tile (K, J)
+constexpr int kCPerSM = kCJ <= 4 ? 2 : 1;          // CTAs per SM (registers: 12 warps of 168)
 constexpr int kCCK = kCK + 1, kCCJ = kCJ + 1;      // cells per tile: 32 x 5
 constexpr int kCCons = 32 * kCCJ, kCThreads = kCCons + 32;
 // rho box: the cells' 98 x 17 fine window from (3K0 - 4, 3J0 - 4), widened to 100 columns so that
@@ -47,18 +51,19 @@ constexpr int kCCons = 32 * kCCJ, kCThreads = kCCons + 32;
 constexpr int kCW = 3 * kCCK + 4, kCH = 3 * kCCJ + 2;
 constexpr int kCRho = (kCW * kCH * 8 + 127) / 128 * 128 / 8;   // 1712 doubles
 constexpr int kCSl = 26;                           // doubles per weight slice (25 + pad)
-constexpr int kCRows = 32;                         // distinct rows per tile plane (cap)
+constexpr int kCRows = kCJ <= 4 ? 32 : 48;         // distinct rows per tile plane (cap)
+static_assert(kCRows <= 64, "the producer stages a row per lane in two passes");
 constexpr int kCWts = 2 * kCRows * kCSl;           // one step's slices: [coarse plane c | nx][row][26]
 constexpr int kCR = 4, kCWR = 3;                   // ring depths: rho planes, weight slice sets
 constexpr int kCNT = 4;                            // table ring (coarse planes)
-constexpr int kCTabBytes = 272;                    // {n, ids[32]} uint32, local[124] uint8 at byte 132
-constexpr int kCTabLoc = 132;
+constexpr int kCTabLoc = 4 + 4 * kCRows;           // {n, ids[kCRows]} uint32, then local[kCK * kCJ] uint8
+constexpr int kCTabBytes = (kCTabLoc + kCK * kCJ + 15) / 16 * 16;
 constexpr int oCWts = kCR * kCRho, oCTab = oCWts + kCWR * kCWts;
 constexpr int oCScr = oCTab + kCNT * kCTabBytes / 8;
 constexpr int kCScr = kCCJ * 32 * 2;               // one exchange buffer: [cell row][lane][field]
 constexpr size_t kSmcSmem = sizeof(double) * (oCScr + 2 * kCScr);
 static_assert(kCWts % 16 == 0 && kCRho % 16 == 0, "slots stay 128-byte aligned");
-static_assert(2 * (kSmcSmem + 1024) <= 227 * 1024, "two CTAs per SM");
+static_assert(kCPerSM * (kSmcSmem + 1024) <= 227 * 1024, "CTAs per SM");
 
 // P's row dictionary in slices: Pds[(id * 5 + si) * 26 + q] = Pd[id * kDictW + si * 25 + q]
 __global__ void k3_dict_slices(const double* __restrict__ pd, size_t rows, double* __restrict__ out) {
@@ -131,7 +136,7 @@ struct Smc {
 };
 
 template <bool JAC>
-__global__ void __launch_bounds__(kCThreads, 2) k3_smc(const __grid_constant__ Smc A) {
+__global__ void __launch_bounds__(kCThreads, kCPerSM) k3_smc(const __grid_constant__ Smc A) {
   extern __shared__ __align__(128) double sc[];
   __shared__ __align__(8) uint64_t full[kCR], done[kCR], wful[kCWR], wdone[kCWR], tful[kCNT];
   const int N = A.N, Nc = A.Nc, n = Nc - 2;
@@ -193,18 +198,22 @@ __global__ void __launch_bounds__(kCThreads, 2) k3_smc(const __grid_constant__ S
         issue_tab(m3 + 2);
       }
       int nc_ = 0, nn_ = 0;
-      uint32_t idc = 0u, idn = 0u;
+      uint32_t idc[2] = {0u, 0u}, idn[2] = {0u, 0u};  // a row per lane, two passes
       if (c) {
         twait(m3);
         const uint32_t* T = reinterpret_cast<const uint32_t*>(tab_of(m3));
         nc_ = (int)T[0];
-        if (lane < nc_) idc = T[1 + lane];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (lane + 32 * h < nc_) idc[h] = T[1 + lane + 32 * h];
       }
       if (nx) {
         twait(m3 + 1);
         const uint32_t* T = reinterpret_cast<const uint32_t*>(tab_of(m3 + 1));
         nn_ = (int)T[0];
-        if (lane < nn_) idn = T[1 + lane];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (lane + 32 * h < nn_) idn[h] = T[1 + lane + 32 * h];
       }
       double* wslot = sc + oCWts + wl * kCWts;
       if (lane == 0) {
@@ -215,10 +224,14 @@ __global__ void __launch_bounds__(kCThreads, 2) k3_smc(const __grid_constant__ S
         else mbar_arrive(&wful[wl]);
       }
       __syncwarp();
-      if (lane < nc_)
-        bulk_load(wslot + lane * kCSl, A.pds + ((size_t)idc * 5 + (o + 2)) * kCSl, 8 * kCSl, &wful[wl]);
-      if (lane < nn_)
-        bulk_load(wslot + (kCRows + lane) * kCSl, A.pds + ((size_t)idn * 5 + (o - 1)) * kCSl, 8 * kCSl, &wful[wl]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int q = lane + 32 * h;
+        if (q < nc_)
+          bulk_load(wslot + q * kCSl, A.pds + ((size_t)idc[h] * 5 + (o + 2)) * kCSl, 8 * kCSl, &wful[wl]);
+        if (q < nn_)
+          bulk_load(wslot + (kCRows + q) * kCSl, A.pds + ((size_t)idn[h] * 5 + (o - 1)) * kCSl, 8 * kCSl, &wful[wl]);
+      }
     }
     return;
   }
