@@ -17,6 +17,13 @@
 // copies (1.745 -> 1.88 ms: the kernel runs at the DRAM rate of its access pattern, 4.8 TB/s, and
 // the prefetches add traffic for row sets the stager would have kept).
 //
+// Also measured and dropped: the last four row sets cached in their slots (least recently used
+// replaced) with the steps of a J-tile column walked in blocks of 9 layers, up on even J tiles and
+// down on odd ones, so that the tiles inside a coefficient block meet the same low-face / interior
+// / high-face sets back to back (44 % fewer set loads by count): 1.78 ms against 1.75 ms -- the
+// cache alone costs 0.06 ms in plain order (lookup ahead of the commit does not recover it) and
+// the step coordinates no longer stay in uniform registers.
+//
 // Warp-specialised: warp 6 is the producer -- it keeps the three rings (slots,
 // tables, rows) ahead of the consumers, and after the consumers of a step have
 // arrived on its `done` barrier stores the step's u with one TMA store and
