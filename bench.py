@@ -470,6 +470,10 @@ def run_ours(args, dist: Dist):
             traffic = None
     roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None, "traffic": traffic,
+                # the same kernel by the DRAM bytes ncu measured for one launch (the plane-run
+                # coefficients / dictionaries move less than the algorithmic bytes)
+                "traffic_GBps": (traffic / (kms / kcnt * 1e-3) / 1e9) if traffic else None,
+                "traffic_frac": (traffic / (kms / kcnt * 1e-3) / 1e9 / peak) if traffic else None,
                 "algorithmic_bytes_per_launch": kbytes, "mean_launch_us": 1e3 * kms / kcnt,
                 "share_of_cycle": kms / total_prof, "peak_source": peak_src,
                 "cycle_B_alg": bm["cycle"],
