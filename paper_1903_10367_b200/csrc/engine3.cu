@@ -457,7 +457,10 @@ int launch_up_tma(Engine3* e, int l, const Up3& a) {
     D.I0 = A.I0;
     D.steps = (int)A.steps;
     D.per = (int)A.per;
-    if (!a.g) k3_up_dict<false, false><<<grid, kDThreads, DLay<false>::smem, e->s>>>(D);
+    D.snake = (D.nI % kDSnake == 0) ? 1 : 0;  // (a compile-time flavour of the kernel: as a run-time branch
+                                              // it pushes the step coordinates out of the uniform registers)
+    if (!a.g && D.snake) k3_up_dict<false, false, true><<<grid, kDThreads, DLay<false>::smem, e->s>>>(D);
+    else if (!a.g) k3_up_dict<false, false><<<grid, kDThreads, DLay<false>::smem, e->s>>>(D);
     else if (a.carry) k3_up_dict<true><<<grid, kDThreads, DLay<true>::smem, e->s>>>(D);
     else k3_up_dict<false><<<grid, kDThreads, DLay<true>::smem, e->s>>>(D);
   } else {
@@ -1114,6 +1117,8 @@ int build(Engine3* e, const tmg_tree3* t) {
   CK3(cudaFuncSetAttribute(k3_up_dict<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DLay<true>::smem));
   CK3(cudaFuncSetAttribute(k3_up_dict<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DLay<true>::smem));
   CK3(cudaFuncSetAttribute(k3_up_dict<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DLay<false>::smem));
+  CK3(cudaFuncSetAttribute(k3_up_dict<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)DLay<false>::smem));
   CK3(cudaFuncSetAttribute(k3_up_tma<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpTmaSmem));
   TRY3(alloc3(e, &e->deg, 1));
   e->thr_next = l0 - 1;

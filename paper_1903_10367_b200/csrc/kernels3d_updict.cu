@@ -17,12 +17,14 @@
 // copies (1.745 -> 1.88 ms: the kernel runs at the DRAM rate of its access pattern, 4.8 TB/s, and
 // the prefetches add traffic for row sets the stager would have kept).
 //
-// Also measured and dropped: the last four row sets cached in their slots (least recently used
-// replaced) with the steps of a J-tile column walked in blocks of 9 layers, up on even J tiles and
-// down on odd ones, so that the tiles inside a coefficient block meet the same low-face / interior
-// / high-face sets back to back (44 % fewer set loads by count): 1.78 ms against 1.75 ms -- the
-// cache alone costs 0.06 ms in plain order (lookup ahead of the commit does not recover it) and
-// the step coordinates no longer stay in uniform registers.
+// Step order (SNAKE, when the layer count is a multiple of 9): a column of J tiles is walked in
+// blocks of 9 layers, J tile after J tile inside a block, the layers up on even J tiles and down on
+// odd ones, so that the tiles inside one coefficient block meet the same low-face / interior /
+// high-face row sets back to back and the re-staged sets come from L2 instead of DRAM: 1.76 ->
+// 1.655 ms at config 5.  (A compile-time flavour: with the order as a run-time branch ptxas moves
+// the step coordinates out of the uniform registers and both orders lose 0.05 ms.  A cache of the
+// last four row sets in their slots on top of it -- least recently used replaced, 44 % fewer
+// set loads by count -- cost more in the stager than the L2 hits it saves: 1.78 ms.)
 //
 // Warp-specialised: warp 6 is the producer -- it keeps the three rings (slots,
 // tables, rows) ahead of the consumers, and after the consumers of a step have
@@ -40,6 +42,7 @@ namespace t3 {
 constexpr int kQRows = 32, kQRowS = 130;  // rows per step (cap), row stride in doubles (1040 B)
 constexpr int kQTabBytes = 256;           // {n, ids[kQRows]} uint32, local[64] uint8 at byte 132
 constexpr int kDNT = 8, kDTD = 6, kDNR = 4, kDRD = 3, kDPF = 4;
+constexpr int kDSnake = 9;  // layers per snake block (config 5's coefficient blocks are 9 cubes wide)
 static_assert(kDNR == kDRD + 1, "row sets: one per step in flight plus the one being staged");
 // consumers: 18 warps = the nine fine rows (ri, rj) of a cube on two warps each (64 cubes), three
 // fine vertices per thread -- with 6 warps (a cube's fine plane per thread) the consumers were busy
@@ -84,6 +87,7 @@ struct UpD {
   const double* dict;      // Pc rows dict[id * kDictW + q]
   const uint8_t* tab;      // step tables, index (I * tilesJ + J0 / 2) * tilesK + K0 / 32
   int tilesK, tilesJ, nI, I0, steps, per;
+  int snake;  // step order: 0 = a tile's layers upwards, tile after tile; else see coords()
 };
 
 // step tables: one thread per (layer I, J tile, K tile); *over = 1 when a step meets more than
@@ -152,7 +156,7 @@ __device__ __forceinline__ void tma_store_3d_ef(const CUtensorMap* map, const vo
 }
 
 // G = false: no g stream (the finest level's g is already in u, Engine3::pp)
-template <bool CARRY, bool G = true>
+template <bool CARRY, bool G = true, bool SNAKE = false>
 __global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant__ UpD A) {
   using LY = DLay<G>;
   constexpr int kDNS = LY::NS, kDSlot = LY::slot, oDU = LY::oU, oDG = LY::oG, oDC = LY::oC, oDTab = LY::oTab,
@@ -166,7 +170,23 @@ __global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant
   const int lt = threadIdx.x;
   const int s0 = blockIdx.x * A.per, s1 = min(A.steps, s0 + A.per);
   if (s0 >= s1) return;
+  // Step order.  Plain: a tile's layers upwards, tile after tile (K tiles fastest).  Snake (nI a
+  // multiple of kDSnake): a column of J tiles is walked in blocks of kDSnake layers -- inside a
+  // block J tile after J tile, the layers up on even J tiles and down on odd ones -- so that the
+  // tiles inside one coefficient block meet the same three row sets (low face, interior, high
+  // face) back to back and the stager's set cache serves them.
   auto coords = [&](int s, int& I, int& J0, int& K0) {  // 32-bit: steps < 2^31
+    if (SNAKE) {
+      const int colsteps = A.tilesJ * A.nI;
+      const int col = s / colsteps, q = s - col * colsteps;
+      const int blk = A.tilesJ * kDSnake;
+      const int ib = q / blk, r = q - ib * blk;
+      const int jt = r / kDSnake, li = r - jt * kDSnake;
+      I = A.I0 + ib * kDSnake + ((jt & 1) ? kDSnake - 1 - li : li);
+      J0 = jt * kQJ;
+      K0 = col * kQK;
+      return;
+    }
     const int t = s / A.nI;
     I = A.I0 + (s - t * A.nI);
     const int tj = t / A.tilesK;
@@ -288,18 +308,48 @@ __global__ void __launch_bounds__(kDThreads, 1) k3_up_dict(const __grid_constant
 
   // ---------------- consumers: warps 0-17, fine row (ri, rj) = warp / 2 ----------------
   const int rg = lt >> 6, cl = lt & 63, tx = cl & 31, ty = cl >> 5;
-  int I, J0, K0;  // coordinates of step s, advanced incrementally
-  coords(s0, I, J0, K0);
+  // step counters, advanced without divisions: (column of K tiles, layer block, J tile, layer in
+  // the block) in snake order, (J tile, K tile, layer) otherwise
+  int c_col, c_ib = 0, c_jt, c_li;
+  const int nIb = A.nI / kDSnake;
+  if (SNAKE) {
+    const int colsteps = A.tilesJ * A.nI, blk = A.tilesJ * kDSnake;
+    c_col = s0 / colsteps;
+    const int q = s0 - c_col * colsteps;
+    c_ib = q / blk;
+    const int r0 = q - c_ib * blk;
+    c_jt = r0 / kDSnake;
+    c_li = r0 - c_jt * kDSnake;
+  } else {
+    const int t = s0 / A.nI;
+    c_li = s0 - t * A.nI;
+    c_jt = t / A.tilesK;
+    c_col = t - c_jt * A.tilesK;
+  }
   for (int s = s0; s < s1; ++s) {
     const int r = s - s0;
-    if (s > s0 && ++I == A.I0 + A.nI) {
-      I = A.I0;
-      K0 += kQK;
-      if (K0 >= A.tilesK * kQK) {
-        K0 = 0;
-        J0 += kQJ;
+    if (s > s0) {
+      if (SNAKE) {
+        if (++c_li == kDSnake) {
+          c_li = 0;
+          if (++c_jt == A.tilesJ) {
+            c_jt = 0;
+            if (++c_ib == nIb) {
+              c_ib = 0;
+              ++c_col;
+            }
+          }
+        }
+      } else if (++c_li == A.nI) {
+        c_li = 0;
+        if (++c_col == A.tilesK) {
+          c_col = 0;
+          ++c_jt;
+        }
       }
     }
+    const int I = SNAKE ? A.I0 + c_ib * kDSnake + ((c_jt & 1) ? kDSnake - 1 - c_li : c_li) : A.I0 + c_li;
+    const int J0 = c_jt * kQJ, K0 = c_col * kQK;
     double* b = sq + (r % kDNS) * kDSlot;
     mbar_wait(&full[r % kDNS], (unsigned)(r / kDNS) & 1u);
     mbar_wait(&tful[r % kDNT], (unsigned)(r / kDNT) & 1u);
