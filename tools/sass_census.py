@@ -15,7 +15,7 @@ for line in sys.stdin:
         if m:
             cnt[cur][m.group(1).split(".")[0]] += 1
 want = ("k3_top4r", "k3_smc", "k3_smr", "k3_up_dict", "k3_up_tma", "k3_down_c", "k3_rap_y", "k3_rap_out", "k3_up_lin",
-        "k3_top2", "k_cycle")
+        "k3_top2", "k3_rle", "k3_chain", "k_cycle")
 ops = ("UTMALDG", "UTMASTG", "UTMAPF", "UBLKCP", "SYNCS", "DFMA", "DMUL", "DADD", "LDS", "STS", "LDG", "STG", "BAR")
 print(f"{'kernel':64s} " + " ".join(f"{o:>7s}" for o in ops))
 for k, c in cnt.items():
