@@ -959,14 +959,22 @@ int build_rle(Engine3* e, int l) {
   const size_t segs = (size_t)c.N * c.N * rseg;
   uint32_t *rmask = nullptr, *rcnt = nullptr, *rbase = nullptr;
   uint8_t* rdup = nullptr;
-  TRY3(alloc3(e, &rmask, segs, false));
-  TRY3(alloc3(e, &rbase, segs + 1, false));
+  CK3(cudaMalloc(&rmask, sizeof(uint32_t) * segs));
+  CK3(cudaMalloc(&rbase, sizeof(uint32_t) * (segs + 1)));
   CK3(cudaMalloc(&rcnt, sizeof(uint32_t) * (segs + 1)));
   void* tmp = nullptr;
+  bool keep = false;  // the masks and bases live on with the handle only when the table is kept
   auto done = [&](int rc) {
     cudaFree(rcnt);
     if (rdup) cudaFree(rdup);
     if (tmp) cudaFree(tmp);
+    if (keep) {
+      e->allocs.push_back(rmask);
+      e->allocs.push_back(rbase);
+    } else {
+      cudaFree(rmask);
+      cudaFree(rbase);
+    }
     return rc;
   };
 #define CKR(x)                                                                  \
@@ -996,6 +1004,7 @@ int build_rle(Engine3* e, int l) {
   else k3_rle_link<<<nblk((size_t)c.N * rseg, 128), 128, 0, e->s>>>(c.N, rseg, rdup, rbase);
   if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(e->s) != cudaSuccess)
     return done(fail3(e, TMG_ECUDA, "k3_rle_fill failed"));
+  keep = true;
   c.op.rtab = rtab;
   c.op.rbase = rbase;
   c.op.rmask = rmask;

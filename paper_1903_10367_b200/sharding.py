@@ -453,6 +453,7 @@ class ShardedEngine3:
     def run(self, n: int):
         for _ in range(n):
             self.cycle()
+        self.sync_halos()  # leave the iterate's halo planes current
         return self.shards[0].history(n)
 
     # -- the cycle as CUDA graphs (one process per GPU) -----------------------------------

@@ -125,9 +125,10 @@ def test_3d_fixture_history_and_iterate(name):
         st = eng.weight_storage(wl.tree.depth - 1)
         assert 0 < st["p_distinct"] <= st["p_rows"] // 4, st
         assert 0 < st["pc_distinct"] <= st["pc_rows"] // 4, st
+        assert 0 < st["galerkin_stored"] <= st["galerkin_rows"] // 2, st  # run-length Galerkin rows
     if name == "random-L5":  # per-cell coefficients: the dense weight streams
         st = eng.weight_storage(wl.tree.depth - 1)
-        assert st["p_distinct"] == 0 and st["pc_distinct"] == 0, st
+        assert st["p_distinct"] == 0 and st["pc_distinct"] == 0 and st["galerkin_stored"] == 0, st
     np.testing.assert_allclose([s.l2h for s in h], z["l2h"], rtol=RTOL)
     np.testing.assert_allclose([s.linf for s in h], z["linf"], rtol=RTOL)
     s = meta["stride"]
@@ -187,6 +188,8 @@ def test_3d_rebuild_after_shard_is_unsharded():
     eng.rebuild()
     with pytest.raises(ValueError, match="not sharded"):
         _abi.check(L.tmg3_phase(eng._h, _abi.PH_DOWN, 3))
+    with pytest.raises(ValueError, match="DOWN and UP only"):
+        _abi.check(L.tmg3_phase_range(eng._h, _abi.PH_REDUCE, 3, 1, 5, 1, 1))
     h2 = eng.advance_many(2)
     np.testing.assert_allclose([s.l2h for s in h2], [s.l2h for s in h1], rtol=1e-13)
 
