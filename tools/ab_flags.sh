@@ -1,5 +1,5 @@
 #!/bin/bash
-# A/B of compile-time variants on one box:  bash tools/ab_flags.sh config5 "" "-DT4_S=4 -DT4_A=2" ...
+# A/B of compile-time variants on one box:  bash tools/ab_flags.sh config5 "" "-DCYC_MINB=2" ...
 # (each argument after the workload is a TMG_NVCC_FLAGS value; prints cycle and per-kernel ms)
 mkdir -p gpurun_out
 W=$1; shift
