@@ -19,7 +19,7 @@
 //   * When a coarse plane completes, the 4 cells around a coarse vertex add their partial sums:
 //     along K by a warp shuffle, along J through a small shared-memory exchange (fixed order).
 // CTA = 11 cell rows x 32 cells (11 consumer warps) for a tile of 10 x 31 coarse vertices, plus one
-// producer warp (12 warps of 168 registers: one CTA per SM): a 4-slot ring of rho planes (TMA box 100 x 17), a 3-slot ring of the steps' weight
+// producer warp (12 warps of 168 registers: one CTA per SM): a 4-slot ring of rho planes (TMA box 100 x 35), a 4-slot ring of the steps' weight
 // slices and a 4-slot ring of the tile-plane tables (distinct dictionary rows of the tile's vertices in a
 // coarse plane + each vertex's index), completion on mbarriers.  The weights come from a sliced
 // copy of P's row dictionary (5 slices of 25 weights per row, one per fine plane offset, padded
@@ -31,7 +31,7 @@
 // 10 rows on one CTA of 12 warps **1.84 ms** (88 %, 11 instead of 10 consumer warps per SM); 8 rows
 // on one CTA of 10 warps 2.09 ms.
 // The kernel needs its 168 registers (12 warps per SM): two CTAs of 7 / 8 warps per SM (128
-// registers, 320 bytes of spills in the step loop) measured 2.98 / 3.12 ms; three rho slots instead of four change nothing; the step unrolled by two with
+// registers, 320 bytes of spills in the step loop) measured 2.98 / 3.12 ms; rho / weight rings of 4 / 3, 5 / 3, 3 / 4 slots measured 1.84 / 1.86 / 1.87 ms against 1.82 ms for 4 / 4; the step unrolled by two with
 // the rho windows swapping roles (no copy of the window's centre, the sign of G folded into its
 // constants) 2.06 ms (20 bytes of spills).
 #include <cuda.h>
@@ -54,7 +54,7 @@ constexpr int kCSl = 26;                           // doubles per weight slice (
 constexpr int kCRows = kCJ <= 4 ? 32 : 48;         // distinct rows per tile plane (cap)
 static_assert(kCRows <= 64, "the producer stages a row per lane in two passes");
 constexpr int kCWts = 2 * kCRows * kCSl;           // one step's slices: [coarse plane c | nx][row][26]
-constexpr int kCR = 4, kCWR = 3;                   // ring depths: rho planes, weight slice sets
+constexpr int kCR = 4, kCWR = 4;                   // ring depths: rho planes, weight slice sets
 constexpr int kCNT = 4;                            // table ring (coarse planes)
 constexpr int kCTabLoc = 4 + 4 * kCRows;           // {n, ids[kCRows]} uint32, then local[kCK * kCJ] uint8
 constexpr int kCTabBytes = (kCTabLoc + kCK * kCJ + 15) / 16 * 16;
