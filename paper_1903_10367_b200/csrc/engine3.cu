@@ -684,7 +684,9 @@ int enqueue_down(Engine3* e, bool write) {
       a.chunk = c.s2_chunk;
       cudaEvent_t e0_ = nullptr;
       TRY3(begin_k(e, &e0_));
-      if (c.op.kind == OP_CONST) k3_top2<OP_CONST><<<c.s2_blocks, dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
+      if (c.op.kind == OP_CONST && a.use_tma && a.rhs_tma)
+        k3_top4c<<<c.s2_blocks, dim3(kSX, k2Y / kT4R), kTop4cSmem, e->s>>>(a);
+      else if (c.op.kind == OP_CONST) k3_top2<OP_CONST><<<c.s2_blocks, dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
       else if (use_top4(a)) k3_top4r<<<c.s2_blocks, dim3(kSX, k2Y / kT4R), kTop4rSmem, e->s>>>(a);
       else k3_top2<OP_ELEMENT><<<c.s2_blocks, dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
       CKL3();
@@ -1120,6 +1122,7 @@ int build(Engine3* e, const tmg_tree3* t) {
   CK3(cudaFuncSetAttribute(k3_top2<OP_CONST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2TopSmem));
   CK3(cudaFuncSetAttribute(k3_top2<OP_ELEMENT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2TopSmem));
   CK3(cudaFuncSetAttribute(k3_top4r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTop4rSmem));
+  CK3(cudaFuncSetAttribute(k3_top4c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTop4cSmem));
   CK3(cudaFuncSetAttribute(k3_smooth2r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2RSmemV));
   CK3(cudaFuncSetAttribute(k3_up_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpTmaSmem));
   CK3(cudaFuncSetAttribute(k3_up_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpTmaSmem));
@@ -1406,7 +1409,9 @@ int phase3(Engine3* e, int phase, int l) {
         e->top_parts += blocks;
         cudaEvent_t e0_ = nullptr;
         TRY3(begin_k(e, &e0_));
-        if (c.op.kind == OP_CONST)
+        if (c.op.kind == OP_CONST && a.use_tma && a.rhs_tma)
+          k3_top4c<<<blocks, dim3(kSX, k2Y / kT4R), kTop4cSmem, e->s>>>(a);
+        else if (c.op.kind == OP_CONST)
           k3_top2<OP_CONST><<<blocks, dim3(kSX, k2Y / 2), k2TopSmem, e->s>>>(a);
         else if (use_top4(a))
           k3_top4r<<<blocks, dim3(kSX, k2Y / kT4R), kTop4rSmem, e->s>>>(a);

@@ -205,4 +205,130 @@ __global__ void __launch_bounds__(kT4B, 2) k3_top4r(const __grid_constant__ Top3
   }
 }
 
+// The constant-coefficient flavour (config 3, OP_CONST): the same ring and register window without
+// the cell planes.  The 27-point row is m at the centre, -se on the 12 edge and -sc on the 8 corner
+// neighbours (0 on the faces), so a plane contributes through two sums per vertex: PE, its four
+// in-plane axis neighbours, and PD, its four in-plane diagonals --
+//   A u = m x - se (PE(i-1) + PE(i+1) + PD(i)) - sc (PD(i-1) + PD(i+1)).
+// A plane's sums are formed once when it arrives (6 additions per vertex) and serve three vertex
+// planes; k3_top2<OP_CONST> re-read all three planes from shared memory (18 loads and 26 additions
+// per vertex).  Summation order differs from mg3d.apply_const's (3D bar: 1e-10).
+constexpr size_t kTop4cSmem = sizeof(double) * kT4S * (k2SlotU + k2SlotR);
+
+__global__ void __launch_bounds__(kT4B, 2) k3_top4c(const __grid_constant__ Top3 a) {
+  extern __shared__ __align__(128) double dyn4c[];
+  __shared__ uint64_t bars[kT4S];
+  auto us = reinterpret_cast<double(*)[k2SlotU]>(dyn4c);
+  auto rs = reinterpret_cast<double(*)[k2SlotR]>(dyn4c + kT4S * k2SlotU);
+  const Column2 col(a.N, a.ilo, a.ihi, a.chunk);
+  const int N = a.N;
+  const size_t NN = (size_t)N * N;
+  const int tx = threadIdx.x, jj = kT4R * threadIdx.y;
+  const int k = col.k0 + tx, j = col.j0 + jj;
+  const size_t col_off = (size_t)j * N + k;
+  const int ia = col.ia, ib = col.ib;
+  const bool live = k <= N - 2 && j <= N - 2;
+  double s = 0.0, mx = 0.0;
+  if (col.lt == 0) {
+    for (int q = 0; q < kT4S; ++q) mbar_init(&bars[q], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int last = ib - ia + 1;
+  auto issue = [&](int g) {  // packet g = {u plane ia - 1 + g, rhs plane ia - 2 + g}
+    if (g > last) return;
+    const int sl = g % kT4S, pu = ia - 1 + g;
+    mbar_expect_tx(&bars[sl], k2BoxBytes + 8u * k2SlotR);
+    tma_load_3d(us[sl], &a.tm, &bars[sl], col.k0 - 1, col.j0 - 1, pu);
+    tma_load_3d(rs[sl], &a.tmr, &bars[sl], col.k0 - 1, col.j0, pu - 1);
+  };
+  auto refill = [&](int g) {
+    __syncthreads();
+    if (col.lt == 0) {
+      fence_proxy_async();
+      issue(g + kT4S);
+    }
+  };
+  if (col.lt == 0)
+    for (int g = 0; g < kT4S; ++g) issue(g);
+  // per vertex aa: (PE, PD) of the plane below, of the own plane, and the own centre
+  double pem[kT4R], pdm[kT4R], pe0[kT4R], pd0[kT4R], xc[kT4R];
+  auto sums = [&](int sl, double* pe, double* pd, double* ctr) {
+    double w[(kT4R + 2) * 3];
+#pragma unroll
+    for (int r = 0; r < kT4R + 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) w[r * 3 + c] = us[sl][(jj + r) * k2RowU + tx + c];
+#pragma unroll
+    for (int aa = 0; aa < kT4R; ++aa) {
+      pe[aa] = (w[aa * 3 + 1] + w[(aa + 2) * 3 + 1]) + (w[(aa + 1) * 3] + w[(aa + 1) * 3 + 2]);
+      pd[aa] = (w[aa * 3] + w[aa * 3 + 2]) + (w[(aa + 2) * 3] + w[(aa + 2) * 3 + 2]);
+      ctr[aa] = w[(aa + 1) * 3 + 1];
+    }
+  };
+  double dump[kT4R];
+  mbar_wait(&bars[0], 0u);
+  sums(0, pem, pdm, dump);
+  mbar_wait(&bars[1], 0u);
+  sums(1, pe0, pd0, xc);
+  refill(0);
+  refill(1);
+  const double m = a.op.m, se = a.op.se, sc = a.op.sc, dg = a.op.cdiag;
+  int sl = 2 % kT4S;
+  unsigned par = 0u;
+  for (int i = ia; i < ib; ++i) {
+    const int g = i - ia + 2;
+    mbar_wait(&bars[sl], par);
+    double pep[kT4R], pdp[kT4R], xp[kT4R], rhs[kT4R];
+    sums(sl, pep, pdp, xp);
+#pragma unroll
+    for (int aa = 0; aa < kT4R; ++aa) rhs[aa] = rs[sl][(jj + aa) * k2RowR + tx + 1];
+    refill(g);
+    if (++sl == kT4S) {
+      sl = 0;
+      par ^= 1u;
+    }
+    if (live) {
+#pragma unroll
+      for (int aa = 0; aa < kT4R; ++aa) {
+        if (j + aa > N - 2) continue;
+        const double SE = (pem[aa] + pep[aa]) + pd0[aa];
+        const double SC = pdm[aa] + pdp[aa];
+        const double au = (m * xc[aa] - se * SE) - sc * SC;
+        const double rho = rhs[aa] - au;
+        const double t = a.hw * rho;
+        s = s + t * t;
+        mx = fmax(mx, fabs(rho));
+        const size_t v = (size_t)i * NN + col_off + (size_t)aa * N;
+        const double gv = div_pos(a.w * rho, dg);
+        if (a.u_out) a.u_out[v] = xc[aa] + gv;
+        else a.g[v] = gv;
+        if (a.rho) a.rho[v] = rho;
+      }
+    }
+#pragma unroll
+    for (int aa = 0; aa < kT4R; ++aa) {
+      pem[aa] = pe0[aa];
+      pdm[aa] = pd0[aa];
+      pe0[aa] = pep[aa];
+      pd0[aa] = pdp[aa];
+      xc[aa] = xp[aa];
+    }
+  }
+  __shared__ double red_s[kT4B / 32], red_m[kT4B / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_down_sync(0xffffffffu, s, o);
+    mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+  }
+  const int lt = threadIdx.y * kT4X + threadIdx.x;
+  if ((lt & 31) == 0) { red_s[lt >> 5] = s; red_m[lt >> 5] = mx; }
+  __syncthreads();
+  if (lt == 0) {
+    double A = 0.0, B = 0.0;
+    for (int q = 0; q < kT4B / 32; ++q) { A += red_s[q]; B = fmax(B, red_m[q]); }
+    a.part_sum[blockIdx.x] = A;
+    a.part_max[blockIdx.x] = B;
+  }
+}
+
 }  // namespace t3
