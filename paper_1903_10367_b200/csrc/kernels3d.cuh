@@ -36,10 +36,12 @@ constexpr double C_D8 = 8.0 / 3.0;
 constexpr double C_E6 = 1.0 / 6.0;
 constexpr double C_C12 = 1.0 / 12.0;
 
-// a / b for a normal, positive b (Jacobi diagonals): hardware reciprocal seed (2^-23), one Newton
+// a / b for a positive b (Jacobi diagonals): hardware reciprocal seed (2^-23), one Newton
 // step, the quotient corrected with its exact FMA residual -- 5 fp64 instructions against the 9 +
 // special-case branch of the IEEE sequence, within an ulp of it (the 3D bar is relative 1e-10).
 __device__ __forceinline__ double div_pos(double a, double b) {
+  // the seed flushes denormals and overflows near the ends of the exponent range: IEEE division there
+  if (!(b > 1e-290 && b < 1e290)) return a / b;
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
   r = fma(fma(-b, r, 1.0), r, r);
