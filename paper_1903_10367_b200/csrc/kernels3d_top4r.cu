@@ -11,7 +11,8 @@
 // ~27 fp64 operations per vertex instead of element_ET's 42, 2.69 -> 2.47 ms at config 5.
 // Measured alternatives: four rows at 3 x 128 threads (168 registers, 388 bytes of spills) 3.16 ms,
 // at 2 x 128 threads (206 registers) 3.03 ms; warps decoupled by per-slot empty barriers instead of
-// the per-step __syncthreads 0.04 ms slower.
+// the per-step __syncthreads 0.04 ms slower; an L2 prefetch of the u / rhs boxes 2 / 4 packets ahead
+// of the ring 0.09 / 0.10 ms slower.
 #include "kernels3d.cuh"
 
 namespace t3 {
