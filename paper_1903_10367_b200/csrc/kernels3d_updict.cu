@@ -26,6 +26,9 @@
 // last four row sets in their slots on top of it -- least recently used replaced, 44 % fewer
 // set loads by count -- cost more in the stager than the L2 hits it saves: 1.78 ms.)
 //
+// The streamed boxes are L2-prefetched kDPF = 4 steps ahead of their TMA loads: 0 / 2 / 4 / 8 steps
+// measured 1.85 / 1.655 / 1.64 / 1.69 ms.
+//
 // Warp-specialised: warp 6 is the producer -- it keeps the three rings (slots,
 // tables, rows) ahead of the consumers, and after the consumers of a step have
 // arrived on its `done` barrier stores the step's u with one TMA store and
